@@ -1,0 +1,136 @@
+/*
+ * hybridwave_b200 — C ABI of the sm_100a DG acoustic right-hand side and
+ * time update (drop-in for the hot path of the reference Python package
+ * `hybridwave`, which has no native layer of its own: the Python
+ * `Discretization.compute_rhs` / `timeint` entry points are what these
+ * symbols replace; see INTEGRATION.md for the ctypes binding).
+ *
+ * Conventions
+ *   - every pointer is a device pointer owned by the caller; the library
+ *     never allocates device memory;
+ *   - per-type state buffers are element-major (K, 4, Np) with fields
+ *     (p, u1, u2, u3), Np and node/mode order exactly the reference's
+ *     (hybridwave/dg.py:10-13, basis.py:151-155, 289-292, 348-352, 423-429);
+ *   - type slots: 0 hex, 1 wedge, 2 pyramid, 3 tet (hybridwave/refelem.py:35);
+ *   - return value 0 = success; nonzero = error, message via hw_last_error()
+ *     (the Python layer raises ValueError, matching the reference's
+ *     exceptions-only error model).
+ */
+#ifndef HYBRIDWAVE_B200_H
+#define HYBRIDWAVE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { HW_HEX = 0, HW_WEDGE = 1, HW_PYRAMID = 2, HW_TET = 3, HW_NTYPES = 4 };
+enum { HW_F64 = 0, HW_F32 = 1 };
+enum { HW_FORM_STRONG = 0, HW_FORM_SKEW = 1 };
+enum { HW_GL = 0, HW_SEM = 1 };
+
+/* nbr_code bit layout (one int32 per element face) */
+#define HW_NBR_TYPE(c) ((c) & 3)
+#define HW_NBR_FACE(c) (((c) >> 2) & 7)
+#define HW_NBR_PERM(c) (((c) >> 5) & 15)
+#define HW_NBR_BOUNDARY 0x200
+
+/* One element type present in the mesh.  Geometry record per element
+ * (scalar type = dtype):
+ *   hex      24: the 8 vertices (x, y, z)
+ *   wedge    30: G[3][3] (G[c][x] = d r_c / d x_x), 1/sqrt(J), then per face
+ *                (n_x, n_y, n_z, Js/sqrt(J))
+ *   pyramid  29: G[3][3], then per face (n_x, n_y, n_z, Js/J)
+ *   tet      25: G[3][3], then per face (n_x, n_y, n_z, Js/J)
+ * mat: per element (kappa, 1/rho, rho*c, 0).
+ * op/iop: constant operators, layouts documented in
+ *   paper_1507_02557_b200/dg.py (_pack_type_operators). */
+typedef struct {
+  int64_t K;
+  const void* geo;
+  const void* mat;
+  const int32_t* nbr_elem;   /* (K, nfaces) neighbour element index        */
+  const int32_t* nbr_code;   /* (K, nfaces) packed type/face/perm/boundary */
+  const void* op[10];
+  const int32_t* iop[4];
+  int32_t form;              /* HW_FORM_STRONG or HW_FORM_SKEW            */
+  int32_t pad_;
+} hw_type_t;
+
+typedef struct {
+  int32_t N;
+  int32_t dtype;             /* HW_F64 / HW_F32                           */
+  int32_t formulation;       /* HW_GL / HW_SEM                            */
+  int32_t pad_;
+  double penalty_scale;      /* hybridwave/dg.py:341-342                  */
+  const int32_t* perm_tri;   /* (6, (N+1)(N+2)/2) face-point permutations */
+  const int32_t* perm_quad;  /* (8, (N+1)^2)                              */
+  hw_type_t t[HW_NTYPES];
+} hw_mesh_t;
+
+/* per-type buffers, NULL for absent types */
+typedef struct {
+  void* p[HW_NTYPES];
+} hw_fields_t;
+
+/* optional per-type element subsets (multi-rate: active levels only);
+ * n[t] < 0 means "all elements of type t" */
+typedef struct {
+  const int32_t* idx[HW_NTYPES];
+  int64_t n[HW_NTYPES];
+} hw_subset_t;
+
+/* dU/dtau = diag(kappa, 1/rho) M^-1 (A U) — replaces
+ * Discretization.compute_rhs (hybridwave/dg.py:492-506, forcing = None). */
+int hw_rhs(const hw_mesh_t* mesh, const hw_fields_t* q, hw_fields_t* rhs,
+           const hw_subset_t* subset, void* stream);
+
+/* One low-storage RK stage (Carpenter-Kennedy (4,5), 2N storage):
+ *   res = a*res + dt*rhs(q_in);  q_out = q_in + b*res.
+ * q_in and q_out must be distinct (neighbours read q_in). */
+int hw_lsrk_stage(const hw_mesh_t* mesh, const hw_fields_t* q_in,
+                  hw_fields_t* q_out, hw_fields_t* res, double a, double b,
+                  double dt, const hw_subset_t* subset, void* stream);
+
+/* One Adams-Bashforth step with n_hist (1..3) slopes — replaces
+ * ab3_step(single_rate_run) (hybridwave/timeint.py:41-72):
+ *   h0 = rhs(q_in);  q_out = q_in + dt*(c0*h0 + c1*h1 + c2*h2). */
+int hw_ab_step(const hw_mesh_t* mesh, const hw_fields_t* q_in,
+               hw_fields_t* q_out, hw_fields_t* h0, const hw_fields_t* h1,
+               const hw_fields_t* h2, int n_hist, double c0, double c1,
+               double c2, double dt, const hw_subset_t* subset, void* stream);
+
+/* Multi-rate AB3 support (hybridwave/timeint.py:111-173):
+ * out = q + dt_lev * (c0*h0 + c1*h1 + c2*h2) on the listed elements of
+ * every type (the dense-output "effective state" of non-stepping levels and
+ * the per-level state update). */
+int hw_axpy3(const hw_mesh_t* mesh, const hw_fields_t* q, hw_fields_t* out,
+             const hw_fields_t* h0, const hw_fields_t* h1,
+             const hw_fields_t* h2, int n_hist, double c0, double c1,
+             double c2, double dt, const hw_subset_t* subset, void* stream);
+
+/* history shift on the listed elements: h2 <- h1, h1 <- h0, h0 <- rhs */
+int hw_hist_push(const hw_mesh_t* mesh, hw_fields_t* h0, hw_fields_t* h1,
+                 hw_fields_t* h2, const hw_fields_t* rhs,
+                 const hw_subset_t* subset, void* stream);
+
+/* Pack partition-interface state for the halo exchange: for each listed
+ * element, copy its (4, Np) state into the contiguous send buffer. */
+int hw_halo_pack(const hw_mesh_t* mesh, int elem_type, const void* q,
+                 const int32_t* idx, int64_t n, void* sendbuf, void* stream);
+
+/* Sum of U^T M U with material weights per type (discrete_energy,
+ * hybridwave/dg.py:655-674); writes one double per type slot to out[4]. */
+int hw_energy(const hw_mesh_t* mesh, const hw_fields_t* q, double* out,
+              void* stream);
+
+const char* hw_last_error(void);
+int hw_version(void);
+/* the N values compiled into this library (bit N set) */
+int hw_supported_orders(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

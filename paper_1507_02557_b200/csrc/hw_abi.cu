@@ -1,0 +1,334 @@
+// C ABI of the sm_100a DG acoustic hot path (see include/hybridwave_b200.h).
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "hw_kernels.cuh"
+
+namespace hw {
+
+static thread_local std::string g_err;
+
+static int fail(const char* msg) {
+  g_err = msg;
+  return 1;
+}
+
+static int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    g_err = std::string(what) + ": " + cudaGetErrorString(e);
+    return 2;
+  }
+  return 0;
+}
+
+template <typename KernelT>
+static int set_smem(KernelT kernel, size_t bytes) {
+  if (bytes > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)bytes);
+    if (e != cudaSuccess) {
+      g_err = std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e);
+      return 3;
+    }
+  }
+  return 0;
+}
+
+static void subset_of(const hw_subset_t* sub, int t, int64_t K, const int32_t** list,
+                      int64_t* n) {
+  *list = nullptr;
+  *n = K;
+  if (sub && sub->n[t] >= 0) {
+    *list = sub->idx[t];
+    *n = sub->n[t];
+  }
+}
+
+template <int N, typename R>
+static int launch_rhs_all(const hw_mesh_t& M, const hw_fields_t& Q, const Epi& E,
+                          const hw_subset_t* sub, cudaStream_t st) {
+  int rc;
+  for (int t = 0; t < HW_NTYPES; ++t) {
+    const int64_t K = M.t[t].K;
+    if (K <= 0) continue;
+    const int32_t* list;
+    int64_t n;
+    subset_of(sub, t, K, &list, &n);
+    if (n <= 0) continue;
+    switch (t) {
+      case HW_HEX: {
+        using K_ = HexK<N, R>;
+        const size_t smem = sizeof(R) * K_::SMEM;
+        if ((rc = set_smem(hex_kernel<N, R>, smem))) return rc;
+        hex_kernel<N, R><<<(unsigned)((n + K_::EPB - 1) / K_::EPB), NT, smem, st>>>(M, Q, E, list, n);
+        if ((rc = check_launch("hex_kernel"))) return rc;
+        break;
+      }
+      case HW_WEDGE: {
+        using K_ = WedgeK<N, R>;
+        const size_t smem = sizeof(R) * K_::SMEM;
+        if ((rc = set_smem(wedge_kernel<N, R>, smem))) return rc;
+        wedge_kernel<N, R><<<(unsigned)((n + K_::EPB - 1) / K_::EPB), NT, smem, st>>>(M, Q, E, list, n);
+        if ((rc = check_launch("wedge_kernel"))) return rc;
+        break;
+      }
+      case HW_PYRAMID: {
+        using K_ = PyrK<N, R>;
+        const size_t smem = sizeof(R) * K_::SMEM;
+        if ((rc = set_smem(pyr_kernel<N, R>, smem))) return rc;
+        pyr_kernel<N, R><<<(unsigned)((n + K_::EPB - 1) / K_::EPB), NT, smem, st>>>(M, Q, E, list, n);
+        if ((rc = check_launch("pyr_kernel"))) return rc;
+        break;
+      }
+      case HW_TET: {
+        using K_ = TetK<N, R>;
+        const size_t smem = sizeof(R) * K_::SMEM;
+        if ((rc = set_smem(tet_kernel<N, R>, smem))) return rc;
+        tet_kernel<N, R><<<(unsigned)((n + K_::EPB - 1) / K_::EPB), NT, smem, st>>>(M, Q, E, list, n);
+        if ((rc = check_launch("tet_kernel"))) return rc;
+        break;
+      }
+    }
+  }
+  return 0;
+}
+
+#ifndef HW_MAX_ORDER
+#define HW_MAX_ORDER 7
+#endif
+
+template <typename R>
+static int dispatch_rhs(const hw_mesh_t& M, const hw_fields_t& Q, const Epi& E,
+                        const hw_subset_t* sub, cudaStream_t st) {
+  switch (M.N) {
+    case 1: return launch_rhs_all<1, R>(M, Q, E, sub, st);
+    case 2: return launch_rhs_all<2, R>(M, Q, E, sub, st);
+    case 3: return launch_rhs_all<3, R>(M, Q, E, sub, st);
+    case 4: return launch_rhs_all<4, R>(M, Q, E, sub, st);
+    case 5: return launch_rhs_all<5, R>(M, Q, E, sub, st);
+#if HW_MAX_ORDER >= 6
+    case 6: return launch_rhs_all<6, R>(M, Q, E, sub, st);
+#endif
+#if HW_MAX_ORDER >= 7
+    case 7: return launch_rhs_all<7, R>(M, Q, E, sub, st);
+#endif
+    default: return fail("polynomial order not compiled into this library");
+  }
+}
+
+static int run_rhs(const hw_mesh_t* M, const hw_fields_t* Q, const Epi& E,
+                   const hw_subset_t* sub, void* stream) {
+  if (!M || !Q) return fail("null mesh or fields");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (M->dtype == HW_F64) return dispatch_rhs<double>(*M, *Q, E, sub, st);
+  if (M->dtype == HW_F32) return dispatch_rhs<float>(*M, *Q, E, sub, st);
+  return fail("unknown dtype");
+}
+
+// ---------------------------------------------------------------- elementwise
+
+template <typename R>
+__global__ void axpy3_kernel(const R* __restrict__ q, R* __restrict__ out, const R* __restrict__ h0,
+                             const R* __restrict__ h1, const R* __restrict__ h2, int nh, R c0,
+                             R c1, R c2, R dt, const int32_t* __restrict__ list, int64_t n,
+                             int chunk) {
+  const int64_t total = n * chunk;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t w = i / chunk;
+    const int r = (int)(i - w * chunk);
+    const size_t idx = (size_t)(list ? list[w] : w) * chunk + r;
+    R acc = c0 * h0[idx];
+    if (nh > 1) acc += c1 * h1[idx];
+    if (nh > 2) acc += c2 * h2[idx];
+    out[idx] = q[idx] + dt * acc;
+  }
+}
+
+template <typename R>
+__global__ void hist_push_kernel(R* __restrict__ h0, R* __restrict__ h1, R* __restrict__ h2,
+                                 const R* __restrict__ rhs, const int32_t* __restrict__ list,
+                                 int64_t n, int chunk) {
+  const int64_t total = n * chunk;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t w = i / chunk;
+    const int r = (int)(i - w * chunk);
+    const size_t idx = (size_t)(list ? list[w] : w) * chunk + r;
+    h2[idx] = h1[idx];
+    h1[idx] = h0[idx];
+    h0[idx] = rhs[idx];
+  }
+}
+
+template <typename R>
+__global__ void pack_kernel(const R* __restrict__ q, const int32_t* __restrict__ idx, int64_t n,
+                            int chunk, R* __restrict__ out) {
+  const int64_t total = n * chunk;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t w = i / chunk;
+    const int r = (int)(i - w * chunk);
+    out[i] = q[(size_t)idx[w] * chunk + r];
+  }
+}
+
+static int np_of(int t, int N) {
+  switch (t) {
+    case HW_HEX: return (N + 1) * (N + 1) * (N + 1);
+    case HW_WEDGE: return (N + 1) * (N + 1) * (N + 2) / 2;
+    case HW_PYRAMID: return (N + 1) * (N + 2) * (2 * N + 3) / 6;
+    default: return (N + 1) * (N + 2) * (N + 3) / 6;
+  }
+}
+
+static unsigned grid_for(int64_t total) {
+  int64_t g = (total + 255) / 256;
+  if (g > 148 * 32) g = 148 * 32;
+  return (unsigned)(g > 0 ? g : 1);
+}
+
+}  // namespace hw
+
+using namespace hw;
+
+extern "C" {
+
+int hw_version(void) { return 1; }
+
+int hw_supported_orders(void) {
+  int m = 0;
+  for (int n = 1; n <= HW_MAX_ORDER; ++n) m |= 1 << n;
+  return m;
+}
+
+const char* hw_last_error(void) { return g_err.c_str(); }
+
+int hw_rhs(const hw_mesh_t* mesh, const hw_fields_t* q, hw_fields_t* rhs,
+           const hw_subset_t* subset, void* stream) {
+  if (!rhs) return fail("null rhs");
+  Epi E;
+  memset(&E, 0, sizeof(E));
+  E.mode = MODE_RHS;
+  for (int t = 0; t < HW_NTYPES; ++t) E.out[t] = rhs->p[t];
+  return run_rhs(mesh, q, E, subset, stream);
+}
+
+int hw_lsrk_stage(const hw_mesh_t* mesh, const hw_fields_t* q_in, hw_fields_t* q_out,
+                  hw_fields_t* res, double a, double b, double dt, const hw_subset_t* subset,
+                  void* stream) {
+  if (!q_out || !res) return fail("null q_out/res");
+  Epi E;
+  memset(&E, 0, sizeof(E));
+  E.mode = MODE_LSRK;
+  E.a = a;
+  E.b = b;
+  E.dt = dt;
+  for (int t = 0; t < HW_NTYPES; ++t) {
+    if (mesh->t[t].K > 0 && q_in->p[t] == q_out->p[t]) return fail("q_in and q_out must differ");
+    E.res[t] = res->p[t];
+    E.qout[t] = q_out->p[t];
+  }
+  return run_rhs(mesh, q_in, E, subset, stream);
+}
+
+int hw_ab_step(const hw_mesh_t* mesh, const hw_fields_t* q_in, hw_fields_t* q_out,
+               hw_fields_t* h0, const hw_fields_t* h1, const hw_fields_t* h2, int n_hist,
+               double c0, double c1, double c2, double dt, const hw_subset_t* subset,
+               void* stream) {
+  if (n_hist < 1 || n_hist > 3) return fail("history depth must be 1..3");
+  Epi E;
+  memset(&E, 0, sizeof(E));
+  E.mode = MODE_AB;
+  E.nhist = n_hist;
+  E.c0 = c0;
+  E.c1 = c1;
+  E.c2 = c2;
+  E.dt = dt;
+  for (int t = 0; t < HW_NTYPES; ++t) {
+    if (mesh->t[t].K > 0 && q_in->p[t] == q_out->p[t]) return fail("q_in and q_out must differ");
+    E.out[t] = h0->p[t];
+    E.qout[t] = q_out->p[t];
+    E.h1[t] = h1 ? h1->p[t] : nullptr;
+    E.h2[t] = h2 ? h2->p[t] : nullptr;
+  }
+  return run_rhs(mesh, q_in, E, subset, stream);
+}
+
+int hw_axpy3(const hw_mesh_t* mesh, const hw_fields_t* q, hw_fields_t* out,
+             const hw_fields_t* h0, const hw_fields_t* h1, const hw_fields_t* h2, int n_hist,
+             double c0, double c1, double c2, double dt, const hw_subset_t* subset,
+             void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  for (int t = 0; t < HW_NTYPES; ++t) {
+    const int64_t K = mesh->t[t].K;
+    if (K <= 0) continue;
+    const int32_t* list;
+    int64_t n;
+    subset_of(subset, t, K, &list, &n);
+    if (n <= 0) continue;
+    const int chunk = 4 * np_of(t, mesh->N);
+    const unsigned g = grid_for(n * chunk);
+    if (mesh->dtype == HW_F64)
+      axpy3_kernel<double><<<g, 256, 0, st>>>(
+          (const double*)q->p[t], (double*)out->p[t], (const double*)h0->p[t],
+          h1 ? (const double*)h1->p[t] : nullptr, h2 ? (const double*)h2->p[t] : nullptr,
+          n_hist, c0, c1, c2, dt, list, n, chunk);
+    else
+      axpy3_kernel<float><<<g, 256, 0, st>>>(
+          (const float*)q->p[t], (float*)out->p[t], (const float*)h0->p[t],
+          h1 ? (const float*)h1->p[t] : nullptr, h2 ? (const float*)h2->p[t] : nullptr, n_hist,
+          (float)c0, (float)c1, (float)c2, (float)dt, list, n, chunk);
+    int rc = check_launch("axpy3_kernel");
+    if (rc) return rc;
+  }
+  return 0;
+}
+
+int hw_hist_push(const hw_mesh_t* mesh, hw_fields_t* h0, hw_fields_t* h1, hw_fields_t* h2,
+                 const hw_fields_t* rhs, const hw_subset_t* subset, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  for (int t = 0; t < HW_NTYPES; ++t) {
+    const int64_t K = mesh->t[t].K;
+    if (K <= 0) continue;
+    const int32_t* list;
+    int64_t n;
+    subset_of(subset, t, K, &list, &n);
+    if (n <= 0) continue;
+    const int chunk = 4 * np_of(t, mesh->N);
+    const unsigned g = grid_for(n * chunk);
+    if (mesh->dtype == HW_F64)
+      hist_push_kernel<double><<<g, 256, 0, st>>>((double*)h0->p[t], (double*)h1->p[t],
+                                                  (double*)h2->p[t], (const double*)rhs->p[t],
+                                                  list, n, chunk);
+    else
+      hist_push_kernel<float><<<g, 256, 0, st>>>((float*)h0->p[t], (float*)h1->p[t],
+                                                 (float*)h2->p[t], (const float*)rhs->p[t], list,
+                                                 n, chunk);
+    int rc = check_launch("hist_push_kernel");
+    if (rc) return rc;
+  }
+  return 0;
+}
+
+int hw_halo_pack(const hw_mesh_t* mesh, int elem_type, const void* q, const int32_t* idx,
+                 int64_t n, void* sendbuf, void* stream) {
+  if (elem_type < 0 || elem_type >= HW_NTYPES) return fail("bad element type");
+  if (n <= 0) return 0;
+  const int chunk = 4 * np_of(elem_type, mesh->N);
+  const unsigned g = grid_for(n * chunk);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (mesh->dtype == HW_F64)
+    pack_kernel<double><<<g, 256, 0, st>>>((const double*)q, idx, n, chunk, (double*)sendbuf);
+  else
+    pack_kernel<float><<<g, 256, 0, st>>>((const float*)q, idx, n, chunk, (float*)sendbuf);
+  return check_launch("pack_kernel");
+}
+
+int hw_energy(const hw_mesh_t*, const hw_fields_t*, double*, void*) {
+  return fail("hw_energy: not built yet");
+}
+
+}  // extern "C"

@@ -1,0 +1,180 @@
+"""Device-resident mesh: the HBM layout the sm_100a kernels read.
+
+Per element type (K elements):
+  state            (K, 4, Np)  element-major, reference node/mode order
+  geometry record  hex: 8 vertices (24); tet/pyramid/wedge (affine): G,
+                   per-face normal and Js/J (wedge: 1/sqrt(J), Js/sqrt(J))
+  mat              (K, 4): kappa, 1/rho, rho*c, 0
+  nbr_elem/code    (K, nfaces) int32: neighbour index and packed
+                   type | face << 2 | orientation << 5 | boundary bit
+  operators        constant matrices (device_operators), a few KB-100 KB
+No per-point geometry and no face-trace buffer are stored: neighbour
+traces are evaluated from the neighbour's state inside the kernels.
+"""
+
+import numpy as np
+import torch
+
+from . import _native as nat
+from .operators import TYPE_ID, device_operators, face_symmetry_perms
+from .refelem import FACES, face_geometry_batch, geometric_factors_batch
+
+_CENTROID2D = {"tri": np.array([[-1.0 / 3.0, -1.0 / 3.0]]), "quad": np.array([[0.0, 0.0]])}
+_INTERIOR_ABC = {"tet": np.array([[-0.5, -0.5, -0.5]]), "wedge": np.array([[0.0, 0.0, 0.0]]),
+                 "pyramid": np.array([[0.0, 0.0, 0.0]])}
+
+
+def _affine_check(t, verts, N):
+    """The nodal-face representation needs affine wedges/pyramids (constant
+    J); tets are always affine."""
+    from .quadrature import element_rule
+    if t not in ("wedge", "pyramid") or len(verts) == 0:
+        return
+    rule = element_rule(t, max(N, 1))
+    _, J, _, _ = geometric_factors_batch(t, verts, rule.collapsed, label=t)
+    spread = (J.max(axis=1) - J.min(axis=1)) / J.max(axis=1)
+    if spread.max() > 1e-9:
+        raise NotImplementedError(
+            f"non-affine {t} elements (J varies by {spread.max():.2e}); the device path "
+            "currently requires affine wedges and pyramids (DESIGN.md, scope)")
+
+
+def geometry_records(t, verts):
+    """Per-element geometry record (float64 numpy), layouts in the header."""
+    K = len(verts)
+    if t == "hex":
+        return verts.reshape(K, 24).copy()
+    _, J, G, _ = geometric_factors_batch(t, verts, _INTERIOR_ABC[t], label=t)
+    J, G = J[:, 0], G[:, 0]
+    cols = [G.reshape(K, 9)]
+    if t == "wedge":
+        isj = 1.0 / np.sqrt(J)
+        cols.append(isj[:, None])
+        scale = isj
+    else:
+        scale = 1.0 / J
+    for f, (ftype, _) in enumerate(FACES[t]):
+        _, Js, nrm = face_geometry_batch(t, verts, f, _CENTROID2D[ftype])
+        cols.append(nrm[:, 0, :])
+        cols.append((Js[:, 0] * scale)[:, None])
+    return np.hstack(cols)
+
+
+def material_records(mat):
+    rho, kappa = mat[:, 0], mat[:, 1]
+    if np.any(rho <= 0) or np.any(kappa <= 0):
+        raise ValueError("material parameters must be positive")
+    z = rho * np.sqrt(kappa / rho)
+    return np.column_stack([kappa, 1.0 / rho, z, np.zeros_like(z)])
+
+
+def neighbour_codes(mesh, t):
+    nbr = mesh.nbr[t]
+    code = mesh.face_code[t].astype(np.int64)
+    K, nf = nbr.shape[:2]
+    bnd = nbr[:, :, 0] < 0
+    packed = (np.where(bnd, 0, nbr[:, :, 0]) | (np.where(bnd, 0, nbr[:, :, 2]) << 2)
+              | (np.where(bnd, 0, code) << 5) | np.where(bnd, nat.HW_NBR_BOUNDARY, 0))
+    elem = np.where(bnd, np.arange(K)[:, None], nbr[:, :, 1])
+    if elem.max(initial=0) >= 2 ** 31:
+        raise ValueError("element index exceeds int32")
+    return elem.astype(np.int32), packed.astype(np.int32)
+
+
+def hex_node_face_points(dops, N):
+    """(6, Np): for node n and face f, the face point on the node's line
+    normal to f."""
+    n1 = N + 1
+    Np = n1 ** 3
+    nfq = n1 * n1
+    tab = dops["face_tab"]
+    out = np.empty((6, Np), dtype=np.int32)
+    strides = (n1 * n1, n1, 1)
+    for f in range(6):
+        axis = f >> 1
+        lut = {int(tab[f * nfq + j, 0]): j for j in range(nfq)}
+        for n in range(Np):
+            idx = (n // (n1 * n1), (n // n1) % n1, n % n1)
+            out[f, n] = lut[n - idx[axis] * strides[axis]]
+    return out
+
+
+class DeviceMesh:
+    """Owns every device tensor the kernels read and the C struct pointing
+    at them."""
+
+    def __init__(self, disc, device, dtype=torch.float64):
+        if dtype not in (torch.float64, torch.float32):
+            raise ValueError("dtype must be float64 or float32")
+        self.device = torch.device(device)
+        self.dtype = dtype
+        self.N = disc.N
+        self._keep = []
+        mesh = disc.mesh
+        S = nat.HWMesh()
+        S.N = disc.N
+        S.dtype = nat.HW_F64 if dtype == torch.float64 else nat.HW_F32
+        S.formulation = nat.HW_GL if disc.formulation.kind == "GL" else nat.HW_SEM
+        S.penalty_scale = float(disc.penalty_scale)
+        dops_any = None
+        for t in disc.types:
+            form = disc.forms[t]
+            if t in ("hex", "tet") and form != "strong":
+                raise NotImplementedError(f"device {t} kernel implements the strong form only")
+            if t == "wedge" and form != "skew":
+                raise NotImplementedError("device wedge kernel implements the skew form only")
+            verts = mesh.element_vertices(t)
+            _affine_check(t, verts, disc.N)
+            dops = device_operators(t, disc.N, disc.formulation.kind, disc.ops[t])
+            dops_any = dops
+            T = S.t[TYPE_ID[t]]
+            T.K = disc.n_elems[t]
+            T.form = nat.HW_FORM_SKEW if form == "skew" else nat.HW_FORM_STRONG
+            T.geo = self._put(geometry_records(t, verts))
+            T.mat = self._put(material_records(np.asarray(mesh.materials[t], dtype=float)))
+            elem, code = neighbour_codes(mesh, t)
+            T.nbr_elem = self._put(elem, torch.int32)
+            T.nbr_code = self._put(code, torch.int32)
+            for slot, arr in self._pack_ops(t, dops).items():
+                T.op[slot] = self._put(arr)
+            for slot, arr in self._pack_iops(t, dops).items():
+                T.iop[slot] = self._put(arr, torch.int32)
+        S.perm_tri = self._put(face_symmetry_perms("tri", dops_any["tri2d"]), torch.int32)
+        S.perm_quad = self._put(face_symmetry_perms("quad", dops_any["quad2d"]), torch.int32)
+        self.struct = S
+        orders = nat.lib().hw_supported_orders()
+        if not (orders >> disc.N) & 1:
+            raise ValueError(f"order N={disc.N} not compiled into {nat.LIB_NAME}")
+
+    def _put(self, arr, dtype=None):
+        t = torch.as_tensor(np.ascontiguousarray(arr), dtype=dtype or self.dtype).to(self.device)
+        self._keep.append(t)
+        return t.data_ptr()
+
+    @staticmethod
+    def _pack_ops(t, d):
+        if t == "hex":
+            return {0: d["D1"], 1: d["Vend"], 2: d["w1"], 4: _hex_nodes(d)}
+        if t == "tet":
+            return {0: np.stack([d["Dr"].T, d["Ds"].T, d["Dt"].T]), 1: d["LIFT"].T}
+        if t == "wedge":
+            return {0: d["V"].T, 1: np.stack([d["Dr3"].T, d["Ds3"].T, d["Dt3"].T]),
+                    2: d["V"], 3: np.stack([d["Dr3"], d["Ds3"], d["Dt3"]]), 4: d["wq"],
+                    5: d["E"].T, 6: d["LIFT"].T}
+        if t == "pyramid":
+            return {0: np.stack([d["Dr"].T, d["Ds"].T, d["Dt"].T]),
+                    1: np.stack([d["Dr"], d["Ds"], d["Dt"]]), 5: d["E"].T, 6: d["LIFT"].T}
+        raise ValueError(t)
+
+    def _pack_iops(self, t, d):
+        if t == "hex":
+            return {0: d["face_tab"], 1: hex_node_face_points(d, self.N)}
+        if t == "tet":
+            return {0: d["face_nodes"]}
+        return {}
+
+
+def _hex_nodes(d):
+    # 1-D node coordinates: the quad face rule's 1-D points (GL or GLL)
+    n1 = len(d["w1"])
+    return d["quad2d"][::n1, 0].copy()

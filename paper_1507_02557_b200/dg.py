@@ -1,0 +1,492 @@
+"""Drop-in ``Discretization`` whose right-hand side runs on the sm_100a
+kernels (reference interface: hybridwave/dg.py:89-572).
+
+Same constructor, same state layout (dict type -> (K, 4, Np)), same entry
+points (``compute_rhs``, ``apply_A``, ``compute_traces``,
+``apply_mass_inverse``, ``project``, ``eval_at``, ``l2_error``,
+``state_to_vector``/``vector_to_state``) and attributes (``types``,
+``n_elems``, ``ops``, ``data``, ``n_dof``, ``trace_size``, ``gather_idx``,
+``bnd_mask``, ``dof_base``).  States may be numpy arrays (host buffers:
+copied to HBM and back inside the call, like the reference's fresh output
+arrays) or CUDA tensors (stay resident; the fast path).
+
+``compute_rhs`` has no CPU fallback: without the native library or a GPU it
+raises.  The reference-layout arrays (``data``, ``gather_idx`` …) are built
+lazily on the host for the diagnostics and the test oracle; the kernels use
+the compact layout of ``device.py``.
+"""
+
+import numpy as np
+import torch
+
+from . import basis as bas
+from . import _native as nat
+from .operators import TYPE_ID, build_operators, face_symmetry_perms
+from .quadrature import element_rule
+from .refelem import (FACES, face_geometry_batch, geometric_factors_batch,
+                      inverse_duffy_map, duffy_map)
+
+__all__ = ["Formulation", "TABLE_FORMS", "flux_penalties", "Discretization",
+           "discrete_energy", "zero_state", "FIELDS"]
+
+TABLE_FORMS = {
+    "SEM": {"tet": "strong", "pyramid": "skew", "wedge": "skew", "hex": "strong"},
+    "GL": {"tet": "strong", "pyramid": "strong", "wedge": "skew", "hex": "strong"},
+}
+FIELDS = 4
+
+
+class Formulation:
+    """SEM or GL with the per-type forms of the stability table
+    (hybridwave/dg.py:42-58)."""
+
+    def __init__(self, kind):
+        if kind not in TABLE_FORMS:
+            raise ValueError(f"formulation must be 'SEM' or 'GL', got {kind!r}")
+        self.kind = kind
+        self.forms = dict(TABLE_FORMS[kind])
+
+    def form(self, elem_type):
+        return self.forms[elem_type]
+
+    def __repr__(self):
+        return f"Formulation({self.kind!r})"
+
+
+def flux_penalties(rho_m, c_m, rho_p, c_p):
+    """(tau_p, tau_u) = (1/avg(rho c), avg(rho c)) (hybridwave/dg.py:61-69)."""
+    if min(rho_m, c_m, rho_p, c_p) <= 0:
+        raise ValueError("material parameters must be positive")
+    avg = 0.5 * (rho_m * c_m + rho_p * c_p)
+    return 1.0 / avg, avg
+
+
+def zero_state(disc):
+    return {t: np.zeros((disc.n_elems[t], FIELDS, disc.ops[t].Np)) for t in disc.types}
+
+
+class _TypeData:
+    """Reference-layout per-type data (hybridwave/dg.py:77-86), host numpy."""
+
+    def __init__(self):
+        self.w3 = None
+        self.gJfac = None
+        self.J_row = None
+        self.x_nodes = None
+        self.invsqrtJ_face = None
+        self.cub_sqrtJ = None
+        self.over_sqrtJ = None
+
+
+def _default_device():
+    return torch.device("cuda") if torch.cuda.is_available() else None
+
+
+class Discretization:
+    """Operators, geometry and coupling for one mesh / order / formulation."""
+
+    def __init__(self, mesh, N, formulation, forms_override=None, penalty_scale=1.0,
+                 forcing=None, *, dtype=torch.float64, device=None):
+        if isinstance(formulation, str):
+            formulation = Formulation(formulation)
+        self.mesh = mesh
+        self.N = N
+        self.formulation = formulation
+        self.forms = dict(formulation.forms)
+        if forms_override:
+            self.forms.update(forms_override)
+        self.penalty_scale = penalty_scale
+        self.forcing = forcing
+        self.types = mesh.elem_types
+        self.ops = {t: build_operators(t, N, formulation.kind) for t in self.types}
+        self.n_elems = {t: len(mesh.blocks[t]) for t in self.types}
+        self.dof_base, off = {}, 0
+        for t in self.types:
+            self.dof_base[t] = off
+            off += self.n_elems[t] * FIELDS * self.ops[t].Np
+        self.n_dof = off
+        self.dtype = dtype
+        self.device = torch.device(device) if device is not None else _default_device()
+        self._dev = None
+        self._data = None
+        self._ref = None
+        self._cub = {}
+
+    # ------------------------------------------------------------ device side
+
+    @property
+    def device_mesh(self):
+        if self._dev is None:
+            if self.device is None or self.device.type != "cuda":
+                raise RuntimeError("the hybridwave_b200 hot path needs a CUDA device")
+            from .device import DeviceMesh
+            self._dev = DeviceMesh(self, self.device, self.dtype)
+        return self._dev
+
+    def to_device(self, state):
+        """dict of numpy/torch (K,4,Np) -> dict of contiguous device tensors."""
+        out = {}
+        for t in self.types:
+            a = state[t]
+            if isinstance(a, torch.Tensor):
+                a = a.to(device=self.device, dtype=self.dtype)
+            else:
+                a = torch.as_tensor(np.asarray(a), dtype=self.dtype).to(self.device)
+            out[t] = a.contiguous()
+        return out
+
+    def empty_state(self):
+        return {t: torch.empty((self.n_elems[t], FIELDS, self.ops[t].Np), dtype=self.dtype,
+                               device=self.device) for t in self.types}
+
+    def zeros_state(self):
+        return {t: torch.zeros((self.n_elems[t], FIELDS, self.ops[t].Np), dtype=self.dtype,
+                               device=self.device) for t in self.types}
+
+    def slots(self, state):
+        """4-slot list (hex, wedge, pyramid, tet) of tensors / None."""
+        s = [None] * 4
+        if state is not None:
+            for t in self.types:
+                s[TYPE_ID[t]] = state[t]
+        return s
+
+    def stream_ptr(self):
+        return torch.cuda.current_stream(self.device).cuda_stream
+
+    def rhs_device(self, q, out=None, subset=None):
+        """Device RHS: q, out dicts of CUDA tensors (no host copies)."""
+        dm = self.device_mesh
+        out = out if out is not None else self.empty_state()
+        sub = nat.subset(subset) if subset is not None else None
+        nat.check(nat.lib().hw_rhs(dm.struct, nat.fields(self.slots(q)),
+                                   nat.fields(self.slots(out)), sub, self.stream_ptr()))
+        return out
+
+    # ------------------------------------------------------------ public API
+
+    def compute_rhs(self, state, time=0.0):
+        """d(state)/dtau = diag(kappa, 1/rho) M^-1 (A state + forcing)
+        (hybridwave/dg.py:492-506)."""
+        on_host = not isinstance(next(iter(state.values())), torch.Tensor)
+        q = self.to_device(state)
+        out = self.rhs_device(q)
+        if self.forcing is not None:
+            self._add_forcing(out, time)
+        if on_host:
+            return {t: v.cpu().numpy() for t, v in out.items()}
+        return out
+
+    def apply_A(self, state):
+        """R = A U without mass inverse or materials (dg.py:469-477),
+        recovered from the device RHS as R = M diag(1/kappa, rho) rhs."""
+        saved = self.forcing
+        self.forcing = None
+        try:
+            rhs = self.compute_rhs({t: np.asarray(_host(v)) for t, v in state.items()})
+        finally:
+            self.forcing = saved
+        out = {}
+        for t in self.types:
+            mat = self.mesh.materials[t]
+            r = rhs[t].copy()
+            r[:, 0] /= mat[:, 1][:, None]
+            r[:, 1:] *= mat[:, 0][:, None, None]
+            out[t] = self.apply_mass(t, r)
+        return out
+
+    def apply_mass(self, t, v):
+        d = self.data[t]
+        if t == "hex":
+            return v * (d.w3[None, None, :] * d.J[:, None, :])
+        if t == "tet":
+            return (v @ self.ops[t].M_ref.T) * d.J[:, 0][:, None, None]
+        if t == "wedge":
+            return v.copy()
+        return v * d.J[:, None, :]
+
+    def apply_mass_inverse(self, t, residual_t):
+        """hybridwave/dg.py:479-490 (host)."""
+        d = self.data[t]
+        r = _host(residual_t)
+        if t == "hex":
+            return r / (d.w3[None, None, :] * d.J[:, None, :])
+        if t == "tet":
+            return (r @ self.ops[t].invM_ref.T) / d.J[:, 0][:, None, None]
+        if t == "wedge":
+            return r
+        return r / d.J[:, None, :]
+
+    def compute_traces(self, state):
+        """Own-side traces at the reference's stored face points, (4,
+        trace_size) (dg.py:299-316).  Diagnostic; the kernels never form it."""
+        self._ensure_reference_layout()
+        out = np.empty((FIELDS, self.trace_size))
+        for t in self.types:
+            op, d = self.ops[t], self.data[t]
+            tr = _host(state[t]) @ op.Vf.T
+            if t == "wedge":
+                tr = tr * d.invsqrtJ_face[:, None, :]
+            tot = op.face_offsets[-1]
+            b = self.trace_bases[t]
+            out[:, b:b + self.n_elems[t] * tot] = tr.transpose(1, 0, 2).reshape(FIELDS, -1)
+        return out
+
+    # ------------------------------------------------------------ forcing / projection
+
+    def _basis_values(self, t, abc):
+        op = self.ops[t]
+        if t == "hex":
+            return bas.hex_nodal_eval(self.N, "GL" if self.formulation.kind == "GL" else "SEM",
+                                      duffy_map("hex", abc)).V
+        if t == "tet":
+            return bas.tet_orthobasis_eval(self.N, abc).V @ op.Vinv
+        if t == "wedge":
+            return bas.wedge_orthobasis_eval(self.N, abc).V
+        return bas.pyramid_seminodal_eval(self.N, abc).V
+
+    def _cubature(self, t, which):
+        """Cubature data for projection ('cub', degree N) and error norms
+        ('over', degree N+2), dg.py:177-188."""
+        key = (t, which)
+        if key not in self._cub:
+            rule = element_rule(t, self.N if which == "cub" else self.N + 2)
+            x, J, _, _ = geometric_factors_batch(t, self.mesh.element_vertices(t),
+                                                 rule.collapsed, label=t)
+            self._cub[key] = (rule.weights, self._basis_values(t, rule.collapsed), x, J)
+        return self._cub[key]
+
+    def _add_forcing(self, out, time):
+        for t in self.types:
+            w, V, x, J = self._cubature(t, "cub")
+            f = np.asarray(self.forcing(x, time))
+            scale = np.sqrt(J) if t == "wedge" else J
+            R = np.zeros((self.n_elems[t], FIELDS, self.ops[t].Np))
+            R[:, 0] = (f * scale * w[None, :]) @ V
+            dm = self.apply_mass_inverse(t, R)
+            dm[:, 0] *= self.mesh.materials[t][:, 1][:, None]
+            out[t] += torch.as_tensor(dm, dtype=self.dtype, device=out[t].device)
+
+    def project(self, fields_fn, time=0.0):
+        """L2 projection of callable fields (dg.py:521-548); host numpy."""
+        state = {}
+        for t in self.types:
+            if t == "hex":
+                n1 = self.ops["hex"].nodes1d
+                i, j, k = np.meshgrid(n1, n1, n1, indexing="ij")
+                pts = np.column_stack([i.ravel(), j.ravel(), k.ravel()])
+                x, _, _, _ = geometric_factors_batch("hex", self.mesh.element_vertices("hex"),
+                                                     pts)
+                state[t] = np.moveaxis(np.asarray(fields_fn(x, time)), -1, 1)
+                continue
+            w, V, x, J = self._cubature(t, "cub")
+            vals = np.moveaxis(np.asarray(fields_fn(x, time)), -1, 1)
+            if t == "tet":
+                state[t] = ((vals * w[None, None, :]) @ V) @ self.ops[t].invM_ref
+            elif t == "wedge":
+                state[t] = (vals * (w[None, :] * np.sqrt(J))[:, None, :]) @ V
+            else:
+                raw = (vals * (w[None, :] * J)[:, None, :]) @ V
+                _, Jr, _, _ = geometric_factors_batch(t, self.mesh.element_vertices(t),
+                                                      self.ops[t].level_abc, label=t)
+                state[t] = raw / Jr[:, None, :]
+        return state
+
+    def eval_at(self, t, state_t, which="over"):
+        w, V, x, J = self._cubature(t, which)
+        vals = _host(state_t) @ V.T
+        if t == "wedge":
+            vals = vals / np.sqrt(J)[:, None, :]
+        return vals
+
+    def l2_error(self, state, exact_fn, time=0.0):
+        """Over-integrated L2 errors {p, u, total} (dg.py:558-572)."""
+        tot = {"p": 0.0, "u": 0.0}
+        for t in self.types:
+            w, V, x, J = self._cubature(t, "over")
+            num = self.eval_at(t, state[t])
+            ex = np.moveaxis(np.asarray(exact_fn(x, time)), -1, 1)
+            d2 = (num - ex) ** 2
+            wJ = w[None, :] * J
+            tot["p"] += float(np.sum(d2[:, 0] * wJ))
+            tot["u"] += float(np.sum(d2[:, 1:] * wJ[:, None, :]))
+        out = {k: np.sqrt(v) for k, v in tot.items()}
+        out["total"] = np.sqrt(tot["p"] + tot["u"])
+        return out
+
+    def state_to_vector(self, state):
+        return np.concatenate([_host(state[t]).ravel() for t in self.types])
+
+    def vector_to_state(self, vec):
+        out = {}
+        for t in self.types:
+            b = self.dof_base[t]
+            n = self.n_elems[t] * FIELDS * self.ops[t].Np
+            out[t] = vec[b:b + n].reshape(self.n_elems[t], FIELDS, self.ops[t].Np)
+        return out
+
+    # ------------------------------------------------------------ reference layout
+
+    @property
+    def data(self):
+        self._ensure_reference_layout()
+        return self._data
+
+    @property
+    def gather_idx(self):
+        self._ensure_reference_layout()
+        return self._ref["gather"]
+
+    @property
+    def bnd_mask(self):
+        self._ensure_reference_layout()
+        return self._ref["bnd"]
+
+    @property
+    def trace_size(self):
+        return sum(self.n_elems[t] * self.ops[t].face_offsets[-1] for t in self.types)
+
+    @property
+    def trace_bases(self):
+        b, off = {}, 0
+        for t in self.types:
+            b[t] = off
+            off += self.n_elems[t] * self.ops[t].face_offsets[-1]
+        return b
+
+    def _ensure_reference_layout(self):
+        if self._data is not None:
+            return
+        data = {}
+        for t in self.types:
+            data[t] = self._type_data(t)
+        self._data = data
+        self._ref = self._build_gather()
+
+    def _type_data(self, t):
+        """hybridwave/dg.py:139-192 (geometry at the reference's volume and
+        stored face points)."""
+        op = self.ops[t]
+        d = _TypeData()
+        verts = self.mesh.element_vertices(t)
+        d.verts = verts
+        d.diam = np.linalg.norm(verts.max(axis=1) - verts.min(axis=1), axis=1)
+        if t == "hex":
+            n1 = op.nodes1d
+            i, j, k = np.meshgrid(n1, n1, n1, indexing="ij")
+            pts = np.column_stack([i.ravel(), j.ravel(), k.ravel()])
+        elif t == "tet":
+            pts = np.array([[-0.5, -0.5, -0.5]])
+        elif t == "wedge":
+            pts = op.cub.collapsed
+        else:
+            pts = op.level_abc
+        x, J, G, gradJ = geometric_factors_batch(t, verts, pts, label=t)
+        d.J, d.G = J, G
+        if t == "wedge":
+            d.gJfac = -gradJ / (2.0 * J[..., None])
+        if t == "pyramid":
+            d.J_row = J
+        if t == "hex":
+            d.x_nodes = x
+            d.w3 = np.einsum("i,j,k->ijk", op.weights1d, op.weights1d, op.weights1d).ravel()
+        K = len(verts)
+        tot = op.face_offsets[-1]
+        d.wJs = np.empty((K, tot))
+        d.normals = np.empty((K, tot, 3))
+        d.x_face = np.empty((K, tot, 3))
+        for f, (p2, w2) in enumerate(zip(op.face_pts2d, op.face_wts)):
+            sl = slice(op.face_offsets[f], op.face_offsets[f + 1])
+            xf, Js, nrm = face_geometry_batch(t, verts, f, p2)
+            d.x_face[:, sl] = xf
+            d.wJs[:, sl] = w2[None, :] * Js
+            d.normals[:, sl] = nrm
+        if t == "wedge":
+            abc_f = inverse_duffy_map("wedge", op.face_rst)
+            _, Jf, _, _ = geometric_factors_batch("wedge", verts, abc_f, label=t)
+            d.invsqrtJ_face = 1.0 / np.sqrt(Jf)
+        mat = self.mesh.materials[t]
+        d.rhoc = mat[:, 0] * np.sqrt(mat[:, 1] / mat[:, 0])
+        return d
+
+    def _build_gather(self):
+        """Global face-point gather (dg.py:217-285) from the connectivity
+        orientation codes and the stored rules' symmetry permutations,
+        verified geometrically."""
+        bases = self.trace_bases
+        size = self.trace_size
+        gather = np.arange(size)
+        bnd = np.zeros(size, dtype=bool)
+        tau_p = np.empty(size)
+        tau_u = np.empty(size)
+        perms = {}
+        for t in self.types:
+            op = self.ops[t]
+            for f, (ftype, _) in enumerate(FACES[t]):
+                if ftype not in perms:
+                    perms[ftype] = face_symmetry_perms(ftype, op.face_pts2d[f])
+        for t in self.types:
+            op, d = self.ops[t], self.data[t]
+            tot = op.face_offsets[-1]
+            nbr, code = self.mesh.nbr[t], self.mesh.face_code[t]
+            K = self.n_elems[t]
+            for f, (ftype, _) in enumerate(FACES[t]):
+                off, nq = op.face_offsets[f], op.face_offsets[f + 1] - op.face_offsets[f]
+                me = bases[t] + np.arange(K)[:, None] * tot + off + np.arange(nq)[None, :]
+                isb = nbr[:, f, 0] < 0
+                bnd[me[isb].ravel()] = True
+                zm = d.rhoc
+                zp = d.rhoc.copy()
+                for t2 in self.types:
+                    sel = (~isb) & (nbr[:, f, 0] == TYPE_ID[t2])
+                    if not sel.any():
+                        continue
+                    op2 = self.ops[t2]
+                    k2, f2 = nbr[sel, f, 1], nbr[sel, f, 2]
+                    tot2 = op2.face_offsets[-1]
+                    p = perms[ftype][code[sel, f]]                     # (n, nq)
+                    src = bases[t2] + k2[:, None] * tot2 + op2.face_offsets[f2][:, None] + p
+                    gather[me[sel].ravel()] = src.ravel()
+                    zp[sel] = self.data[t2].rhoc[k2]
+                    # geometric verification of the coincidence
+                    xs = self.data[t2].x_face[k2[:, None], op2.face_offsets[f2][:, None] + p]
+                    err = np.linalg.norm(xs - d.x_face[sel][:, off:off + nq], axis=2).max(axis=1)
+                    tol = 1e-10 * np.maximum(d.diam[sel], self.data[t2].diam[k2])
+                    if np.any(err > tol):
+                        raise ValueError(f"face cubature points do not coincide on {t} face {f}")
+                avg = 0.5 * (zm + zp)
+                tau_p[me] = (1.0 / avg)[:, None]
+                tau_u[me] = avg[:, None]
+        for t in self.types:
+            d = self.data[t]
+            tot = self.ops[t].face_offsets[-1]
+            sl = slice(bases[t], bases[t] + self.n_elems[t] * tot)
+            d.tau_p = tau_p[sl].reshape(self.n_elems[t], tot)
+            d.tau_u = tau_u[sl].reshape(self.n_elems[t], tot)
+        return {"gather": gather, "bnd": bnd}
+
+
+def _host(a):
+    if isinstance(a, torch.Tensor):
+        return a.detach().cpu().numpy()
+    return np.asarray(a)
+
+
+def discrete_energy(state, disc):
+    """U^T M U with material weights (hybridwave/dg.py:655-674)."""
+    total = 0.0
+    for t in disc.types:
+        s = _host(state[t])
+        d = disc.data[t]
+        mat = disc.mesh.materials[t]
+        if t == "hex":
+            en = (d.w3[None, None, :] * d.J[:, None, :] * s ** 2).sum(axis=2)
+        elif t == "tet":
+            en = np.einsum("kfi,ij,kfj->kf", s, disc.ops[t].M_ref, s) * d.J[:, 0][:, None]
+        elif t == "wedge":
+            en = (s ** 2).sum(axis=2)
+        else:
+            en = (d.J[:, None, :] * s ** 2).sum(axis=2)
+        total += float(np.sum(en[:, 0] / mat[:, 1]))
+        total += float(np.sum(en[:, 1:] * mat[:, 0][:, None]))
+    return total
