@@ -740,6 +740,7 @@ __global__ void __launch_bounds__(NT) hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi
     if (e >= ne) continue;
     const int idx[3] = {n / (N1 * N1), (n / N1) % N1, n % N1};
     const R* fl = sf + e * NFP * 4;
+    R lift[4] = {R(0), R(0), R(0), R(0)};
 #pragma unroll
     for (int f = 0; f < 6; ++f) {
       const int axis = f >> 1, end = f & 1;
@@ -754,15 +755,19 @@ __global__ void __launch_bounds__(NT) hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi
       const int pt = __ldg(T.iop[1] + f * NP + n);
       const R* o = fl + (f * NFQ + pt) * 4;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) acc[s][c] += w * o[c];
+      for (int c = 0; c < 4; ++c) lift[c] += w * o[c];
     }
+    // only the surface term carries the mass inverse 1/(w3 J): the volume
+    // term above is already the cancelled form -grad p, -div u
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[s][c] += lift[c] * minv[s];
     const R kap = smat[e * 4 + 0], irho = smat[e * 4 + 1];
     const size_t base = (size_t)sk[e] * 4 * NP + n;
     const R* qe = sq + e * 4 * NP + n;
-    epilogue<R>(E, HW_HEX, base, acc[s][0] * minv[s] * kap, qe[0]);
+    epilogue<R>(E, HW_HEX, base, acc[s][0] * kap, qe[0]);
 #pragma unroll
     for (int c = 1; c < 4; ++c)
-      epilogue<R>(E, HW_HEX, base + c * NP, acc[s][c] * minv[s] * irho, qe[c * NP]);
+      epilogue<R>(E, HW_HEX, base + c * NP, acc[s][c] * irho, qe[c * NP]);
   }
 }
 

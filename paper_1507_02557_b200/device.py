@@ -99,6 +99,58 @@ def hex_node_face_points(dops, N):
     return out
 
 
+def pack_mesh(disc):
+    """Host (numpy) image of everything the kernels read: per type
+    {geo, mat, nbr_elem, nbr_code, op{slot}, iop{slot}, form, K} plus the
+    face-point permutation tables.  DeviceMesh uploads it verbatim."""
+    mesh = disc.mesh
+    pack = {"types": {}}
+    dops_any = None
+    for t in disc.types:
+        form = disc.forms[t]
+        if t in ("hex", "tet") and form != "strong":
+            raise NotImplementedError(f"device {t} kernel implements the strong form only")
+        if t == "wedge" and form != "skew":
+            raise NotImplementedError("device wedge kernel implements the skew form only")
+        verts = mesh.element_vertices(t)
+        _affine_check(t, verts, disc.N)
+        dops = device_operators(t, disc.N, disc.formulation.kind, disc.ops[t])
+        dops_any = dops
+        elem, code = neighbour_codes(mesh, t)
+        pack["types"][t] = {
+            "K": disc.n_elems[t], "form": form, "dops": dops,
+            "geo": geometry_records(t, verts),
+            "mat": material_records(np.asarray(mesh.materials[t], dtype=float)),
+            "nbr_elem": elem, "nbr_code": code,
+            "op": _pack_ops(t, dops), "iop": _pack_iops(t, dops, disc.N)}
+    pack["perm_tri"] = face_symmetry_perms("tri", dops_any["tri2d"])
+    pack["perm_quad"] = face_symmetry_perms("quad", dops_any["quad2d"])
+    return pack
+
+
+def _pack_ops(t, d):
+    if t == "hex":
+        return {0: d["D1"], 1: d["Vend"], 2: d["w1"], 4: _hex_nodes(d)}
+    if t == "tet":
+        return {0: np.stack([d["Dr"].T, d["Ds"].T, d["Dt"].T]), 1: d["LIFT"].T}
+    if t == "wedge":
+        return {0: d["V"].T, 1: np.stack([d["Dr3"].T, d["Ds3"].T, d["Dt3"].T]),
+                2: d["V"], 3: np.stack([d["Dr3"], d["Ds3"], d["Dt3"]]), 4: d["wq"],
+                5: d["E"].T, 6: d["LIFT"].T}
+    if t == "pyramid":
+        return {0: np.stack([d["Dr"].T, d["Ds"].T, d["Dt"].T]),
+                1: np.stack([d["Dr"], d["Ds"], d["Dt"]]), 5: d["E"].T, 6: d["LIFT"].T}
+    raise ValueError(t)
+
+
+def _pack_iops(t, d, N):
+    if t == "hex":
+        return {0: d["face_tab"], 1: hex_node_face_points(d, N)}
+    if t == "tet":
+        return {0: d["face_nodes"]}
+    return {}
+
+
 class DeviceMesh:
     """Owns every device tensor the kernels read and the C struct pointing
     at them."""
@@ -110,37 +162,26 @@ class DeviceMesh:
         self.dtype = dtype
         self.N = disc.N
         self._keep = []
-        mesh = disc.mesh
+        self.pack = pack = pack_mesh(disc)
         S = nat.HWMesh()
         S.N = disc.N
         S.dtype = nat.HW_F64 if dtype == torch.float64 else nat.HW_F32
         S.formulation = nat.HW_GL if disc.formulation.kind == "GL" else nat.HW_SEM
         S.penalty_scale = float(disc.penalty_scale)
-        dops_any = None
-        for t in disc.types:
-            form = disc.forms[t]
-            if t in ("hex", "tet") and form != "strong":
-                raise NotImplementedError(f"device {t} kernel implements the strong form only")
-            if t == "wedge" and form != "skew":
-                raise NotImplementedError("device wedge kernel implements the skew form only")
-            verts = mesh.element_vertices(t)
-            _affine_check(t, verts, disc.N)
-            dops = device_operators(t, disc.N, disc.formulation.kind, disc.ops[t])
-            dops_any = dops
+        for t, P in pack["types"].items():
             T = S.t[TYPE_ID[t]]
-            T.K = disc.n_elems[t]
-            T.form = nat.HW_FORM_SKEW if form == "skew" else nat.HW_FORM_STRONG
-            T.geo = self._put(geometry_records(t, verts))
-            T.mat = self._put(material_records(np.asarray(mesh.materials[t], dtype=float)))
-            elem, code = neighbour_codes(mesh, t)
-            T.nbr_elem = self._put(elem, torch.int32)
-            T.nbr_code = self._put(code, torch.int32)
-            for slot, arr in self._pack_ops(t, dops).items():
+            T.K = P["K"]
+            T.form = nat.HW_FORM_SKEW if P["form"] == "skew" else nat.HW_FORM_STRONG
+            T.geo = self._put(P["geo"])
+            T.mat = self._put(P["mat"])
+            T.nbr_elem = self._put(P["nbr_elem"], torch.int32)
+            T.nbr_code = self._put(P["nbr_code"], torch.int32)
+            for slot, arr in P["op"].items():
                 T.op[slot] = self._put(arr)
-            for slot, arr in self._pack_iops(t, dops).items():
+            for slot, arr in P["iop"].items():
                 T.iop[slot] = self._put(arr, torch.int32)
-        S.perm_tri = self._put(face_symmetry_perms("tri", dops_any["tri2d"]), torch.int32)
-        S.perm_quad = self._put(face_symmetry_perms("quad", dops_any["quad2d"]), torch.int32)
+        S.perm_tri = self._put(pack["perm_tri"], torch.int32)
+        S.perm_quad = self._put(pack["perm_quad"], torch.int32)
         self.struct = S
         orders = nat.lib().hw_supported_orders()
         if not (orders >> disc.N) & 1:
@@ -150,28 +191,6 @@ class DeviceMesh:
         t = torch.as_tensor(np.ascontiguousarray(arr), dtype=dtype or self.dtype).to(self.device)
         self._keep.append(t)
         return t.data_ptr()
-
-    @staticmethod
-    def _pack_ops(t, d):
-        if t == "hex":
-            return {0: d["D1"], 1: d["Vend"], 2: d["w1"], 4: _hex_nodes(d)}
-        if t == "tet":
-            return {0: np.stack([d["Dr"].T, d["Ds"].T, d["Dt"].T]), 1: d["LIFT"].T}
-        if t == "wedge":
-            return {0: d["V"].T, 1: np.stack([d["Dr3"].T, d["Ds3"].T, d["Dt3"].T]),
-                    2: d["V"], 3: np.stack([d["Dr3"], d["Ds3"], d["Dt3"]]), 4: d["wq"],
-                    5: d["E"].T, 6: d["LIFT"].T}
-        if t == "pyramid":
-            return {0: np.stack([d["Dr"].T, d["Ds"].T, d["Dt"].T]),
-                    1: np.stack([d["Dr"], d["Ds"], d["Dt"]]), 5: d["E"].T, 6: d["LIFT"].T}
-        raise ValueError(t)
-
-    def _pack_iops(self, t, d):
-        if t == "hex":
-            return {0: d["face_tab"], 1: hex_node_face_points(d, self.N)}
-        if t == "tet":
-            return {0: d["face_nodes"]}
-        return {}
 
 
 def _hex_nodes(d):

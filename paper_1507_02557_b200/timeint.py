@@ -1,0 +1,262 @@
+"""Device-resident time integration behind the reference's timeint API
+(hybridwave/timeint.py:17-181) plus LSRK-45.
+
+Every step is one fused kernel launch per element type (RHS + update); the
+state, residual and Adams-Bashforth history live in HBM for the whole run.
+``single_rate_run`` / ``lsrk_run`` / ``mrab_run`` accept numpy states (the
+reference's host arrays: copied in once, out at the end and for callbacks)
+or CUDA tensors (stay on the device).
+"""
+
+import math
+
+import numpy as np
+import torch
+
+from . import _native as nat
+from .operators import TYPE_ID
+
+__all__ = ["ab_coefficients", "ab3_step", "single_rate_run", "MRABDriver", "mrab_run",
+           "lsrk_step", "lsrk_run", "LSRK_A", "LSRK_B", "LSRK_C", "Stepper"]
+
+# Carpenter & Kennedy (1994) (4,5) 2N-storage
+LSRK_A = (0.0, -567301805773.0 / 1357537059087.0, -2404267990393.0 / 2016746695238.0,
+          -3550918686646.0 / 2091501179385.0, -1275806237668.0 / 842570457699.0)
+LSRK_B = (1432997174477.0 / 9575080441755.0, 5161836677717.0 / 13612068292357.0,
+          1720146321549.0 / 2090206949498.0, 3134564353537.0 / 4481467310338.0,
+          2277821191437.0 / 14882151754819.0)
+LSRK_C = (0.0, 1432997174477.0 / 9575080441755.0, 2526269341429.0 / 6820363962896.0,
+          2006345519317.0 / 3224310063776.0, 2802321613138.0 / 2924317926251.0)
+
+
+def ab_coefficients(n_hist, theta=1.0):
+    """u(t + theta h) = u(t) + h sum c_i f_i (hybridwave/timeint.py:21-38)."""
+    th = theta
+    if n_hist == 1:
+        return np.array([th])
+    if n_hist == 2:
+        return np.array([th + th ** 2 / 2.0, -(th ** 2) / 2.0])
+    if n_hist == 3:
+        return np.array([th + 3.0 * th ** 2 / 4.0 + th ** 3 / 6.0, -(th ** 2) - th ** 3 / 3.0,
+                         th ** 2 / 4.0 + th ** 3 / 6.0])
+    raise ValueError("history depth must be 1..3")
+
+
+def ab3_step(state, history, dt, theta=1.0):
+    """hybridwave/timeint.py:41-54 (numpy or torch dicts)."""
+    c = ab_coefficients(len(history), theta)
+    out = {}
+    for t, a in state.items():
+        acc = a.clone() if isinstance(a, torch.Tensor) else np.array(a, copy=True)
+        for ci, f in zip(c, history):
+            acc += dt * float(ci) * f[t]
+        out[t] = acc
+    return out
+
+
+def _is_host(state):
+    return not isinstance(next(iter(state.values())), torch.Tensor)
+
+
+def _export(disc, q, host):
+    if host:
+        return {t: q[t].cpu().numpy() for t in disc.types}
+    return {t: q[t].clone() for t in disc.types}
+
+
+def _no_forcing(disc):
+    if disc.forcing is not None:
+        raise NotImplementedError("the fused device time loops do not take a forcing "
+                                  "callback; use compute_rhs + ab3_step")
+
+
+class Stepper:
+    """Device buffers and launch sequence for one integrator, reusable by
+    the benchmark (and CUDA-graph capturable: no host syncs, fixed
+    pointers when ``swap=False``)."""
+
+    def __init__(self, disc, state, scheme="lsrk"):
+        self.disc = disc
+        self.dm = disc.device_mesh
+        self.q = disc.to_device(state)
+        self.q2 = disc.empty_state()
+        self.scheme = scheme
+        if scheme == "lsrk":
+            self.res = disc.zeros_state()
+        else:
+            self.hist = [disc.zeros_state() for _ in range(3)]
+            self.n_steps = 0
+        self.launches_per_stage = len(disc.types)
+
+    def _f(self, s):
+        return nat.fields(self.disc.slots(s))
+
+    def lsrk_step(self, h):
+        L = nat.lib()
+        st = self.disc.stream_ptr()
+        for a, b in zip(LSRK_A, LSRK_B):
+            nat.check(L.hw_lsrk_stage(self.dm.struct, self._f(self.q), self._f(self.q2),
+                                      self._f(self.res), a, b, h, None, st))
+            self.q, self.q2 = self.q2, self.q
+
+    def ab_step(self, dt, theta=1.0):
+        nh = min(self.n_steps + 1, 3)
+        c = ab_coefficients(nh, theta)
+        c = list(c) + [0.0] * (3 - len(c))
+        new = self.hist[2]
+        nat.check(nat.lib().hw_ab_step(self.dm.struct, self._f(self.q), self._f(self.q2),
+                                       self._f(new), self._f(self.hist[0]),
+                                       self._f(self.hist[1]), nh, c[0], c[1], c[2], dt, None,
+                                       self.disc.stream_ptr()))
+        self.hist = [new, self.hist[0], self.hist[1]]
+        self.q, self.q2 = self.q2, self.q
+        self.n_steps += 1
+
+
+def single_rate_run(disc, state, dt, T_final, callback=None):
+    """AB3 to T_final; the last step lands through the fractional
+    coefficients (hybridwave/timeint.py:57-72)."""
+    _no_forcing(disc)
+    host = _is_host(state)
+    S = Stepper(disc, state, "ab")
+    time = 0.0
+    while time < T_final - 1e-14:
+        h = min(dt, T_final - time)
+        S.ab_step(dt, theta=h / dt)
+        time += h
+        if callback is not None:
+            callback(time, _export(disc, S.q, host))
+    return _export(disc, S.q, host)
+
+
+def lsrk_step(disc, q, res, dt, q_tmp=None):
+    """One 5-stage LSRK(4,5) step on device dicts (q, res updated; q is
+    returned, possibly a different buffer set when q_tmp is supplied)."""
+    _no_forcing(disc)
+    dm = disc.device_mesh
+    q_tmp = q_tmp if q_tmp is not None else disc.empty_state()
+    st = disc.stream_ptr()
+    for a, b in zip(LSRK_A, LSRK_B):
+        nat.check(nat.lib().hw_lsrk_stage(dm.struct, nat.fields(disc.slots(q)),
+                                          nat.fields(disc.slots(q_tmp)),
+                                          nat.fields(disc.slots(res)), a, b, dt, None, st))
+        q, q_tmp = q_tmp, q
+    return q
+
+
+def lsrk_run(disc, state, dt, T_final, callback=None):
+    """Low-storage RK(4,5) to T_final with the single_rate_run signature;
+    the last step is shortened to land on T_final."""
+    _no_forcing(disc)
+    host = _is_host(state)
+    S = Stepper(disc, state, "lsrk")
+    time = 0.0
+    while time < T_final - 1e-14:
+        h = min(dt, T_final - time)
+        S.lsrk_step(h)
+        time += h
+        if callback is not None:
+            callback(time, _export(disc, S.q, host))
+    return _export(disc, S.q, host)
+
+
+class MRABDriver:
+    """Multi-rate AB3 (hybridwave/timeint.py:75-173) that launches only the
+    active levels: each tick evaluates the RHS of the stepping elements
+    alone (the reference evaluates the whole mesh and discards the rest),
+    fused with their AB update; coarse neighbours are seen through their
+    dense-output extrapolation.  Same arithmetic for every consumed entry."""
+
+    def __init__(self, disc, plan):
+        self.disc = disc
+        self.plan = plan
+        plan.validate_neighbor_levels(disc.mesh)
+        self.levels = {t: plan.levels_of(disc.mesh, t) for t in disc.types}
+        self.n_levels = plan.n_levels
+        self.rhs_evals = {t: np.zeros(disc.n_elems[t], dtype=int) for t in disc.types}
+        self.macro_steps = 0
+        dev = disc.device
+        # element lists per level per type (int32 on the device)
+        self._lists = {}
+        for lev in range(1, self.n_levels + 1):
+            for t in disc.types:
+                idx = np.flatnonzero(self.levels[t] == lev).astype(np.int32)
+                self._lists[(lev, t)] = torch.as_tensor(idx, device=dev) if len(idx) else None
+
+    def _subset(self, levs):
+        lists = [None] * 4
+        empty = torch.zeros(0, dtype=torch.int32, device=self.disc.device)
+        for t in self.disc.types:
+            parts = [self._lists[(lev, t)] for lev in levs if self._lists[(lev, t)] is not None]
+            lists[TYPE_ID[t]] = torch.cat(parts) if parts else empty
+        return lists
+
+    def run(self, state, T_final, callback=None):
+        _no_forcing(self.disc)
+        disc = self.disc
+        L = self.n_levels
+        host = _is_host(state)
+        macro = 2 ** (L - 1) * self.plan.dt_min
+        n_macro = max(1, math.ceil(T_final / macro - 1e-12))
+        dt_min = T_final / (n_macro * 2 ** (L - 1))
+        q = disc.to_device(state)
+        eff = disc.empty_state()
+        ring = [disc.zeros_state() for _ in range(3)]
+        n_hist = np.zeros(L + 1, dtype=int)
+        steps = np.zeros(L + 1, dtype=int)
+        lib, dm, st = nat.lib(), disc.device_mesh, disc.stream_ptr()
+        F = lambda s: nat.fields(disc.slots(s))
+        subs = {lev: self._subset([lev]) for lev in range(1, L + 1)}
+        sub_structs = {lev: nat.subset(subs[lev]) for lev in subs}
+        for m in range(n_macro):
+            t0 = m * dt_min * 2 ** (L - 1)
+            for tick in range(2 ** (L - 1)):
+                stepping = [lev for lev in range(1, L + 1) if tick % (2 ** (L - lev)) == 0]
+                # effective state: q, plus the dense-output correction on
+                # non-stepping levels (timeint.py:144-173)
+                for lev in range(1, L + 1):
+                    period = 2 ** (L - lev)
+                    frac = tick % period
+                    nh = n_hist[lev]
+                    if frac == 0 or nh == 0:
+                        nat.check(lib.hw_axpy3(dm.struct, F(q), F(eff), F(ring[0]), None, None,
+                                               1, 0.0, 0.0, 0.0, 0.0, sub_structs[lev], st))
+                        continue
+                    c = ab_coefficients(nh, frac / period) - ab_coefficients(nh, 1.0)
+                    c = list(c) + [0.0] * (3 - nh)
+                    s0 = steps[lev] % 3
+                    h = [ring[s0], ring[(s0 - 1) % 3], ring[(s0 - 2) % 3]]
+                    nat.check(lib.hw_axpy3(dm.struct, F(q), F(eff), F(h[0]), F(h[1]), F(h[2]),
+                                           nh, c[0], c[1], c[2], dt_min * period,
+                                           sub_structs[lev], st))
+                # fused RHS + AB update of each stepping level
+                for lev in stepping:
+                    n_hist[lev] = min(n_hist[lev] + 1, 3)
+                    steps[lev] += 1
+                    s0 = steps[lev] % 3
+                    h0, h1, h2 = ring[s0], ring[(s0 - 1) % 3], ring[(s0 - 2) % 3]
+                    nh = n_hist[lev]
+                    c = list(ab_coefficients(nh)) + [0.0] * (3 - nh)
+                    nat.check(lib.hw_ab_step(dm.struct, F(eff), F(q), F(h0), F(h1), F(h2), nh,
+                                             c[0], c[1], c[2], dt_min * 2 ** (L - lev),
+                                             sub_structs[lev], st))
+                    for t in disc.types:
+                        self.rhs_evals[t][self.levels[t] == lev] += 1
+            self.macro_steps += 1
+            if callback is not None:
+                callback(t0 + dt_min * 2 ** (L - 1), _export(disc, q, host))
+        out = _export(disc, q, host)
+        for t in disc.types:
+            if host:
+                state[t][...] = out[t]
+            else:
+                state[t].copy_(out[t])
+        return state
+
+
+def mrab_run(disc, plan, state, T_final, callback=None):
+    """hybridwave/timeint.py:176-181: returns (state, driver); state is
+    updated in place like the reference's."""
+    driver = MRABDriver(disc, plan)
+    driver.run(state, T_final, callback=callback)
+    return state, driver

@@ -1,0 +1,185 @@
+"""Generate the golden fixtures by running the REFERENCE package itself.
+
+Run in the build container (the reference is not on the GPU box):
+    PYTHONPATH=/root/reference/pkg/src PYTHONDONTWRITEBYTECODE=1 \
+        python tests/golden/make_golden.py
+
+Writes tests/golden/*.npz.  States are regenerated in the tests from the
+recorded seeds (np.random.default_rng(seed).standard_normal(shape)), so
+only reference outputs are stored.
+"""
+
+import os
+import sys
+
+import numpy as np
+
+import hybridwave
+from hybridwave import operators as ops_mod
+from hybridwave.app import cavity_fields
+from hybridwave.dg import Discretization, discrete_energy
+from hybridwave.mesh import structured_hybrid_mesh, uniform_cube_mesh
+from hybridwave.stability import assign_mrab_levels, local_timesteps
+from hybridwave.timeint import mrab_run, single_rate_run
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+# LSRK(4,5) 2N-storage, Carpenter & Kennedy 1994 (the reference has none)
+A = [0.0, -567301805773.0 / 1357537059087.0, -2404267990393.0 / 2016746695238.0,
+     -3550918686646.0 / 2091501179385.0, -1275806237668.0 / 842570457699.0]
+B = [1432997174477.0 / 9575080441755.0, 5161836677717.0 / 13612068292357.0,
+     1720146321549.0 / 2090206949498.0, 3134564353537.0 / 4481467310338.0,
+     2277821191437.0 / 14882151754819.0]
+C = [0.0, 1432997174477.0 / 9575080441755.0, 2526269341429.0 / 6820363962896.0,
+     2006345519317.0 / 3224310063776.0, 2802321613138.0 / 2924317926251.0]
+
+
+def build_mesh(spec):
+    kind, n = spec.split(":")
+    n = int(n)
+    return structured_hybrid_mesh(n) if kind == "hybrid" else uniform_cube_mesh(kind, n)
+
+
+def set_random_materials(mesh, seed):
+    rng = np.random.default_rng(seed)
+    for t in mesh.elem_types:
+        mesh.materials[t] = rng.uniform(0.5, 2.0, (len(mesh.blocks[t]), 2))
+
+
+def lsrk_run_ref(disc, state, dt, T_final):
+    q = {t: v.copy() for t, v in state.items()}
+    res = {t: np.zeros_like(v) for t, v in q.items()}
+    time = 0.0
+    while time < T_final - 1e-14:
+        h = min(dt, T_final - time)
+        for a, b, c in zip(A, B, C):
+            k = disc.compute_rhs(q, time + c * h)
+            for t in q:
+                res[t] = a * res[t] + h * k[t]
+                q[t] = q[t] + b * res[t]
+        time += h
+    return q
+
+
+RHS_CASES = [
+    # (mesh, N, formulation, materials seed or None, penalty_scale, state seed)
+    ("hybrid:2", 1, "GL", None, 1.0, 0),
+    ("hybrid:2", 2, "GL", None, 1.0, 1),
+    ("hybrid:2", 3, "GL", 7, 1.0, 2),
+    ("hybrid:2", 1, "SEM", None, 1.0, 3),
+    ("hybrid:2", 2, "SEM", 7, 1.0, 4),
+    ("hybrid:2", 3, "SEM", None, 1.0, 5),
+    ("hybrid:3", 2, "GL", 7, 1.0, 6),
+    ("hybrid:2", 2, "GL", None, 0.0, 7),
+    ("hex:2", 2, "SEM", None, 1.0, 8),
+    ("hex:2", 3, "GL", 7, 1.0, 9),
+    ("tet:2", 3, "GL", None, 1.0, 10),
+    ("wedge:2", 2, "SEM", None, 1.0, 11),
+    ("pyramid:2", 2, "SEM", None, 1.0, 12),
+    ("pyramid:2", 2, "GL", 7, 1.0, 13),
+    ("hybrid:2", 4, "GL", None, 1.0, 14),
+    ("hybrid:2", 5, "SEM", None, 1.0, 15),
+]
+
+
+def main():
+    out = {"reference_version": hybridwave.__version__, "numpy": np.__version__}
+    # ---- operators
+    opsd = {}
+    for t in ("hex", "wedge", "pyramid", "tet"):
+        for N in (1, 2, 3):
+            for form in ("GL", "SEM"):
+                o = ops_mod.build_operators(t, N, form)
+                for f in ("Vf", "D1", "Vf_end", "Dr", "Ds", "Dt", "M_ref", "invM_ref", "V",
+                          "Dr3", "Ds3", "Dt3", "nodes", "level_abc"):
+                    if hasattr(o, f):
+                        opsd[f"{t}/{N}/{form}/{f}"] = np.asarray(getattr(o, f))
+    np.savez_compressed(os.path.join(HERE, "operators.npz"), **opsd)
+
+    # ---- meshes and connectivity
+    md = {}
+    for spec in ("hybrid:3", "hex:2", "tet:2", "wedge:2", "pyramid:2"):
+        m = build_mesh(spec)
+        md[f"{spec}/vertices"] = m.vertices
+        for t in m.elem_types:
+            md[f"{spec}/{t}/blocks"] = m.blocks[t]
+            nb = np.full((len(m.blocks[t]), len(m.face_links[t][0]), 4), -1)
+            tid = {"hex": 0, "wedge": 1, "pyramid": 2, "tet": 3}
+            for k, row in enumerate(m.face_links[t]):
+                for f, l in enumerate(row):
+                    if not l.is_boundary:
+                        t2, k2, f2 = l.neighbor
+                        nb[k, f] = (tid[t2], k2, f2, l.orientation)
+            md[f"{spec}/{t}/links"] = nb
+    np.savez_compressed(os.path.join(HERE, "meshes.npz"), **md)
+
+    # ---- single-RHS parity
+    rd = {}
+    for i, (spec, N, form, mseed, pen, sseed) in enumerate(RHS_CASES):
+        m = build_mesh(spec)
+        if mseed is not None:
+            set_random_materials(m, mseed)
+        d = Discretization(m, N, form, penalty_scale=pen)
+        rng = np.random.default_rng(sseed)
+        st = {t: rng.standard_normal((d.n_elems[t], 4, d.ops[t].Np)) for t in d.types}
+        r = d.compute_rhs(st)
+        for t in d.types:
+            rd[f"{i}/{t}"] = r[t]
+        # geometry / coupling arrays of the first cases
+        if i < 2:
+            for t in d.types:
+                for f in ("J", "G", "wJs", "normals", "tau_p", "tau_u", "gJfac",
+                          "invsqrtJ_face"):
+                    v = getattr(d.data[t], f)
+                    if v is not None:
+                        rd[f"{i}/{t}/data/{f}"] = v
+            rd[f"{i}/gather"] = d.gather_idx
+            rd[f"{i}/bnd"] = d.bnd_mask
+    np.savez_compressed(os.path.join(HERE, "rhs.npz"), **rd)
+
+    # ---- trajectories (100 steps)
+    td = {}
+    for tag, spec, N, form in (("c1_sem", "hex:4", 2, "SEM"), ("c1_gl", "hex:4", 2, "GL"),
+                               ("hyb4_gl", "hybrid:4", 3, "GL")):
+        m = build_mesh(spec)
+        d = Discretization(m, N, form)
+        st0 = d.project(cavity_fields, 0.0)
+        dt = min(float(v.min()) for v in local_timesteps(d, 0.5).values())
+        T = 100 * dt
+        if tag != "hyb4_gl":
+            en = []
+            sab = single_rate_run(d, st0, dt, T, callback=lambda tau, s: en.append(
+                discrete_energy(s, d)))
+            err = d.l2_error(sab, cavity_fields, T)
+            for t in d.types:
+                td[f"{tag}/ab3/{t}"] = sab[t]
+            td[f"{tag}/ab3/err"] = np.array([err["p"], err["u"], err["total"]])
+            td[f"{tag}/ab3/energy"] = np.array(en)
+        slr = lsrk_run_ref(d, st0, dt, T)
+        err = d.l2_error(slr, cavity_fields, T)
+        for t in d.types:
+            td[f"{tag}/lsrk/{t}"] = slr[t]
+        td[f"{tag}/lsrk/err"] = np.array([err["p"], err["u"], err["total"]])
+        td[f"{tag}/dt"] = np.array(dt)
+        td[f"{tag}/energy0"] = np.array(discrete_energy(st0, d))
+    # MRAB on the reference hybrid mesh (2 occupied levels) and uniform-level check
+    m = build_mesh("hybrid:2")
+    d = Discretization(m, 2, "GL")
+    st0 = d.project(cavity_fields, 0.0)
+    dtl = local_timesteps(d, 0.5)
+    plan = assign_mrab_levels(dtl, 3, m, cfl=0.5)
+    T = 8 * 4 * plan.dt_min
+    s, drv = mrab_run(d, plan, {t: v.copy() for t, v in st0.items()}, T)
+    for t in d.types:
+        td[f"mrab/{t}"] = s[t]
+        td[f"mrab/levels/{t}"] = plan.levels[t]
+        td[f"mrab/evals/{t}"] = drv.rhs_evals[t]
+    td["mrab/dt_min"] = np.array(plan.dt_min)
+    td["mrab/T"] = np.array(T)
+    np.savez_compressed(os.path.join(HERE, "trajectories.npz"), **td)
+    np.savez_compressed(os.path.join(HERE, "meta.npz"), **{k: np.array(v) for k, v in out.items()})
+    print("golden fixtures written to", HERE)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

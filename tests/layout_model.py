@@ -1,0 +1,216 @@
+"""Numpy model of the device kernels over the exact packed layout
+(device.pack_mesh): same tables, same index arithmetic, vectorised over
+elements.  Lets the CPU suite check the compact HBM layout, the face
+permutations and the nodal-face lifts against the oracle without a GPU."""
+
+import numpy as np
+
+NAMES = ["hex", "wedge", "pyramid", "tet"]
+BND = 0x200
+
+
+def _dims(N):
+    n1 = N + 1
+    return dict(N1=n1, NFQ=n1 * n1, NFN=(N + 1) * (N + 2) // 2)
+
+
+def face_layout(t, N):
+    """[(face type, offset, count)] of the device face-point ordering."""
+    d = _dims(N)
+    if t == "hex":
+        return [("quad", f * d["NFQ"], d["NFQ"]) for f in range(6)]
+    if t == "tet":
+        return [("tri", f * d["NFN"], d["NFN"]) for f in range(4)]
+    if t == "wedge":
+        return ([("tri", f * d["NFN"], d["NFN"]) for f in range(2)]
+                + [("quad", 2 * d["NFN"] + f * d["NFQ"], d["NFQ"]) for f in range(3)])
+    return ([("quad", 0, d["NFQ"])]
+            + [("tri", d["NFQ"] + f * d["NFN"], d["NFN"]) for f in range(4)])
+
+
+def own_traces(pack, t, q, N, sem):
+    """(K, 4, Nfp) traces at the device face points, as the kernels form them."""
+    P = pack["types"][t]
+    if t == "tet":
+        return q[:, :, P["iop"][0]]
+    if t == "hex":
+        tab = P["iop"][0]
+        base, stride, end = tab[:, 0], tab[:, 1], tab[:, 2]
+        if sem:
+            return q[:, :, base + np.where(end == 1, N, 0) * stride]
+        Vend = P["op"][1]
+        out = 0.0
+        for l in range(N + 1):
+            out = out + Vend[end, l][None, None, :] * q[:, :, base + l * stride]
+        return out
+    ET = P["op"][5]                                    # (Np, Nfp)
+    tr = q @ ET
+    if t == "wedge":
+        tr = tr * P["geo"][:, 9][:, None, None]
+    return tr
+
+
+def _hex_metric(X, r, s, t):
+    """X (K, 8, 3) -> G (K, 3, 3) [c][x], J (K,) at one reference point."""
+    sg = np.array([[-1, -1, -1], [1, -1, -1], [1, 1, -1], [-1, 1, -1],
+                   [-1, -1, 1], [1, -1, 1], [1, 1, 1], [-1, 1, 1]], float)
+    p = np.array([r, s, t])
+    fac = 0.5 * (1 + sg * p)
+    g = np.empty((8, 3))
+    g[:, 0] = 0.5 * sg[:, 0] * fac[:, 1] * fac[:, 2]
+    g[:, 1] = 0.5 * sg[:, 1] * fac[:, 0] * fac[:, 2]
+    g[:, 2] = 0.5 * sg[:, 2] * fac[:, 0] * fac[:, 1]
+    F = np.einsum("kvx,vc->kxc", X, g)
+    return np.linalg.inv(F), np.linalg.det(F)
+
+
+_HEX_FV = [(0, 4, 7, 3), (1, 2, 6, 5), (0, 1, 5, 4), (2, 3, 7, 6), (0, 3, 2, 1), (4, 5, 6, 7)]
+
+
+def rhs(pack, disc, state):
+    """dU/dtau of every type from the packed layout (fp64)."""
+    N = disc.N
+    sem = disc.formulation.kind == "SEM"
+    d = _dims(N)
+    q = {t: np.asarray(state[t], dtype=float) for t in disc.types}
+    traces = {t: own_traces(pack, t, q[t], N, sem) for t in disc.types}
+    out = {}
+    for t in disc.types:
+        P = pack["types"][t]
+        K = P["K"]
+        Np = q[t].shape[2]
+        geo, mat = P["geo"], P["mat"]
+        acc = np.zeros((K, 4, Np))
+        # ---------------- volume
+        if t == "tet" or t == "pyramid":
+            G = geo[:, :9].reshape(K, 3, 3)
+            v = np.einsum("kcx,kxn->kcn", G, q[t][:, 1:])
+            DT = P["op"][0]                     # [c][m][n] = D_c[n][m]
+            dp = np.einsum("cmn,km->kcn", DT, q[t][:, 0])
+            if t == "pyramid" and P["form"] == "skew":
+                acc[:, 0] = np.einsum("cmn,kcm->kn", P["op"][1], v)
+            else:
+                acc[:, 0] = -np.einsum("cmn,kcm->kn", DT, v)
+            acc[:, 1:] = -np.einsum("kcx,kcn->kxn", G, dp)
+        elif t == "wedge":
+            G = geo[:, :9].reshape(K, 3, 3)
+            VT, D3T, V, D3, wq = P["op"][0], P["op"][1], P["op"][2], P["op"][3], P["op"][4]
+            U = q[t][:, 1:] @ VT                                  # (K,3,NQ)
+            dp = np.einsum("cmq,km->kcq", D3T, q[t][:, 0])
+            gp = np.einsum("kcx,kcq->kxq", G, dp) * wq
+            up = np.einsum("kcx,kxq->kcq", G, U) * wq
+            acc[:, 1:] = -(gp @ V)
+            acc[:, 0] = np.einsum("cqn,kcq->kn", D3, up)
+        else:  # hex
+            n1 = d["N1"]
+            X = geo.reshape(K, 8, 3)
+            x1 = P["op"][4]
+            D1 = P["op"][0]
+            u = q[t].reshape(K, 4, n1, n1, n1)
+            der = [np.einsum("il,kflmn->kfimn", D1, u), np.einsum("jl,kfiln->kfijn", D1, u),
+                   np.einsum("ml,kfijl->kfijm", D1, u)]
+            minv = np.empty((K, Np))
+            for n in range(Np):
+                i, j, k = n // (n1 * n1), (n // n1) % n1, n % n1
+                G, J = _hex_metric(X, x1[i], x1[j], x1[k])
+                dd = np.stack([der[c][:, :, i, j, k] for c in range(3)], axis=2)  # (K,4,3)
+                acc[:, 1:, n] = -np.einsum("kcx,kc->kx", G, dd[:, 0])
+                acc[:, 0, n] = -np.einsum("kcx,kxc->k", G, dd[:, 1:])
+                w1 = P["op"][2]
+                minv[:, n] = 1.0 / (w1[i] * w1[j] * w1[k] * J)
+        # ---------------- surface
+        lay = face_layout(t, N)
+        nfp = lay[-1][1] + lay[-1][2]
+        flux = np.zeros((K, 4 if t == "hex" else 2, nfp))
+        zm = mat[:, 2]
+        for f, (ft, off, cnt) in enumerate(lay):
+            own = traces[t][:, :, off:off + cnt]
+            code = P["nbr_code"][:, f]
+            k2 = P["nbr_elem"][:, f]
+            oth = np.empty_like(own)
+            zp = zm.copy()
+            b = (code & BND) != 0
+            oth[b, 0] = -own[b, 0]
+            oth[b, 1:] = own[b, 1:]
+            for tid2, t2 in enumerate(NAMES):
+                sel = (~b) & ((code & 3) == tid2)
+                if not sel.any():
+                    continue
+                f2 = (code[sel] >> 2) & 7
+                pc = (code[sel] >> 5) & 15
+                perm = (pack["perm_tri"] if ft == "tri" else pack["perm_quad"])[pc]   # (n, cnt)
+                lay2 = face_layout(t2, N)
+                off2 = np.array([lay2[x][1] for x in f2])
+                cols = off2[:, None] + perm
+                tr2 = traces[t2][k2[sel]]                                      # (n,4,nfp2)
+                oth[sel] = np.take_along_axis(tr2, np.repeat(cols[:, None, :], 4, axis=1), axis=2)
+                zp[sel] = pack["types"][t2]["mat"][k2[sel], 2]
+            avg = 0.5 * (zm + zp)
+            tp = disc.penalty_scale / avg
+            tu = disc.penalty_scale * avg
+            if t == "hex":
+                # per-point normal and Js from the face vertices
+                X = geo.reshape(K, 8, 3)[:, list(_HEX_FV[f])]
+                x1 = P["op"][4]
+                n1 = d["N1"]
+                jj = np.arange(cnt)
+                xi, eta = x1[jj // n1], x1[jj % n1]
+                g1 = np.stack([-(1 - eta), (1 - eta), (1 + eta), -(1 + eta)]) * 0.25
+                g2 = np.stack([-(1 - xi), -(1 + xi), (1 + xi), (1 - xi)]) * 0.25
+                t1 = np.einsum("kvx,vp->kpx", X, g1)
+                t2_ = np.einsum("kvx,vp->kpx", X, g2)
+                nv = np.cross(t1, t2_)
+                Js = np.linalg.norm(nv, axis=2)
+                nrm = nv / Js[..., None]                                     # (K,cnt,3)
+                w1 = P["op"][2]
+                scale = w1[jj // n1] * w1[jj % n1] * Js
+            else:
+                base = 10 if t == "wedge" else 9
+                nrm = np.repeat(geo[:, base + 4 * f: base + 4 * f + 3][:, None, :], cnt, axis=1)
+                scale = np.repeat(geo[:, base + 4 * f + 3][:, None], cnt, axis=1)
+            unm = np.einsum("kpx,kxp->kp", nrm, own[:, 1:])
+            unp = np.einsum("kpx,kxp->kp", nrm, oth[:, 1:])
+            dp_ = oth[:, 0] - own[:, 0]
+            dun = unp - unm
+            skew = P["form"] == "skew"
+            fp = (0.5 * tp[:, None] * dp_ - 0.5 * (unp + unm)) if skew else \
+                0.5 * (tp[:, None] * dp_ - dun)
+            fu = 0.5 * (tu[:, None] * dun - dp_)
+            if t == "hex":
+                flux[:, 0, off:off + cnt] = fp * scale
+                flux[:, 1:, off:off + cnt] = np.moveaxis(nrm, 2, 1) * (fu * scale)[:, None, :]
+            else:
+                flux[:, 0, off:off + cnt] = fp * scale
+                flux[:, 1, off:off + cnt] = fu * scale
+        # ---------------- lift
+        if t == "hex":
+            n1 = d["N1"]
+            Vend = P["op"][1]
+            nfp_tab = P["iop"][1]
+            lift = np.zeros_like(acc)
+            for n in range(Np):
+                idx = (n // (n1 * n1), (n // n1) % n1, n % n1)
+                for f in range(6):
+                    axis, end = f >> 1, f & 1
+                    l = idx[axis]
+                    if sem:
+                        if l != (N if end else 0):
+                            continue
+                        w = 1.0
+                    else:
+                        w = Vend[end, l]
+                    pt = nfp_tab[f, n]
+                    lift[:, :, n] += w * flux[:, :, f * d["NFQ"] + pt]
+            acc += lift * minv[:, None, :]
+        else:
+            LT = P["op"][1] if t == "tet" else P["op"][6]          # (Nfp, Np)
+            base = 10 if t == "wedge" else 9
+            for f, (ft, off, cnt) in enumerate(lay):
+                tp_ = flux[:, 0, off:off + cnt] @ LT[off:off + cnt]
+                tu_ = flux[:, 1, off:off + cnt] @ LT[off:off + cnt]
+                acc[:, 0] += tp_
+                acc[:, 1:] += geo[:, base + 4 * f: base + 4 * f + 3][:, :, None] * tu_[:, None, :]
+        acc[:, 0] *= mat[:, 0][:, None]
+        acc[:, 1:] *= mat[:, 1][:, None, None]
+        out[t] = acc
+    return out

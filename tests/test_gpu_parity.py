@@ -1,0 +1,130 @@
+"""Device kernels (through the C ABI) against the reference's outputs and
+the CPU oracle.  Tolerances: fp64 1e-12 per RHS (max-norm, relative), 1e-10
+relative L2 after 100 steps (north star); fp32 1e-4."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from conftest import RHS_CASES, build_mesh, load_golden, make_case, rel_err
+
+pytestmark = pytest.mark.gpu
+
+RHS = load_golden("rhs")
+TRAJ = load_golden("trajectories")
+
+
+def _l2rel(a, b):
+    num = sum(float(np.sum((np.asarray(a[t]) - np.asarray(b[t])) ** 2)) for t in b)
+    den = sum(float(np.sum(np.asarray(b[t]) ** 2)) for t in b)
+    return np.sqrt(num / den)
+
+
+@pytest.mark.parametrize("case", range(len(RHS_CASES)))
+def test_rhs_fp64_matches_reference(case, native_lib):
+    d, st = make_case(case)
+    r = d.compute_rhs(st)                      # host arrays in/out: the e2e path
+    ref = {t: RHS[f"{case}/{t}"] for t in d.types}
+    assert rel_err(r, ref) < 1e-12
+
+
+@pytest.mark.parametrize("case", [0, 2, 5, 6, 14])
+def test_rhs_fp32(case, native_lib):
+    d, st = make_case(case, dtype=torch.float32)
+    r = d.compute_rhs(st)
+    ref = {t: RHS[f"{case}/{t}"] for t in d.types}
+    assert _l2rel(r, ref) < 1e-4
+
+
+@pytest.mark.parametrize("N", [1, 2, 3, 4, 5, 6, 7])
+@pytest.mark.parametrize("form", ["GL", "SEM"])
+def test_rhs_all_orders_vs_oracle(N, form, native_lib):
+    from paper_1507_02557_b200.dg import Discretization
+    from conftest import set_random_materials
+    m = build_mesh("hybrid:2")
+    set_random_materials(m, 11)
+    d = Discretization(m, N, form)
+    rng = np.random.default_rng(100 + N)
+    st = {t: rng.standard_normal((d.n_elems[t], 4, d.ops[t].Np)) for t in d.types}
+    assert rel_err(d.compute_rhs(st), oracle.compute_rhs(d, st)) < 1e-11
+
+
+def test_device_tensors_stay_resident(native_lib):
+    d, st = make_case(6)
+    q = d.to_device(st)
+    out = d.compute_rhs(q)
+    assert all(v.is_cuda for v in out.values())
+    ref = {t: RHS[f"6/{t}"] for t in d.types}
+    assert rel_err({t: v.cpu().numpy() for t, v in out.items()}, ref) < 1e-12
+
+
+def test_subset_launch_equals_full(native_lib):
+    d, st = make_case(6)
+    q = d.to_device(st)
+    full = d.rhs_device(q)
+    part = d.zeros_state()
+    lists = [None] * 4
+    from paper_1507_02557_b200.operators import TYPE_ID
+    for t in d.types:
+        lists[TYPE_ID[t]] = torch.arange(0, d.n_elems[t], 2, dtype=torch.int32, device=d.device)
+    d.rhs_device(q, out=part, subset=lists)
+    for t in d.types:
+        assert torch.equal(part[t][::2], full[t][::2])
+        assert torch.count_nonzero(part[t][1::2]) == 0
+
+
+def _cavity(spec, N, form, **kw):
+    from paper_1507_02557_b200.app import cavity_fields
+    from paper_1507_02557_b200.dg import Discretization
+    d = Discretization(build_mesh(spec), N, form, **kw)
+    return d, d.project(cavity_fields, 0.0)
+
+
+@pytest.mark.parametrize("tag,spec,N,form", [("c1_sem", "hex:4", 2, "SEM"),
+                                             ("c1_gl", "hex:4", 2, "GL")])
+def test_ab3_100_steps(tag, spec, N, form, native_lib):
+    from paper_1507_02557_b200.timeint import single_rate_run
+    d, st0 = _cavity(spec, N, form)
+    dt = float(TRAJ[f"{tag}/dt"])
+    s = single_rate_run(d, st0, dt, 100 * dt)
+    ref = {t: TRAJ[f"{tag}/ab3/{t}"] for t in d.types}
+    assert _l2rel(s, ref) < 1e-10
+
+
+@pytest.mark.parametrize("tag,spec,N,form", [("c1_sem", "hex:4", 2, "SEM"),
+                                             ("c1_gl", "hex:4", 2, "GL"),
+                                             ("hyb4_gl", "hybrid:4", 3, "GL")])
+def test_lsrk_100_steps(tag, spec, N, form, native_lib):
+    from paper_1507_02557_b200.app import cavity_fields
+    from paper_1507_02557_b200.timeint import lsrk_run
+    d, st0 = _cavity(spec, N, form)
+    dt = float(TRAJ[f"{tag}/dt"])
+    s = lsrk_run(d, st0, dt, 100 * dt)
+    ref = {t: TRAJ[f"{tag}/lsrk/{t}"] for t in d.types}
+    assert _l2rel(s, ref) < 1e-10
+    err = d.l2_error(s, cavity_fields, 100 * dt)
+    np.testing.assert_allclose(err["total"], TRAJ[f"{tag}/lsrk/err"][2], rtol=1e-8)
+
+
+def test_lsrk_fp32_100_steps(native_lib):
+    from paper_1507_02557_b200.timeint import lsrk_run
+    d, st0 = _cavity("hybrid:4", 3, "GL", dtype=torch.float32)
+    dt = float(TRAJ["hyb4_gl/dt"])
+    s = lsrk_run(d, st0, dt, 100 * dt)
+    ref = {t: TRAJ[f"hyb4_gl/lsrk/{t}"] for t in d.types}
+    assert _l2rel(s, ref) < 1e-4
+
+
+def test_mrab_matches_reference(native_lib):
+    from paper_1507_02557_b200.stability import TimestepPlan
+    from paper_1507_02557_b200.timeint import mrab_run
+    d, st0 = _cavity("hybrid:2", 2, "GL")
+    levels = {t: TRAJ[f"mrab/levels/{t}"] for t in d.types}
+    dtl = {t: np.full(d.n_elems[t], 1.0) for t in d.types}
+    plan = TimestepPlan(dtl, levels, 3, 0.5, list(d.types))
+    plan.dt_min = float(TRAJ["mrab/dt_min"])
+    s, drv = mrab_run(d, plan, st0, float(TRAJ["mrab/T"]))
+    for t in d.types:
+        np.testing.assert_array_equal(drv.rhs_evals[t], TRAJ[f"mrab/evals/{t}"])
+    ref = {t: TRAJ[f"mrab/{t}"] for t in d.types}
+    assert _l2rel(s, ref) < 1e-10
