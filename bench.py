@@ -1,0 +1,347 @@
+#!/usr/bin/env python
+"""Benchmark: LSRK-45 steps of the DG acoustic RHS + update on B200.
+
+Headline workload (BASELINE.json metric "GDOF·stage/s per LSRK step",
+configs[2]): the reference's structured hybrid cube hybrid:38 (14,440 hex,
+25,992 wedge, 7,220 pyramid, 158,840 tet = 206,492 elements), N=3, GL,
+fp64, cavity-mode initial data projected on the host, dt from the
+reference's local timestep rule (CFL 0.5).  One step = 5 RHS stages, each
+one fused kernel launch per element type; the timed loop replays a CUDA
+graph of one step.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+                  [--mesh hybrid:38 --order 3 --form GL --dtype f64]
+
+Multi-GPU (torchrun): every rank advances its own copy of the workload
+(weak scaling, no data-path collective yet: the partitioned halo path is
+listed as next work in DESIGN.md); timing is the max over ranks.
+"""
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "GDOF·stage/s per LSRK step (N=1..5, hybrid mesh, 1/2/4/8 B200); kernel GB/s vs HBM"
+UNIT = "GDOF*stage/s"
+GEO_WORDS = {"hex": 24, "wedge": 30, "pyramid": 29, "tet": 25}
+NFACES = {"hex": 6, "wedge": 5, "pyramid": 5, "tet": 4}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=40)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--mesh", default="hybrid:38")
+    ap.add_argument("--order", type=int, default=3)
+    ap.add_argument("--form", default="GL", choices=["GL", "SEM"])
+    ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
+    ap.add_argument("--cpu-mesh", default=None, help="reference-arm sample mesh")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true")
+    return ap.parse_args()
+
+
+def build_mesh(spec):
+    from paper_1507_02557_b200.app import build_mesh as bm
+    return bm(spec)
+
+
+def n_dof(disc):
+    return disc.n_dof
+
+
+# ------------------------------------------------------------------ CPU arm
+
+def cpu_sample_mesh(args):
+    """Bounded sample of the workload for the CPU oracle: the same band
+    layout, order and formulation on a coarser cube (per-DOF rate)."""
+    if args.cpu_mesh:
+        return args.cpu_mesh
+    kind, n = args.mesh.split(":")
+    n = int(n)
+    return f"{kind}:{min(n, 10)}"
+
+
+def run_cpu_oracle(args, steps, warmup):
+    """The reference's algorithm (oracle/ numpy port) for LSRK steps on the
+    host cores; returns (value GDOF*stage/s, seconds/step, sample, cores)."""
+    import oracle
+    from paper_1507_02557_b200.app import cavity_fields
+    from paper_1507_02557_b200.dg import Discretization
+    from paper_1507_02557_b200.stability import local_timesteps
+    spec = cpu_sample_mesh(args)
+    d = Discretization(build_mesh(spec), args.order, args.form)
+    st = d.project(cavity_fields, 0.0)
+    dt = min(float(v.min()) for v in local_timesteps(d, 0.5).values())
+    d._ensure_reference_layout()
+    rhs = lambda s, tau: oracle.compute_rhs(d, s)
+    for _ in range(warmup):
+        st = oracle.lsrk_run(rhs, st, dt, dt)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        st = oracle.lsrk_run(rhs, st, dt, dt)
+    el = time.perf_counter() - t0
+    value = d.n_dof * 5 * steps / el / 1e9
+    cores = int(os.environ.get("OPENBLAS_NUM_THREADS", os.cpu_count() or 1))
+    sample = (f"{spec} N={args.order} {args.form} fp64 ({sum(d.n_elems.values())} elements, "
+              f"{d.n_dof} DOF), {steps} LSRK steps (5 oracle RHS each)")
+    return value, el / steps, sample, cores
+
+
+def reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    steps = max(1, min(args.steps, 5))
+    warm = 1
+    value, sps, sample, cores = run_cpu_oracle(args, steps, warm)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+            "n_gpus": args.gpus, "steps": steps, "warmup": warm, "ms_per_step": sps * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (cavity eigenmode projected on the mesh)",
+            "config": {"workload": f"{args.mesh} N={args.order} {args.form} LSRK-45",
+                       "sample": sample},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ clocks
+
+class ClockSampler:
+    """SM clock + throttle reasons sampled with NVML during the timed region."""
+
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown", 0x1: "gpu_idle",
+               0x2: "applications_clocks_setting"}
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # pragma: no cover - NVML missing
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.01)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv is not None:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons)}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------ GPU arm
+
+def alg_bytes_per_elem(t, Np, s):
+    """Compulsory HBM traffic of one LSRK stage per element in this layout:
+    read q, read res, write res, write q_out (4 x 4 Np words), geometry
+    record, material record, neighbour index + code per face.  Neighbour
+    states are re-read from L2 (not counted)."""
+    return 4 * 4 * Np * s + GEO_WORDS[t] * s + 4 * s + 8 * NFACES[t]
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return reference_arm(args)
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl")
+    dev = torch.device("cuda", local)
+    from paper_1507_02557_b200 import _native as nat
+    from paper_1507_02557_b200.app import cavity_fields
+    from paper_1507_02557_b200.dg import Discretization
+    from paper_1507_02557_b200.operators import TYPE_ID
+    from paper_1507_02557_b200.stability import local_timesteps
+    from paper_1507_02557_b200.timeint import LSRK_A, LSRK_B, Stepper, lsrk_run
+
+    dtype = torch.float64 if args.dtype == "f64" else torch.float32
+    s_bytes = 8 if args.dtype == "f64" else 4
+    t_setup = time.perf_counter()
+    mesh = build_mesh(args.mesh)
+    disc = Discretization(mesh, args.order, args.form, dtype=dtype, device=dev)
+    host_state = disc.project(cavity_fields, 0.0)
+    dt = min(float(v.min()) for v in local_timesteps(disc, 0.5).values())
+    _ = disc.device_mesh
+    setup_s = time.perf_counter() - t_setup
+    S = Stepper(disc, host_state, "lsrk")
+    stream = torch.cuda.current_stream(dev)
+
+    # CUDA graphs of one step for each buffer parity
+    graphs = []
+    if not args.no_graph:
+        S.lsrk_step(dt)               # warm (sets kernel attributes outside capture)
+        S.lsrk_step(dt)
+        torch.cuda.synchronize()
+        cap = torch.cuda.Stream(dev)
+        for _ in range(2):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=cap):
+                S.lsrk_step(dt)
+            graphs.append(g)
+
+    def step(i):
+        if graphs:
+            graphs[i % 2].replay()
+        else:
+            S.lsrk_step(dt)
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for i in range(args.steps):
+            step(args.warmup + i)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    total_dof = disc.n_dof * world
+    value = total_dof * 5 * args.steps / (ms * 1e-3) / 1e9
+    assert all(torch.isfinite(S.q[t]).all() for t in disc.types), "state diverged"
+
+    # ---- per-type kernel time (roofline of the dominant kernel)
+    per_type = {}
+    L = nat.lib()
+    for t in disc.types:
+        lists = [torch.zeros(0, dtype=torch.int32, device=dev)] * 4
+        lists[TYPE_ID[t]] = None
+        sub = nat.subset(lists)
+        F = lambda x: nat.fields(disc.slots(x))
+        reps = 20
+        for _ in range(3):
+            nat.check(L.hw_lsrk_stage(disc.device_mesh.struct, F(S.q), F(S.q2), F(S.res),
+                                      LSRK_A[1], LSRK_B[1], 0.0, sub, stream.cuda_stream))
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(reps):
+            nat.check(L.hw_lsrk_stage(disc.device_mesh.struct, F(S.q), F(S.q2), F(S.res),
+                                      LSRK_A[1], LSRK_B[1], 0.0, sub, stream.cuda_stream))
+        b.record(stream)
+        torch.cuda.synchronize()
+        us = a.elapsed_time(b) * 1e3 / reps
+        Np = disc.ops[t].Np
+        nbytes = disc.n_elems[t] * alg_bytes_per_elem(t, Np, s_bytes)
+        per_type[t] = {"us_per_launch": us, "elements": disc.n_elems[t],
+                       "alg_bytes": nbytes, "GBps": nbytes / (us * 1e-6) / 1e9}
+    dom = max(per_type, key=lambda t: per_type[t]["us_per_launch"])
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    prof = {}
+    try:
+        prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+    except Exception:
+        pass
+    traffic = prof.get(f"{args.mesh}/N{args.order}/{args.form}/{args.dtype}/{dom}")
+    roof = {"bound": "hbm", "kernel": f"{dom}_kernel<{args.order},{'double' if s_bytes == 8 else 'float'}>",
+            "achieved": per_type[dom]["GBps"], "peak": hbm, "unit": "GB/s",
+            "frac": per_type[dom]["GBps"] / hbm, "traffic": traffic,
+            "peak_source": "measured (MEASURED_PEAKS.json hbm_gbs)" if "hbm_gbs" in peaks
+            else "fallback 6650 GB/s",
+            "per_type": per_type,
+            "step_share": {t: per_type[t]["us_per_launch"] * 5 / (ms * 1e3 / args.steps)
+                           for t in per_type}}
+
+    # ---- end-to-end through the public API: host numpy state in, host out
+    e2e_steps = max(2, min(args.steps, 20))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    out = lsrk_run(disc, host_state, dt, e2e_steps * dt * (1 - 1e-12))
+    t1 = time.perf_counter()
+    state_bytes = sum(v.nbytes for v in out.values()) * s_bytes // 8
+    e2e_val = disc.n_dof * world * 5 * e2e_steps / (t1 - t0) / 1e9
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, sps, sample, cores = run_cpu_oracle(args, 3, 1)
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": args.dtype,
+                "data": "synthetic (cavity eigenmode projected on the mesh), per-rank replica",
+                "config": {"workload": f"{args.mesh} N={args.order} {args.form} LSRK-45 "
+                                       f"(configs[2])",
+                           "elements": {t: disc.n_elems[t] for t in disc.types},
+                           "n_dof_per_rank": disc.n_dof, "dt": dt,
+                           "l2_policy": "inputs larger than L2 (state+res+q_out "
+                                        f"{3 * disc.n_dof * s_bytes / 1e6:.0f} MB > 126 MB)",
+                           "cuda_graph": bool(graphs), "setup_s": setup_s,
+                           "parallelism": f"replica x{world}"},
+                "gpu_launches": args.steps * 5 * len(disc.types),
+                "clocks": clk.summary(), "roofline": roof,
+                "e2e": {"value": e2e_val, "unit": UNIT,
+                        "h2d_bytes_per_step": state_bytes / e2e_steps,
+                        "d2h_bytes_per_step": state_bytes / e2e_steps,
+                        "steps": e2e_steps,
+                        "api": "timeint.lsrk_run(disc, numpy_state, dt, T) host in/out"},
+                "cpu_baseline": cpu}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -23,9 +23,12 @@ static int check_launch(const char* what) {
   return 0;
 }
 
+// Raise the dynamic shared-memory limit once per kernel instantiation (the
+// call is not a stream operation; doing it once keeps launches capturable).
 template <typename KernelT>
 static int set_smem(KernelT kernel, size_t bytes) {
-  if (bytes > 48 * 1024) {
+  static bool done = false;
+  if (!done && bytes > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)bytes);
     if (e != cudaSuccess) {
@@ -33,6 +36,7 @@ static int set_smem(KernelT kernel, size_t bytes) {
       return 3;
     }
   }
+  done = true;
   return 0;
 }
 

@@ -23,8 +23,8 @@ from . import basis as bas
 from . import _native as nat
 from .operators import TYPE_ID, build_operators, face_symmetry_perms
 from .quadrature import element_rule
-from .refelem import (FACES, face_geometry_batch, geometric_factors_batch,
-                      inverse_duffy_map, duffy_map)
+from .refelem import (FACES, duffy_map, face_geometry_batch, geometric_factors_batch,
+                      inverse_duffy_map, jacobian_det, map_points)
 
 __all__ = ["Formulation", "TABLE_FORMS", "flux_penalties", "Discretization",
            "discrete_energy", "zero_state", "FIELDS"]
@@ -251,8 +251,13 @@ class Discretization:
         key = (t, which)
         if key not in self._cub:
             rule = element_rule(t, self.N if which == "cub" else self.N + 2)
-            x, J, _, _ = geometric_factors_batch(t, self.mesh.element_vertices(t),
-                                                 rule.collapsed, label=t)
+            verts = self.mesh.element_vertices(t)
+            x = map_points(t, verts, rule.collapsed)
+            if t == "tet":   # affine: one determinant per element
+                J = np.repeat(jacobian_det(t, verts, rule.collapsed[:1]), len(rule.weights),
+                              axis=1)
+            else:
+                J = jacobian_det(t, verts, rule.collapsed)
             self._cub[key] = (rule.weights, self._basis_values(t, rule.collapsed), x, J)
         return self._cub[key]
 
@@ -275,8 +280,7 @@ class Discretization:
                 n1 = self.ops["hex"].nodes1d
                 i, j, k = np.meshgrid(n1, n1, n1, indexing="ij")
                 pts = np.column_stack([i.ravel(), j.ravel(), k.ravel()])
-                x, _, _, _ = geometric_factors_batch("hex", self.mesh.element_vertices("hex"),
-                                                     pts)
+                x = map_points("hex", self.mesh.element_vertices("hex"), pts)
                 state[t] = np.moveaxis(np.asarray(fields_fn(x, time)), -1, 1)
                 continue
             w, V, x, J = self._cubature(t, "cub")
@@ -287,8 +291,7 @@ class Discretization:
                 state[t] = (vals * (w[None, :] * np.sqrt(J))[:, None, :]) @ V
             else:
                 raw = (vals * (w[None, :] * J)[:, None, :]) @ V
-                _, Jr, _, _ = geometric_factors_batch(t, self.mesh.element_vertices(t),
-                                                      self.ops[t].level_abc, label=t)
+                Jr = jacobian_det(t, self.mesh.element_vertices(t), self.ops[t].level_abc)
                 state[t] = raw / Jr[:, None, :]
         return state
 

@@ -14,6 +14,7 @@ __all__ = [
     "duffy_map", "inverse_duffy_map", "shape_functions_abc",
     "shape_gradients_rst", "geometric_factors_batch",
     "face_quadrature_points", "face_geometry_batch", "face_shape2d",
+    "map_points", "jacobian_det",
 ]
 
 ELEMENT_TYPES = ("hex", "wedge", "pyramid", "tet")
@@ -186,6 +187,24 @@ def geometric_factors_batch(elem_type, verts, abc, label="element"):
         dJ = J[..., None] * np.einsum("kprx,kxrc->kpc", G, dF)
         gradJ = np.einsum("kpc,kpcx->kpx", dJ, G)
     return x, J, G, gradJ
+
+
+def map_points(elem_type, verts, abc):
+    """Physical positions (K, P, 3) of collapsed points (no metric work)."""
+    return np.einsum("kvx,pv->kpx", np.asarray(verts, dtype=float),
+                     shape_functions_abc(elem_type, abc))
+
+
+def jacobian_det(elem_type, verts, abc):
+    """det(dx/dr) (K, P) without forming the inverse."""
+    F = np.einsum("kvx,pvr->kpxr", np.asarray(verts, dtype=float),
+                  shape_gradients_rst(elem_type, abc))
+    J = (F[..., 0, 0] * (F[..., 1, 1] * F[..., 2, 2] - F[..., 1, 2] * F[..., 2, 1])
+         - F[..., 0, 1] * (F[..., 1, 0] * F[..., 2, 2] - F[..., 1, 2] * F[..., 2, 0])
+         + F[..., 0, 2] * (F[..., 1, 0] * F[..., 2, 1] - F[..., 1, 1] * F[..., 2, 0]))
+    if np.any(J <= 0):
+        raise InvalidElementError(f"nonpositive Jacobian in {elem_type} (min J = {J.min():.3e})")
+    return J
 
 
 def face_shape2d(face_type, p):

@@ -12,7 +12,7 @@ from . import basis as bas
 from .operators import face_rule_2d
 from .quadrature import element_rule, gauss_lobatto_1d
 from .refelem import (FACES, REF_VERTS, face_geometry_batch, face_quadrature_points,
-                      geometric_factors_batch, inverse_duffy_map)
+                      inverse_duffy_map, jacobian_det)
 
 __all__ = ["computed_trace_constant", "analytic_trace_constant", "local_timesteps",
            "material_constant", "TimestepPlan", "assign_mrab_levels"]
@@ -88,20 +88,32 @@ def material_constant(disc, t):
 
 
 def _jacobian_norms(disc, t):
+    """Maxima of J, 1/J, Js (and Js/J_face for wedges) over the quadrature
+    points (hybridwave/stability.py:215-226).  Triangle faces are planar, so
+    Js is evaluated once per face; J at wedge face points only when the
+    wedge is not affine."""
     verts = disc.mesh.element_vertices(t)
     cub = element_rule(t, disc.N)
-    _, cJ, _, _ = geometric_factors_batch(t, verts, cub.collapsed, label=t)
+    cJ = jacobian_det(t, verts, cub.collapsed if t != "tet" else cub.collapsed[:1])
     Jmax, Jinv = cJ.max(axis=1), (1.0 / cJ).max(axis=1)
+    affine = np.all((cJ.max(axis=1) - cJ.min(axis=1)) <= 1e-13 * cJ.max(axis=1))
     op = disc.ops[t]
     Jsmax = np.zeros(len(verts))
     JsoJ = np.zeros(len(verts)) if t == "wedge" else None
-    for f, p2 in enumerate(op.face_pts2d):
+    for f, (ftype, _) in enumerate(FACES[t]):
+        p2 = op.face_pts2d[f]
+        if ftype == "tri":
+            p2 = p2[:1]
         _, Js, _ = face_geometry_batch(t, verts, f, p2)
         Jsmax = np.maximum(Jsmax, Js.max(axis=1))
         if t == "wedge":
-            sl = slice(op.face_offsets[f], op.face_offsets[f + 1])
-            _, Jf, _, _ = geometric_factors_batch(t, verts, inverse_duffy_map(t, op.face_rst[sl]))
-            JsoJ = np.maximum(JsoJ, (Js / Jf).max(axis=1))
+            if affine:
+                JsoJ = np.maximum(JsoJ, Js.max(axis=1) / cJ[:, 0])
+            else:
+                sl = slice(op.face_offsets[f], op.face_offsets[f + 1])
+                _, Js_all, _ = face_geometry_batch(t, verts, f, op.face_pts2d[f])
+                Jf = jacobian_det(t, verts, inverse_duffy_map(t, op.face_rst[sl]))
+                JsoJ = np.maximum(JsoJ, (Js_all / Jf).max(axis=1))
     return Jmax, Jinv, Jsmax, JsoJ
 
 
