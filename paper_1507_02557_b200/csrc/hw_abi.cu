@@ -1,7 +1,9 @@
 // C ABI of the sm_100a DG acoustic hot path (see include/hybridwave_b200.h).
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <string>
+#include <unordered_set>
 
 #include "hw_kernels.cuh"
 
@@ -27,8 +29,12 @@ static int check_launch(const char* what) {
 // call is not a stream operation; doing it once keeps launches capturable).
 template <typename KernelT>
 static int set_smem(KernelT kernel, size_t bytes) {
-  static bool done = false;
-  if (!done && bytes > 48 * 1024) {
+  static std::mutex mu;
+  static std::unordered_set<const void*> done;
+  std::lock_guard<std::mutex> lock(mu);
+  const void* key = (const void*)kernel;
+  if (done.count(key)) return 0;
+  if (bytes > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)bytes);
     if (e != cudaSuccess) {
@@ -36,7 +42,7 @@ static int set_smem(KernelT kernel, size_t bytes) {
       return 3;
     }
   }
-  done = true;
+  done.insert(key);
   return 0;
 }
 
@@ -50,10 +56,21 @@ static void subset_of(const hw_subset_t* sub, int t, int64_t K, const int32_t** 
   }
 }
 
+template <int N, int T, typename R>
+static int launch_dense(const hw_mesh_t& M, const hw_fields_t& Q, const Epi& E,
+                        const int32_t* list, int64_t n, cudaStream_t st) {
+  using L = Smem<N, T, R>;
+  int rc;
+  if ((rc = set_smem(dense_kernel<N, T, R>, L::BYTES))) return rc;
+  dense_kernel<N, T, R><<<(unsigned)((n + L::EPB - 1) / L::EPB), NT, L::BYTES, st>>>(M, Q, E,
+                                                                                    list, n);
+  return check_launch("dense_kernel");
+}
+
 template <int N, typename R>
 static int launch_rhs_all(const hw_mesh_t& M, const hw_fields_t& Q, const Epi& E,
                           const hw_subset_t* sub, cudaStream_t st) {
-  int rc;
+  int rc = 0;
   for (int t = 0; t < HW_NTYPES; ++t) {
     const int64_t K = M.t[t].K;
     if (K <= 0) continue;
@@ -63,38 +80,18 @@ static int launch_rhs_all(const hw_mesh_t& M, const hw_fields_t& Q, const Epi& E
     if (n <= 0) continue;
     switch (t) {
       case HW_HEX: {
-        using K_ = HexK<N, R>;
-        const size_t smem = sizeof(R) * K_::SMEM;
-        if ((rc = set_smem(hex_kernel<N, R>, smem))) return rc;
-        hex_kernel<N, R><<<(unsigned)((n + K_::EPB - 1) / K_::EPB), NT, smem, st>>>(M, Q, E, list, n);
-        if ((rc = check_launch("hex_kernel"))) return rc;
+        using L = Smem<N, HW_HEX, R>;
+        if ((rc = set_smem(hex_kernel<N, R>, L::BYTES))) return rc;
+        hex_kernel<N, R><<<(unsigned)((n + L::EPB - 1) / L::EPB), NT, L::BYTES, st>>>(M, Q, E,
+                                                                                   list, n);
+        rc = check_launch("hex_kernel");
         break;
       }
-      case HW_WEDGE: {
-        using K_ = WedgeK<N, R>;
-        const size_t smem = sizeof(R) * K_::SMEM;
-        if ((rc = set_smem(wedge_kernel<N, R>, smem))) return rc;
-        wedge_kernel<N, R><<<(unsigned)((n + K_::EPB - 1) / K_::EPB), NT, smem, st>>>(M, Q, E, list, n);
-        if ((rc = check_launch("wedge_kernel"))) return rc;
-        break;
-      }
-      case HW_PYRAMID: {
-        using K_ = PyrK<N, R>;
-        const size_t smem = sizeof(R) * K_::SMEM;
-        if ((rc = set_smem(pyr_kernel<N, R>, smem))) return rc;
-        pyr_kernel<N, R><<<(unsigned)((n + K_::EPB - 1) / K_::EPB), NT, smem, st>>>(M, Q, E, list, n);
-        if ((rc = check_launch("pyr_kernel"))) return rc;
-        break;
-      }
-      case HW_TET: {
-        using K_ = TetK<N, R>;
-        const size_t smem = sizeof(R) * K_::SMEM;
-        if ((rc = set_smem(tet_kernel<N, R>, smem))) return rc;
-        tet_kernel<N, R><<<(unsigned)((n + K_::EPB - 1) / K_::EPB), NT, smem, st>>>(M, Q, E, list, n);
-        if ((rc = check_launch("tet_kernel"))) return rc;
-        break;
-      }
+      case HW_WEDGE: rc = launch_dense<N, HW_WEDGE, R>(M, Q, E, list, n, st); break;
+      case HW_PYRAMID: rc = launch_dense<N, HW_PYRAMID, R>(M, Q, E, list, n, st); break;
+      case HW_TET: rc = launch_dense<N, HW_TET, R>(M, Q, E, list, n, st); break;
     }
+    if (rc) return rc;
   }
   return 0;
 }

@@ -1,84 +1,359 @@
-// Fused per-element-type RHS + time-update kernels (sm_100a).
+// Fused per-element-type RHS + time-update kernels (sm_100a), v2.
 //
-// One launch per element type per stage.  A block owns EPB elements and
-// runs, with a block barrier between phases:
-//   load      q (4 x Np per element) and the per-element geometry record
-//   volume    strong/skew volume term with the mass inverse folded out
-//             (SURVEY.md 8a "algebraic cancellations")
-//   flux      own trace, neighbour trace (read from the neighbour's input
-//             state), upwind flux, scaled by the face Jacobian
-//   lift      face-to-volume lift, mass inverse, material scaling, and the
-//             epilogue (RHS / LSRK stage / AB step)
+// One launch per element type per stage.  A block owns EPB elements:
+//   P0 load       q, geometry record, material, neighbour links -> smem
+//   P1 stage      cp.async (LDGSTS) of every neighbour's face data and of
+//                 the LSRK residual -> smem; fire-and-forget, so the L2
+//                 round trips overlap the volume work below
+//   P2 volume     strong/skew volume term, mass inverse folded out
+//   P3 flux       own + neighbour traces from smem, upwind flux x face Jacobian
+//   P4 lift       face-to-volume lift, mass inverse, materials, epilogue
+//                 (RHS / LSRK stage / AB step)
 // Reference data flow: hybridwave/dg.py:299-506.
 #pragma once
 #include "hw_common.cuh"
 
 namespace hw {
 
-// ------------------------------------------------------------------ tet
-// Strong form (both formulations, hybridwave/dg.py:34-37, 401-421):
-//   rhs_p = -sum_c D_c (sum_x G[c][x] u_x),  rhs_u_x = -sum_c G[c][x] D_c p
-// then + (Js_f/J) LIFT_f flux_f, LIFT = invM_ref Vf^T W L (nodal faces).
-template <int N, typename R>
-struct TetK {
+__host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
+
+// ------------------------------------------------------------------ traits
+
+template <int N, int T>
+struct TT;
+
+template <int N>
+struct TT<N, HW_TET> {
   using D = Dims<N>;
-  static constexpr int NP = D::NP_TET, NFN = D::NFN, NFP = D::NFP_TET;
-  static constexpr int EPB = (NT / NP) > 0 ? (NT / NP) : 1;
-  static constexpr int S = (EPB * NP + NT - 1) / NT;
-  static constexpr int SQ = 0, SV = SQ + EPB * 4 * NP, SF = SV + EPB * 3 * NP,
-                       SG = SF + EPB * NFP * 2, SM = SG + EPB * GEO_TET,
-                       SMEM = SM + EPB * 4;
+  static constexpr int NP = D::NP_TET, NF = 4, NFP = D::NFP_TET, GEO = GEO_TET, GF = 9;
+  __host__ __device__ static constexpr bool tri(int) { return true; }
+  __host__ __device__ static constexpr int off(int f) { return f * D::NFN; }
+  __host__ __device__ static constexpr int cnt(int) { return D::NFN; }
+  // staging budget per face: tet neighbours only (the rare dense neighbours
+  // of a tet take the direct path, neighbour_trace)
+  __host__ __device__ static constexpr int stage(int) { return 4 * D::NFN; }
 };
 
-template <int N, typename R>
-__global__ void __launch_bounds__(NT) tet_kernel(hw_mesh_t M, hw_fields_t Q, Epi E,
-                                                 const int32_t* __restrict__ list,
-                                                 int64_t nwork) {
-  using K_ = TetK<N, R>;
-  constexpr int NP = K_::NP, NFN = K_::NFN, NFP = K_::NFP, EPB = K_::EPB, S = K_::S;
+template <int N>
+struct TT<N, HW_WEDGE> {
+  using D = Dims<N>;
+  static constexpr int NP = D::NP_WEDGE, NF = 5, NFP = D::NFP_WEDGE, GEO = GEO_WEDGE, GF = 10;
+  __host__ __device__ static constexpr bool tri(int f) { return f < 2; }
+  __host__ __device__ static constexpr int off(int f) {
+    return f < 2 ? f * D::NFN : 2 * D::NFN + (f - 2) * D::NFQ;
+  }
+  __host__ __device__ static constexpr int cnt(int f) { return f < 2 ? D::NFN : D::NFQ; }
+  __host__ __device__ static constexpr int stage(int f) {
+    return tri(f) ? 4 * cmax(D::NFN, cmax(D::NP_WEDGE, D::NP_PYR))
+                  : 4 * cmax(D::NFQ * D::N1, cmax(D::NP_WEDGE, D::NP_PYR));
+  }
+};
+
+template <int N>
+struct TT<N, HW_PYRAMID> {
+  using D = Dims<N>;
+  static constexpr int NP = D::NP_PYR, NF = 5, NFP = D::NFP_PYR, GEO = GEO_PYR, GF = 9;
+  __host__ __device__ static constexpr bool tri(int f) { return f > 0; }
+  __host__ __device__ static constexpr int off(int f) {
+    return f == 0 ? 0 : D::NFQ + (f - 1) * D::NFN;
+  }
+  __host__ __device__ static constexpr int cnt(int f) { return f == 0 ? D::NFQ : D::NFN; }
+  __host__ __device__ static constexpr int stage(int f) {
+    return tri(f) ? 4 * cmax(D::NFN, cmax(D::NP_WEDGE, D::NP_PYR))
+                  : 4 * cmax(D::NFQ * D::N1, cmax(D::NP_WEDGE, D::NP_PYR));
+  }
+};
+
+template <int N>
+struct TT<N, HW_HEX> {
+  using D = Dims<N>;
+  static constexpr int NP = D::NP_HEX, NF = 6, NFP = D::NFP_HEX, GEO = GEO_HEX, GF = 0;
+  __host__ __device__ static constexpr bool tri(int) { return false; }
+  __host__ __device__ static constexpr int off(int f) { return f * D::NFQ; }
+  __host__ __device__ static constexpr int cnt(int) { return D::NFQ; }
+  __host__ __device__ static constexpr int stage(int) {
+    return 4 * cmax(D::NFQ * D::N1, cmax(D::NP_WEDGE, D::NP_PYR));
+  }
+};
+
+template <int N, int T>
+__host__ __device__ constexpr int stage_off(int f) {
+  int s = 0;
+  for (int g = 0; g < f; ++g) s += TT<N, T>::stage(g);
+  return s;
+}
+
+template <int N, int T>
+__device__ __forceinline__ int face_of_point(int j, int& jj) {
+  using X = TT<N, T>;
+  int f = 0;
+#pragma unroll
+  for (int g = 1; g < X::NF; ++g)
+    if (j >= X::off(g)) f = g;
+  jj = j - X::off(f);
+  return f;
+}
+
+// ------------------------------------------------------------------ cp.async
+
+template <typename R>
+__device__ __forceinline__ void cp_async(R* smem, const R* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  if (sizeof(R) == 8)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+}
+
+// number of staged values for a neighbour of type t2
+template <int N>
+__device__ __forceinline__ int stage_count(int t2, bool sem) {
+  using D = Dims<N>;
+  switch (t2) {
+    case HW_TET: return 4 * D::NFN;
+    case HW_HEX: return sem ? 4 * D::NFQ : 4 * D::NFQ * D::N1;
+    case HW_WEDGE: return 4 * D::NP_WEDGE;
+    default: return 4 * D::NP_PYR;
+  }
+}
+
+// P1: one warp per (element, face) pair copies what the neighbour trace
+// needs: tet face-node values (4 x NFN), hex SEM face values (4 x NFQ), hex
+// GL normal lines (4 x NFQ x N1), or the whole wedge/pyramid state.
+template <int N, int T, typename R>
+__device__ __forceinline__ void stage_neighbours(const hw_mesh_t& M, const hw_fields_t& Q,
+                                                 const int* snc, const int* sne, int ne,
+                                                 R* st, bool sem) {
+  using X = TT<N, T>;
+  using D = Dims<N>;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int pr = warp; pr < ne * X::NF; pr += NT / 32) {
+    const int e = pr / X::NF, f = pr - e * X::NF;
+    const int code = snc[pr];
+    if (code & HW_NBR_BOUNDARY) continue;
+    const int t2 = HW_NBR_TYPE(code), f2 = HW_NBR_FACE(code);
+    if (stage_count<N>(t2, sem) > X::stage(f)) continue;   // direct path later
+    const int k2 = sne[pr];
+    R* dst = st + e * stage_off<N, T>(X::NF) + stage_off<N, T>(f);
+    if (t2 == HW_TET) {
+      const R* q2 = (const R*)Q.p[HW_TET] + (size_t)k2 * 4 * D::NP_TET;
+      const int* fn = M.t[HW_TET].iop[0] + f2 * D::NFN;
+      for (int i = lane; i < 4 * D::NFN; i += 32) {
+        const int c = i / D::NFN, n = i - c * D::NFN;
+        cp_async(dst + i, q2 + c * D::NP_TET + __ldg(fn + n));
+      }
+    } else if (t2 == HW_HEX) {
+      const R* q2 = (const R*)Q.p[HW_HEX] + (size_t)k2 * 4 * D::NP_HEX;
+      const int* tab = M.t[HW_HEX].iop[0] + 3 * f2 * D::NFQ;
+      if (sem) {
+        for (int i = lane; i < 4 * D::NFQ; i += 32) {
+          const int c = i / D::NFQ, p = i - c * D::NFQ;
+          const int base = __ldg(tab + 3 * p), stride = __ldg(tab + 3 * p + 1),
+                    end = __ldg(tab + 3 * p + 2);
+          cp_async(dst + i, q2 + c * D::NP_HEX + base + (end ? N : 0) * stride);
+        }
+      } else {
+        for (int i = lane; i < 4 * D::NFQ * D::N1; i += 32) {
+          const int l = i % D::N1, cpi = i / D::N1;
+          const int c = cpi / D::NFQ, p = cpi - c * D::NFQ;
+          const int base = __ldg(tab + 3 * p), stride = __ldg(tab + 3 * p + 1);
+          cp_async(dst + i, q2 + c * D::NP_HEX + base + l * stride);
+        }
+      }
+    } else {
+      const int np = (t2 == HW_WEDGE) ? D::NP_WEDGE : D::NP_PYR;
+      const R* q2 = (const R*)Q.p[t2] + (size_t)k2 * 4 * np;
+      for (int i = lane; i < 4 * np; i += 32) cp_async(dst + i, q2 + i);
+    }
+  }
+}
+
+// neighbour trace at my face point jj from the staged data (or the direct
+// global path when the neighbour was not staged)
+template <int N, int T, typename R>
+__device__ __forceinline__ void staged_trace(const hw_mesh_t& M, const hw_fields_t& Q,
+                                             int code, int k2, int f, int jj, const R* st_e,
+                                             bool sem, R tr[4]) {
+  using X = TT<N, T>;
+  using D = Dims<N>;
+  const int t2 = HW_NBR_TYPE(code), f2 = HW_NBR_FACE(code), pc = HW_NBR_PERM(code);
+  if (stage_count<N>(t2, sem) > X::stage(f)) {
+    neighbour_trace<N, R>(M, Q, code, k2, jj, X::tri(f), tr);
+    return;
+  }
+  const int p = X::tri(f) ? __ldg(M.perm_tri + pc * D::NFN + jj)
+                          : __ldg(M.perm_quad + pc * D::NFQ + jj);
+  const R* s = st_e + stage_off<N, T>(f);
+  if (t2 == HW_TET) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) tr[c] = s[c * D::NFN + p];
+  } else if (t2 == HW_HEX) {
+    if (sem) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tr[c] = s[c * D::NFQ + p];
+    } else {
+      const R* ve = (const R*)M.t[HW_HEX].op[1] + (f2 & 1) * D::N1;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        R a = R(0);
+#pragma unroll
+        for (int l = 0; l < D::N1; ++l) a += ldg(ve + l) * s[(c * D::NFQ + p) * D::N1 + l];
+        tr[c] = a;
+      }
+    }
+  } else {
+    const int np = (t2 == HW_WEDGE) ? D::NP_WEDGE : D::NP_PYR;
+    const int nfp = (t2 == HW_WEDGE) ? D::NFP_WEDGE : D::NFP_PYR;
+    const R* ET = (const R*)M.t[t2].op[5] + face_offset<N>(t2, f2) + p;
+    R a0 = R(0), a1 = R(0), a2 = R(0), a3 = R(0);
+#pragma unroll 4
+    for (int m = 0; m < np; ++m) {
+      const R e = ldg(ET + (size_t)m * nfp);
+      a0 += e * s[m];
+      a1 += e * s[np + m];
+      a2 += e * s[2 * np + m];
+      a3 += e * s[3 * np + m];
+    }
+    tr[0] = a0; tr[1] = a1; tr[2] = a2; tr[3] = a3;
+    if (t2 == HW_WEDGE) {
+      const R sc = ldg((const R*)M.t[HW_WEDGE].geo + (size_t)k2 * GEO_WEDGE + 9);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tr[c] *= sc;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ smem layout
+
+template <int N, int T, typename R>
+struct Smem {
+  using X = TT<N, T>;
+  static constexpr int NP = X::NP, NF = X::NF, NFP = X::NFP;
+  static constexpr int EPB = (NT / NP) > 0 ? (NT / NP) : 1;
+  static constexpr int S = (EPB * NP + NT - 1) / NT;
+  static constexpr int FLUXW = (T == HW_HEX) ? 4 : 2;       // flux words per face point
+  static constexpr int STG = stage_off<N, T>(NF);           // staged values per element
+  static constexpr int SQ = 0;
+  static constexpr int SRES = SQ + EPB * 4 * NP;
+  static constexpr int SV = SRES + EPB * 4 * NP;
+  static constexpr int SF = SV + ((T == HW_HEX) ? 0 : EPB * 3 * NP);
+  static constexpr int SG = SF + EPB * NFP * FLUXW;
+  static constexpr int SMAT = SG + EPB * X::GEO;
+  static constexpr int SZ = SMAT + EPB * 4;                 // neighbour impedance per face
+  static constexpr int SST = SZ + EPB * NF;
+  static constexpr int SOPS = SST + EPB * STG;              // hex: D1, nodes, w, Vend
+  static constexpr int TOTAL = SOPS + ((T == HW_HEX) ? (N + 1) * (N + 1) + 4 * (N + 1) : 0);
+  static constexpr size_t BYTES = sizeof(R) * TOTAL + sizeof(int) * (2 * EPB * NF + EPB);
+};
+
+template <int N, int T, typename R>
+__device__ __forceinline__ void prologue(const hw_mesh_t& M, const hw_fields_t& Q, const Epi& E,
+                                         const int32_t* list, int64_t w0, int ne, R* sm, int* sk,
+                                         int* snc, int* sne) {
+  using L = Smem<N, T, R>;
+  using X = TT<N, T>;
+  const hw_type_t& TY = M.t[T];
+  const int tid = threadIdx.x;
+  if (tid < ne) sk[tid] = list ? list[w0 + tid] : (int)(w0 + tid);
+  __syncthreads();
+  const R* q = (const R*)Q.p[T];
+  for (int i = tid; i < ne * 4 * L::NP; i += NT) {
+    const int e = i / (4 * L::NP), r = i - e * 4 * L::NP;
+    sm[L::SQ + i] = ldg(q + (size_t)sk[e] * 4 * L::NP + r);
+  }
+  for (int i = tid; i < ne * X::GEO; i += NT) {
+    const int e = i / X::GEO, r = i - e * X::GEO;
+    sm[L::SG + i] = ldg((const R*)TY.geo + (size_t)sk[e] * X::GEO + r);
+  }
+  for (int i = tid; i < ne * 4; i += NT)
+    sm[L::SMAT + i] = ldg((const R*)TY.mat + (size_t)sk[i >> 2] * 4 + (i & 3));
+  for (int i = tid; i < ne * X::NF; i += NT) {
+    const int e = i / X::NF, f = i - e * X::NF;
+    const int code = __ldg(TY.nbr_code + (size_t)sk[e] * X::NF + f);
+    const int k2 = __ldg(TY.nbr_elem + (size_t)sk[e] * X::NF + f);
+    snc[i] = code;
+    sne[i] = k2;
+    sm[L::SZ + i] = (code & HW_NBR_BOUNDARY) ? R(-1) : neighbour_z<R>(M, code, k2);
+  }
+  __syncthreads();
+  // P1: asynchronous staging (neighbour data, LSRK residual)
+  stage_neighbours<N, T, R>(M, Q, snc, sne, ne, sm + L::SST, M.formulation == HW_SEM);
+  if (E.mode == MODE_LSRK) {
+    const R* res = (const R*)E.res[T];
+    for (int i = tid; i < ne * 4 * L::NP; i += NT) {
+      const int e = i / (4 * L::NP), r = i - e * 4 * L::NP;
+      cp_async(sm + L::SRES + i, res + (size_t)sk[e] * 4 * L::NP + r);
+    }
+  }
+  cp_async_commit();
+}
+
+// epilogue for one value with the LSRK residual prefetched in smem
+template <typename R>
+__device__ __forceinline__ void epilogue_s(const Epi& E, int t, size_t idx, R v, R qv, R resv) {
+  if (E.mode == MODE_LSRK) {
+    const R r = R(E.a) * resv + R(E.dt) * v;
+    ((R*)E.res[t])[idx] = r;
+    ((R*)E.qout[t])[idx] = qv + R(E.b) * r;
+  } else {
+    epilogue<R>(E, t, idx, v, qv);
+  }
+}
+
+// ------------------------------------------------------------------ dense types
+// tet (nodal, strong), pyramid (semi-nodal quadrature-free, strong GL / skew
+// SEM) and affine wedge (LSC-DG, skew).  With constant geometric factors
+//   rhs_u_x = -sum_c G[c][x] (A_c p),
+//   rhs_p   = -sum_c A_c v_c (strong)  or  +sum_c A_c^T v_c (skew),
+//   v_c = sum_x G[c][x] u_x,
+// with A_c = D_c (tet, pyramid; hybridwave/dg.py:401-421, 446-463) or
+// S_c = V^T W D3_c (wedge: the reference's two cubature passes,
+// hybridwave/dg.py:423-444, collapse to it when G and J are constant).
+// op[0][c][m][n] = A_c[n][m], op[1][c][m][n] = A_c[m][n].
+
+template <int N, int T, typename R>
+__global__ void __launch_bounds__(NT) dense_kernel(hw_mesh_t M, hw_fields_t Q, Epi E,
+                                                   const int32_t* __restrict__ list,
+                                                   int64_t nwork) {
+  using L = Smem<N, T, R>;
+  using X = TT<N, T>;
+  constexpr int NP = L::NP, NF = L::NF, NFP = L::NFP, EPB = L::EPB, S = L::S;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   R* sm = reinterpret_cast<R*>(smem_raw);
-  R* sq = sm + K_::SQ;
-  R* sv = sm + K_::SV;
-  R* sf = sm + K_::SF;
-  R* sg = sm + K_::SG;
-  R* smat = sm + K_::SM;
-  __shared__ int sk[EPB];
+  int* sk = reinterpret_cast<int*>(sm + L::TOTAL);
+  int* snc = sk + EPB;
+  int* sne = snc + EPB * NF;
+  R* sq = sm + L::SQ;
+  R* sv = sm + L::SV;
+  R* sf = sm + L::SF;
+  R* sg = sm + L::SG;
+  R* smat = sm + L::SMAT;
 
-  const hw_type_t& T = M.t[HW_TET];
+  const hw_type_t& TY = M.t[T];
   const int tid = threadIdx.x;
   const int64_t w0 = (int64_t)blockIdx.x * EPB;
   const int ne = (int)((nwork - w0) < EPB ? (nwork - w0) : EPB);
-  if (tid < ne) sk[tid] = list ? list[w0 + tid] : (int)(w0 + tid);
-  __syncthreads();
-
-  const R* q = (const R*)Q.p[HW_TET];
-  for (int i = tid; i < ne * 4 * NP; i += NT) {
-    const int e = i / (4 * NP), r = i - e * 4 * NP;
-    sq[i] = ldg(q + (size_t)sk[e] * 4 * NP + r);
-  }
-  for (int i = tid; i < ne * GEO_TET; i += NT) {
-    const int e = i / GEO_TET, r = i - e * GEO_TET;
-    sg[i] = ldg((const R*)T.geo + (size_t)sk[e] * GEO_TET + r);
-  }
-  for (int i = tid; i < ne * 4; i += NT) {
-    sm[K_::SM + i] = ldg((const R*)T.mat + (size_t)sk[i / 4] * 4 + (i & 3));
-  }
-  __syncthreads();
+  prologue<N, T, R>(M, Q, E, list, w0, ne, sm, sk, snc, sne);
 
   // contravariant velocity components v_c = sum_x G[c][x] u_x
   for (int i = tid; i < ne * NP; i += NT) {
     const int e = i / NP, n = i - e * NP;
-    const R* G = sg + e * GEO_TET;
+    const R* G = sg + e * X::GEO;
     const R* u = sq + e * 4 * NP + NP + n;
 #pragma unroll
     for (int c = 0; c < 3; ++c)
-      sv[(e * 3 + c) * NP + n] = G[c * 3 + 0] * u[0] + G[c * 3 + 1] * u[NP] + G[c * 3 + 2] * u[2 * NP];
+      sv[(e * 3 + c) * NP + n] = G[c * 3] * u[0] + G[c * 3 + 1] * u[NP] + G[c * 3 + 2] * u[2 * NP];
   }
   __syncthreads();
 
+  const bool skew = TY.form == HW_FORM_SKEW;
+  const R* AT = (const R*)TY.op[0];
+  const R* AR = (const R*)TY.op[1];
   R acc[S][4];
-  const R* DT = (const R*)T.op[0];
 #pragma unroll
   for (int s = 0; s < S; ++s) {
     const int i = tid + s * NT;
@@ -86,216 +361,87 @@ __global__ void __launch_bounds__(NT) tet_kernel(hw_mesh_t M, hw_fields_t Q, Epi
 #pragma unroll
     for (int c = 0; c < 4; ++c) acc[s][c] = R(0);
     if (e < ne) {
-      R div = R(0), dp[3] = {R(0), R(0), R(0)};
+      R div = R(0), dp0 = R(0), dp1 = R(0), dp2 = R(0);
       const R* p = sq + e * 4 * NP;
       const R* v = sv + e * 3 * NP;
+      if (skew) {
 #pragma unroll 4
-      for (int m = 0; m < NP; ++m) {
-        const R pm = p[m];
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          const R d = ldg(DT + (c * NP + m) * NP + n);
-          div += d * v[c * NP + m];
-          dp[c] += d * pm;
+        for (int m = 0; m < NP; ++m) {
+          const R pm = p[m];
+          dp0 += ldg(AT + (0 * NP + m) * NP + n) * pm;
+          dp1 += ldg(AT + (1 * NP + m) * NP + n) * pm;
+          dp2 += ldg(AT + (2 * NP + m) * NP + n) * pm;
+          div += ldg(AR + (0 * NP + m) * NP + n) * v[m] + ldg(AR + (1 * NP + m) * NP + n) * v[NP + m] +
+                 ldg(AR + (2 * NP + m) * NP + n) * v[2 * NP + m];
+        }
+      } else {
+#pragma unroll 4
+        for (int m = 0; m < NP; ++m) {
+          const R pm = p[m];
+          const R a0 = ldg(AT + (0 * NP + m) * NP + n);
+          const R a1 = ldg(AT + (1 * NP + m) * NP + n);
+          const R a2 = ldg(AT + (2 * NP + m) * NP + n);
+          dp0 += a0 * pm;
+          dp1 += a1 * pm;
+          dp2 += a2 * pm;
+          div += a0 * v[m] + a1 * v[NP + m] + a2 * v[2 * NP + m];
         }
       }
-      const R* G = sg + e * GEO_TET;
-      acc[s][0] = -div;
-#pragma unroll
-      for (int x = 0; x < 3; ++x)
-        acc[s][1 + x] = -(G[x] * dp[0] + G[3 + x] * dp[1] + G[6 + x] * dp[2]);
-    }
-  }
-
-  // face flux at the tet face nodes
-  const R pen = R(M.penalty_scale);
-  for (int i = tid; i < ne * NFP; i += NT) {
-    const int e = i / NFP, j = i - e * NFP;
-    const int f = j / NFN, jj = j - f * NFN;
-    const int k = sk[e];
-    const int node = __ldg(T.iop[0] + j);
-    const R* qe = sq + e * 4 * NP;
-    const R pm = qe[node];
-    const R um[3] = {qe[NP + node], qe[2 * NP + node], qe[3 * NP + node]};
-    const R* g = sg + e * GEO_TET + 9 + 4 * f;
-    const R nrm[3] = {g[0], g[1], g[2]};
-    const int code = __ldg(T.nbr_code + (size_t)k * NF_TET + f);
-    const R zm = smat[e * 4 + 2];
-    R pp, up[3], zp;
-    if (code & HW_NBR_BOUNDARY) {
-      pp = -pm; up[0] = um[0]; up[1] = um[1]; up[2] = um[2]; zp = zm;
-    } else {
-      const int k2 = __ldg(T.nbr_elem + (size_t)k * NF_TET + f);
-      R tr[4];
-      neighbour_trace<N, R>(M, Q, code, k2, jj, true, tr);
-      pp = tr[0]; up[0] = tr[1]; up[1] = tr[2]; up[2] = tr[3];
-      zp = neighbour_z<R>(M, code, k2);
-    }
-    R tp, tu, fp, fu;
-    penalties(zm, zp, pen, tp, tu);
-    upwind_flux(pm, um, pp, up, nrm, tp, tu, T.form == HW_FORM_SKEW, fp, fu);
-    sf[(e * NFP + j) * 2 + 0] = fp * g[3];
-    sf[(e * NFP + j) * 2 + 1] = fu * g[3];
-  }
-  __syncthreads();
-
-  const R* LT = (const R*)T.op[1];
-#pragma unroll
-  for (int s = 0; s < S; ++s) {
-    const int i = tid + s * NT;
-    const int e = i / NP, n = i - e * NP;
-    if (e >= ne) continue;
-    const R* fl = sf + e * NFP * 2;
-    const R* g = sg + e * GEO_TET + 9;
-#pragma unroll
-    for (int f = 0; f < 4; ++f) {
-      R tp = R(0), tu = R(0);
-#pragma unroll 4
-      for (int jj = 0; jj < NFN; ++jj) {
-        const int j = f * NFN + jj;
-        const R l = ldg(LT + j * NP + n);
-        tp += l * fl[2 * j];
-        tu += l * fl[2 * j + 1];
-      }
-      acc[s][0] += tp;
-      acc[s][1] += g[4 * f + 0] * tu;
-      acc[s][2] += g[4 * f + 1] * tu;
-      acc[s][3] += g[4 * f + 2] * tu;
-    }
-    const R kap = smat[e * 4 + 0], irho = smat[e * 4 + 1];
-    const size_t base = (size_t)sk[e] * 4 * NP + n;
-    const R* qe = sq + e * 4 * NP + n;
-    epilogue<R>(E, HW_TET, base, acc[s][0] * kap, qe[0]);
-#pragma unroll
-    for (int c = 1; c < 4; ++c) epilogue<R>(E, HW_TET, base + c * NP, acc[s][c] * irho, qe[c * NP]);
-  }
-}
-
-// ------------------------------------------------------------------ pyramid
-// Quadrature-free semi-nodal pyramid (hybridwave/dg.py:446-463), affine:
-//   strong (GL):  rhs_p = -sum_c D_c v_c
-//   skew (SEM):   rhs_p = +sum_c D_c^T v_c        (v_c = sum_x G[c][x] u_x)
-//   rhs_u_x = -sum_c G[c][x] D_c p
-// surface: (Js/J) LIFT flux with LIFT = Vf^T W L.
-template <int N, typename R>
-struct PyrK {
-  using D = Dims<N>;
-  static constexpr int NP = D::NP_PYR, NFN = D::NFN, NFQ = D::NFQ, NFP = D::NFP_PYR;
-  static constexpr int EPB = (NT / NP) > 0 ? (NT / NP) : 1;
-  static constexpr int S = (EPB * NP + NT - 1) / NT;
-  static constexpr int SQ = 0, SV = SQ + EPB * 4 * NP, SF = SV + EPB * 3 * NP,
-                       SG = SF + EPB * NFP * 2, SM = SG + EPB * GEO_PYR,
-                       SMEM = SM + EPB * 4;
-};
-
-template <int N, typename R>
-__global__ void __launch_bounds__(NT) pyr_kernel(hw_mesh_t M, hw_fields_t Q, Epi E,
-                                                 const int32_t* __restrict__ list,
-                                                 int64_t nwork) {
-  using K_ = PyrK<N, R>;
-  constexpr int NP = K_::NP, NFN = K_::NFN, NFQ = K_::NFQ, NFP = K_::NFP, EPB = K_::EPB,
-                S = K_::S;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  R* sm = reinterpret_cast<R*>(smem_raw);
-  R* sq = sm + K_::SQ;
-  R* sv = sm + K_::SV;
-  R* sf = sm + K_::SF;
-  R* sg = sm + K_::SG;
-  R* smat = sm + K_::SM;
-  __shared__ int sk[EPB];
-
-  const hw_type_t& T = M.t[HW_PYRAMID];
-  const int tid = threadIdx.x;
-  const int64_t w0 = (int64_t)blockIdx.x * EPB;
-  const int ne = (int)((nwork - w0) < EPB ? (nwork - w0) : EPB);
-  if (tid < ne) sk[tid] = list ? list[w0 + tid] : (int)(w0 + tid);
-  __syncthreads();
-
-  const R* q = (const R*)Q.p[HW_PYRAMID];
-  for (int i = tid; i < ne * 4 * NP; i += NT) {
-    const int e = i / (4 * NP), r = i - e * 4 * NP;
-    sq[i] = ldg(q + (size_t)sk[e] * 4 * NP + r);
-  }
-  for (int i = tid; i < ne * GEO_PYR; i += NT) {
-    const int e = i / GEO_PYR, r = i - e * GEO_PYR;
-    sg[i] = ldg((const R*)T.geo + (size_t)sk[e] * GEO_PYR + r);
-  }
-  for (int i = tid; i < ne * 4; i += NT)
-    smat[i] = ldg((const R*)T.mat + (size_t)sk[i / 4] * 4 + (i & 3));
-  __syncthreads();
-
-  for (int i = tid; i < ne * NP; i += NT) {
-    const int e = i / NP, n = i - e * NP;
-    const R* G = sg + e * GEO_PYR;
-    const R* u = sq + e * 4 * NP + NP + n;
-#pragma unroll
-    for (int c = 0; c < 3; ++c)
-      sv[(e * 3 + c) * NP + n] = G[c * 3 + 0] * u[0] + G[c * 3 + 1] * u[NP] + G[c * 3 + 2] * u[2 * NP];
-  }
-  __syncthreads();
-
-  const bool skew = T.form == HW_FORM_SKEW;
-  R acc[S][4];
-  const R* DT = (const R*)T.op[0];   // DT[c][m][n] = D_c[n][m]
-  const R* DR = (const R*)T.op[1];   // DR[c][m][n] = D_c[m][n]
-#pragma unroll
-  for (int s = 0; s < S; ++s) {
-    const int i = tid + s * NT;
-    const int e = i / NP, n = i - e * NP;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) acc[s][c] = R(0);
-    if (e < ne) {
-      R div = R(0), dp[3] = {R(0), R(0), R(0)};
-      const R* p = sq + e * 4 * NP;
-      const R* v = sv + e * 3 * NP;
-      const R* DV = skew ? DR : DT;
-#pragma unroll 2
-      for (int m = 0; m < NP; ++m) {
-        const R pm = p[m];
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          const R d = ldg(DT + (c * NP + m) * NP + n);
-          dp[c] += d * pm;
-          div += ldg(DV + (c * NP + m) * NP + n) * v[c * NP + m];
-        }
-      }
-      const R* G = sg + e * GEO_PYR;
+      const R* G = sg + e * X::GEO;
       acc[s][0] = skew ? div : -div;
 #pragma unroll
-      for (int x = 0; x < 3; ++x)
-        acc[s][1 + x] = -(G[x] * dp[0] + G[3 + x] * dp[1] + G[6 + x] * dp[2]);
+      for (int x = 0; x < 3; ++x) acc[s][1 + x] = -(G[x] * dp0 + G[3 + x] * dp1 + G[6 + x] * dp2);
     }
   }
 
+  cp_async_wait_all();
+  __syncthreads();
+
+  // flux at the face points
   const R pen = R(M.penalty_scale);
-  const R* ET = (const R*)T.op[5];
+  const bool sem = M.formulation == HW_SEM;
+  const R* ET = (const R*)TY.op[5];
   for (int i = tid; i < ne * NFP; i += NT) {
     const int e = i / NFP, j = i - e * NFP;
-    int f, jj;
-    if (j < NFQ) { f = 0; jj = j; }
-    else { f = 1 + (j - NFQ) / NFN; jj = (j - NFQ) - (f - 1) * NFN; }
-    const int k = sk[e];
+    int jj;
+    const int f = face_of_point<N, T>(j, jj);
     const R* qe = sq + e * 4 * NP;
-    R own[4] = {R(0), R(0), R(0), R(0)};
-    for (int m = 0; m < NP; ++m) {
-      const R ev = ldg(ET + m * NFP + j);
+    R own[4];
+    if (T == HW_TET) {
+      const int node = __ldg(TY.iop[0] + j);
 #pragma unroll
-      for (int c = 0; c < 4; ++c) own[c] += ev * qe[c * NP + m];
+      for (int c = 0; c < 4; ++c) own[c] = qe[c * NP + node];
+    } else {
+      R a0 = R(0), a1 = R(0), a2 = R(0), a3 = R(0);
+#pragma unroll 4
+      for (int m = 0; m < NP; ++m) {
+        const R ev = ldg(ET + m * NFP + j);
+        a0 += ev * qe[m];
+        a1 += ev * qe[NP + m];
+        a2 += ev * qe[2 * NP + m];
+        a3 += ev * qe[3 * NP + m];
+      }
+      own[0] = a0; own[1] = a1; own[2] = a2; own[3] = a3;
+      if (T == HW_WEDGE) {
+        const R isj = sg[e * X::GEO + 9];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) own[c] *= isj;
+      }
     }
     const R um[3] = {own[1], own[2], own[3]};
-    const R* g = sg + e * GEO_PYR + 9 + 4 * f;
+    const R* g = sg + e * X::GEO + X::GF + 4 * f;
     const R nrm[3] = {g[0], g[1], g[2]};
-    const int code = __ldg(T.nbr_code + (size_t)k * NF_PYR + f);
+    const int code = snc[e * NF + f];
     const R zm = smat[e * 4 + 2];
     R pp, up[3], zp;
     if (code & HW_NBR_BOUNDARY) {
       pp = -own[0]; up[0] = um[0]; up[1] = um[1]; up[2] = um[2]; zp = zm;
     } else {
-      const int k2 = __ldg(T.nbr_elem + (size_t)k * NF_PYR + f);
       R tr[4];
-      neighbour_trace<N, R>(M, Q, code, k2, jj, f != 0, tr);
+      staged_trace<N, T, R>(M, Q, code, sne[e * NF + f], f, jj, sm + L::SST + e * L::STG, sem,
+                            tr);
       pp = tr[0]; up[0] = tr[1]; up[1] = tr[2]; up[2] = tr[3];
-      zp = neighbour_z<R>(M, code, k2);
+      zp = sm[L::SZ + e * NF + f];
     }
     R tp, tu, fp, fu;
     penalties(zm, zp, pen, tp, tu);
@@ -305,19 +451,20 @@ __global__ void __launch_bounds__(NT) pyr_kernel(hw_mesh_t M, hw_fields_t Q, Epi
   }
   __syncthreads();
 
-  const R* LT = (const R*)T.op[6];
+  const R* LT = (const R*)TY.op[T == HW_TET ? 1 : 6];
 #pragma unroll
   for (int s = 0; s < S; ++s) {
     const int i = tid + s * NT;
     const int e = i / NP, n = i - e * NP;
     if (e >= ne) continue;
     const R* fl = sf + e * NFP * 2;
-    const R* g = sg + e * GEO_PYR + 9;
-    for (int f = 0; f < 5; ++f) {
-      const int j0 = f == 0 ? 0 : NFQ + (f - 1) * NFN;
-      const int cnt = f == 0 ? NFQ : NFN;
+    const R* g = sg + e * X::GEO + X::GF;
+#pragma unroll
+    for (int f = 0; f < NF; ++f) {
       R tp = R(0), tu = R(0);
-      for (int jj = 0; jj < cnt; ++jj) {
+      const int j0 = X::off(f);
+#pragma unroll 4
+      for (int jj = 0; jj < X::cnt(f); ++jj) {
         const int j = j0 + jj;
         const R l = ldg(LT + j * NP + n);
         tp += l * fl[2 * j];
@@ -331,194 +478,11 @@ __global__ void __launch_bounds__(NT) pyr_kernel(hw_mesh_t M, hw_fields_t Q, Epi
     const R kap = smat[e * 4 + 0], irho = smat[e * 4 + 1];
     const size_t base = (size_t)sk[e] * 4 * NP + n;
     const R* qe = sq + e * 4 * NP + n;
-    epilogue<R>(E, HW_PYRAMID, base, acc[s][0] * kap, qe[0]);
+    const R* re = sm + L::SRES + e * 4 * NP + n;
+    epilogue_s<R>(E, T, base, acc[s][0] * kap, qe[0], re[0]);
 #pragma unroll
     for (int c = 1; c < 4; ++c)
-      epilogue<R>(E, HW_PYRAMID, base + c * NP, acc[s][c] * irho, qe[c * NP]);
-  }
-}
-
-// ------------------------------------------------------------------ wedge
-// LSC-DG wedge, skew form, affine (hybridwave/dg.py:423-444): two passes
-// through the (N+1)^3 cubature points; identity mass; traces carry 1/sqrt(J).
-template <int N, typename R>
-struct WedgeK {
-  using D = Dims<N>;
-  static constexpr int NP = D::NP_WEDGE, NQ = D::NQ_WEDGE, NFN = D::NFN, NFQ = D::NFQ,
-                       NFP = D::NFP_WEDGE;
-  static constexpr int EPB = (NT / NQ) > 0 ? (NT / NQ) : 1;
-  static constexpr int S = (EPB * NP + NT - 1) / NT;
-  static constexpr int SQ = 0, SW = SQ + EPB * 4 * NP, SF = SW + EPB * 6 * NQ,
-                       SG = SF + EPB * NFP * 2, SM = SG + EPB * GEO_WEDGE,
-                       SMEM = SM + EPB * 4;
-};
-
-template <int N, typename R>
-__global__ void __launch_bounds__(NT) wedge_kernel(hw_mesh_t M, hw_fields_t Q, Epi E,
-                                                   const int32_t* __restrict__ list,
-                                                   int64_t nwork) {
-  using K_ = WedgeK<N, R>;
-  constexpr int NP = K_::NP, NQ = K_::NQ, NFN = K_::NFN, NFQ = K_::NFQ, NFP = K_::NFP,
-                EPB = K_::EPB, S = K_::S;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  R* sm = reinterpret_cast<R*>(smem_raw);
-  R* sq = sm + K_::SQ;
-  R* sw = sm + K_::SW;
-  R* sf = sm + K_::SF;
-  R* sg = sm + K_::SG;
-  R* smat = sm + K_::SM;
-  __shared__ int sk[EPB];
-
-  const hw_type_t& T = M.t[HW_WEDGE];
-  const int tid = threadIdx.x;
-  const int64_t w0 = (int64_t)blockIdx.x * EPB;
-  const int ne = (int)((nwork - w0) < EPB ? (nwork - w0) : EPB);
-  if (tid < ne) sk[tid] = list ? list[w0 + tid] : (int)(w0 + tid);
-  __syncthreads();
-
-  const R* q = (const R*)Q.p[HW_WEDGE];
-  for (int i = tid; i < ne * 4 * NP; i += NT) {
-    const int e = i / (4 * NP), r = i - e * 4 * NP;
-    sq[i] = ldg(q + (size_t)sk[e] * 4 * NP + r);
-  }
-  for (int i = tid; i < ne * GEO_WEDGE; i += NT) {
-    const int e = i / GEO_WEDGE, r = i - e * GEO_WEDGE;
-    sg[i] = ldg((const R*)T.geo + (size_t)sk[e] * GEO_WEDGE + r);
-  }
-  for (int i = tid; i < ne * 4; i += NT)
-    smat[i] = ldg((const R*)T.mat + (size_t)sk[i / 4] * 4 + (i & 3));
-  __syncthreads();
-
-  // trial pass at cubature points
-  const R* VT = (const R*)T.op[0];    // (NP, NQ)
-  const R* D3T = (const R*)T.op[1];   // (3, NP, NQ)
-  const R* wq = (const R*)T.op[4];
-  for (int i = tid; i < ne * NQ; i += NT) {
-    const int e = i / NQ, qi = i - e * NQ;
-    const R* qe = sq + e * 4 * NP;
-    R U[3] = {R(0), R(0), R(0)}, dp[3] = {R(0), R(0), R(0)};
-#pragma unroll 2
-    for (int m = 0; m < NP; ++m) {
-      const R v = ldg(VT + m * NQ + qi);
-      const R pm = qe[m];
-      U[0] += v * qe[NP + m];
-      U[1] += v * qe[2 * NP + m];
-      U[2] += v * qe[3 * NP + m];
-#pragma unroll
-      for (int c = 0; c < 3; ++c) dp[c] += ldg(D3T + (c * NP + m) * NQ + qi) * pm;
-    }
-    const R* G = sg + e * GEO_WEDGE;
-    const R w = ldg(wq + qi);
-    R* o = sw + e * 6 * NQ + qi;
-#pragma unroll
-    for (int x = 0; x < 3; ++x) o[x * NQ] = w * (G[x] * dp[0] + G[3 + x] * dp[1] + G[6 + x] * dp[2]);
-#pragma unroll
-    for (int c = 0; c < 3; ++c)
-      o[(3 + c) * NQ] = w * (G[c * 3] * U[0] + G[c * 3 + 1] * U[1] + G[c * 3 + 2] * U[2]);
-  }
-  __syncthreads();
-
-  // test pass
-  const R* V = (const R*)T.op[2];     // (NQ, NP)
-  const R* D3 = (const R*)T.op[3];    // (3, NQ, NP)
-  R acc[S][4];
-#pragma unroll
-  for (int s = 0; s < S; ++s) {
-    const int i = tid + s * NT;
-    const int e = i / NP, n = i - e * NP;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) acc[s][c] = R(0);
-    if (e < ne) {
-      const R* o = sw + e * 6 * NQ;
-      R rp = R(0), ru[3] = {R(0), R(0), R(0)};
-#pragma unroll 2
-      for (int qi = 0; qi < NQ; ++qi) {
-        const R v = ldg(V + qi * NP + n);
-        ru[0] += v * o[qi];
-        ru[1] += v * o[NQ + qi];
-        ru[2] += v * o[2 * NQ + qi];
-#pragma unroll
-        for (int c = 0; c < 3; ++c) rp += ldg(D3 + (c * NQ + qi) * NP + n) * o[(3 + c) * NQ + qi];
-      }
-      acc[s][0] = rp;
-      acc[s][1] = -ru[0];
-      acc[s][2] = -ru[1];
-      acc[s][3] = -ru[2];
-    }
-  }
-
-  const R pen = R(M.penalty_scale);
-  const R* ET = (const R*)T.op[5];
-  for (int i = tid; i < ne * NFP; i += NT) {
-    const int e = i / NFP, j = i - e * NFP;
-    int f, jj;
-    bool tri;
-    if (j < 2 * NFN) { f = j / NFN; jj = j - f * NFN; tri = true; }
-    else { f = 2 + (j - 2 * NFN) / NFQ; jj = (j - 2 * NFN) - (f - 2) * NFQ; tri = false; }
-    const int k = sk[e];
-    const R* qe = sq + e * 4 * NP;
-    const R isj = sg[e * GEO_WEDGE + 9];
-    R own[4] = {R(0), R(0), R(0), R(0)};
-    for (int m = 0; m < NP; ++m) {
-      const R ev = ldg(ET + m * NFP + j);
-#pragma unroll
-      for (int c = 0; c < 4; ++c) own[c] += ev * qe[c * NP + m];
-    }
-#pragma unroll
-    for (int c = 0; c < 4; ++c) own[c] *= isj;
-    const R um[3] = {own[1], own[2], own[3]};
-    const R* g = sg + e * GEO_WEDGE + 10 + 4 * f;
-    const R nrm[3] = {g[0], g[1], g[2]};
-    const int code = __ldg(T.nbr_code + (size_t)k * NF_WEDGE + f);
-    const R zm = smat[e * 4 + 2];
-    R pp, up[3], zp;
-    if (code & HW_NBR_BOUNDARY) {
-      pp = -own[0]; up[0] = um[0]; up[1] = um[1]; up[2] = um[2]; zp = zm;
-    } else {
-      const int k2 = __ldg(T.nbr_elem + (size_t)k * NF_WEDGE + f);
-      R tr[4];
-      neighbour_trace<N, R>(M, Q, code, k2, jj, tri, tr);
-      pp = tr[0]; up[0] = tr[1]; up[1] = tr[2]; up[2] = tr[3];
-      zp = neighbour_z<R>(M, code, k2);
-    }
-    R tp, tu, fp, fu;
-    penalties(zm, zp, pen, tp, tu);
-    upwind_flux(own[0], um, pp, up, nrm, tp, tu, true, fp, fu);
-    sf[(e * NFP + j) * 2 + 0] = fp * g[3];
-    sf[(e * NFP + j) * 2 + 1] = fu * g[3];
-  }
-  __syncthreads();
-
-  const R* LT = (const R*)T.op[6];
-#pragma unroll
-  for (int s = 0; s < S; ++s) {
-    const int i = tid + s * NT;
-    const int e = i / NP, n = i - e * NP;
-    if (e >= ne) continue;
-    const R* fl = sf + e * NFP * 2;
-    const R* g = sg + e * GEO_WEDGE + 10;
-    for (int f = 0; f < 5; ++f) {
-      const int j0 = f < 2 ? f * NFN : 2 * NFN + (f - 2) * NFQ;
-      const int cnt = f < 2 ? NFN : NFQ;
-      R tp = R(0), tu = R(0);
-      for (int jj = 0; jj < cnt; ++jj) {
-        const int j = j0 + jj;
-        const R l = ldg(LT + j * NP + n);
-        tp += l * fl[2 * j];
-        tu += l * fl[2 * j + 1];
-      }
-      acc[s][0] += tp;
-      acc[s][1] += g[4 * f + 0] * tu;
-      acc[s][2] += g[4 * f + 1] * tu;
-      acc[s][3] += g[4 * f + 2] * tu;
-    }
-    const R kap = smat[e * 4 + 0], irho = smat[e * 4 + 1];
-    const size_t base = (size_t)sk[e] * 4 * NP + n;
-    const R* qe = sq + e * 4 * NP + n;
-    epilogue<R>(E, HW_WEDGE, base, acc[s][0] * kap, qe[0]);
-#pragma unroll
-    for (int c = 1; c < 4; ++c)
-      epilogue<R>(E, HW_WEDGE, base + c * NP, acc[s][c] * irho, qe[c * NP]);
+      epilogue_s<R>(E, T, base + c * NP, acc[s][c] * irho, qe[c * NP], re[c * NP]);
   }
 }
 
@@ -554,7 +518,6 @@ __device__ __forceinline__ R hex_metric(const R* X, R r, R s, R t, R G[9]) {
   const R J = F[0] * (F[4] * F[8] - F[5] * F[7]) - F[1] * (F[3] * F[8] - F[5] * F[6]) +
               F[2] * (F[3] * F[7] - F[4] * F[6]);
   const R iJ = R(1) / J;
-  // G = F^{-1}: G[c][x]
   G[0] = (F[4] * F[8] - F[5] * F[7]) * iJ;
   G[1] = (F[2] * F[7] - F[1] * F[8]) * iJ;
   G[2] = (F[1] * F[5] - F[2] * F[4]) * iJ;
@@ -568,61 +531,38 @@ __device__ __forceinline__ R hex_metric(const R* X, R r, R s, R t, R G[9]) {
 }
 
 template <int N, typename R>
-struct HexK {
-  using D = Dims<N>;
-  static constexpr int N1 = D::N1, NP = D::NP_HEX, NFQ = D::NFQ, NFP = D::NFP_HEX;
-  static constexpr int EPB = (NT / NP) > 0 ? (NT / NP) : 1;
-  static constexpr int S = (EPB * NP + NT - 1) / NT;
-  static constexpr int SQ = 0, SF = SQ + EPB * 4 * NP, SG = SF + EPB * NFP * 4,
-                       SM = SG + EPB * GEO_HEX, SD = SM + EPB * 4,
-                       SMEM = SD + N1 * N1 + 3 * N1 + 2 * N1;
-};
-
-template <int N, typename R>
 __global__ void __launch_bounds__(NT) hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi E,
                                                  const int32_t* __restrict__ list,
                                                  int64_t nwork) {
-  using K_ = HexK<N, R>;
-  constexpr int N1 = K_::N1, NP = K_::NP, NFQ = K_::NFQ, NFP = K_::NFP, EPB = K_::EPB,
-                S = K_::S;
+  using L = Smem<N, HW_HEX, R>;
+  using D = Dims<N>;
+  constexpr int N1 = D::N1, NP = L::NP, NFQ = D::NFQ, NFP = L::NFP, EPB = L::EPB, S = L::S;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   R* sm = reinterpret_cast<R*>(smem_raw);
-  R* sq = sm + K_::SQ;
-  R* sf = sm + K_::SF;
-  R* sg = sm + K_::SG;
-  R* smat = sm + K_::SM;
-  R* sD = sm + K_::SD;           // D1 (N1 x N1)
+  int* sk = reinterpret_cast<int*>(sm + L::TOTAL);
+  int* snc = sk + EPB;
+  int* sne = snc + EPB * 6;
+  R* sq = sm + L::SQ;
+  R* sf = sm + L::SF;
+  R* sg = sm + L::SG;
+  R* smat = sm + L::SMAT;
+  R* sD = sm + L::SOPS;          // D1 (N1 x N1)
   R* sx = sD + N1 * N1;          // 1-D nodes
   R* sw1 = sx + N1;              // 1-D weights
   R* sve = sw1 + N1;             // endpoint rows (2 x N1)
-  __shared__ int sk[EPB];
 
-  const hw_type_t& T = M.t[HW_HEX];
+  const hw_type_t& TY = M.t[HW_HEX];
   const bool sem = M.formulation == HW_SEM;
   const int tid = threadIdx.x;
   const int64_t w0 = (int64_t)blockIdx.x * EPB;
   const int ne = (int)((nwork - w0) < EPB ? (nwork - w0) : EPB);
-  if (tid < ne) sk[tid] = list ? list[w0 + tid] : (int)(w0 + tid);
-  if (tid < N1 * N1) sD[tid] = ldg((const R*)T.op[0] + tid);
-  if (tid < 2 * N1) sve[tid] = ldg((const R*)T.op[1] + tid);
+  if (tid < N1 * N1) sD[tid] = ldg((const R*)TY.op[0] + tid);
+  if (tid < 2 * N1) sve[tid] = ldg((const R*)TY.op[1] + tid);
   if (tid < N1) {
-    sw1[tid] = ldg((const R*)T.op[2] + tid);
-    sx[tid] = ldg((const R*)T.op[4] + tid);
+    sw1[tid] = ldg((const R*)TY.op[2] + tid);
+    sx[tid] = ldg((const R*)TY.op[4] + tid);
   }
-  __syncthreads();
-
-  const R* q = (const R*)Q.p[HW_HEX];
-  for (int i = tid; i < ne * 4 * NP; i += NT) {
-    const int e = i / (4 * NP), r = i - e * 4 * NP;
-    sq[i] = ldg(q + (size_t)sk[e] * 4 * NP + r);
-  }
-  for (int i = tid; i < ne * GEO_HEX; i += NT) {
-    const int e = i / GEO_HEX, r = i - e * GEO_HEX;
-    sg[i] = ldg((const R*)T.geo + (size_t)sk[e] * GEO_HEX + r);
-  }
-  for (int i = tid; i < ne * 4; i += NT)
-    smat[i] = ldg((const R*)T.mat + (size_t)sk[i / 4] * 4 + (i & 3));
-  __syncthreads();
+  prologue<N, HW_HEX, R>(M, Q, E, list, w0, ne, sm, sk, snc, sne);
 
   R acc[S][4], minv[S];
 #pragma unroll
@@ -660,12 +600,14 @@ __global__ void __launch_bounds__(NT) hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi
     }
   }
 
+  cp_async_wait_all();
+  __syncthreads();
+
   const R pen = R(M.penalty_scale);
   for (int i = tid; i < ne * NFP; i += NT) {
     const int e = i / NFP, j = i - e * NFP;
     const int f = j / NFQ, jj = j - f * NFQ;
-    const int k = sk[e];
-    const int* tab = T.iop[0] + 3 * j;
+    const int* tab = TY.iop[0] + 3 * j;
     const int base = __ldg(tab), stride = __ldg(tab + 1), end = __ldg(tab + 2);
     const R* qe = sq + e * 4 * NP;
     R own[4];
@@ -686,7 +628,7 @@ __global__ void __launch_bounds__(NT) hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi
     // face geometry at (xi, eta) = (x[a], x[b]) from the 4 face vertices
     const int a = jj / N1, b = jj - a * N1;
     const R xi = sx[a], eta = sx[b];
-    const R* X = sg + e * GEO_HEX;
+    const R* Xv = sg + e * GEO_HEX;
     R t1[3], t2[3];
     {
       const R g1[4] = {-(R(1) - eta), (R(1) - eta), (R(1) + eta), -(R(1) + eta)};
@@ -696,7 +638,7 @@ __global__ void __launch_bounds__(NT) hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi
         R s1 = R(0), s2 = R(0);
 #pragma unroll
         for (int v = 0; v < 4; ++v) {
-          const R xv = X[c_hex_face_verts[f][v] * 3 + x];
+          const R xv = Xv[c_hex_face_verts[f][v] * 3 + x];
           s1 += g1[v] * xv;
           s2 += g2[v] * xv;
         }
@@ -704,27 +646,27 @@ __global__ void __launch_bounds__(NT) hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi
         t2[x] = R(0.25) * s2;
       }
     }
-    R nv[3] = {t1[1] * t2[2] - t1[2] * t2[1], t1[2] * t2[0] - t1[0] * t2[2],
-               t1[0] * t2[1] - t1[1] * t2[0]};
+    const R nv[3] = {t1[1] * t2[2] - t1[2] * t2[1], t1[2] * t2[0] - t1[0] * t2[2],
+                     t1[0] * t2[1] - t1[1] * t2[0]};
     const R Js = sqrt(nv[0] * nv[0] + nv[1] * nv[1] + nv[2] * nv[2]);
     const R nrm[3] = {nv[0] / Js, nv[1] / Js, nv[2] / Js};
     const R wJs = sw1[a] * sw1[b] * Js;
     const R um[3] = {own[1], own[2], own[3]};
-    const int code = __ldg(T.nbr_code + (size_t)k * NF_HEX + f);
+    const int code = snc[e * 6 + f];
     const R zm = smat[e * 4 + 2];
     R pp, up[3], zp;
     if (code & HW_NBR_BOUNDARY) {
       pp = -own[0]; up[0] = um[0]; up[1] = um[1]; up[2] = um[2]; zp = zm;
     } else {
-      const int k2 = __ldg(T.nbr_elem + (size_t)k * NF_HEX + f);
       R tr[4];
-      neighbour_trace<N, R>(M, Q, code, k2, jj, false, tr);
+      staged_trace<N, HW_HEX, R>(M, Q, code, sne[e * 6 + f], f, jj, sm + L::SST + e * L::STG,
+                                 sem, tr);
       pp = tr[0]; up[0] = tr[1]; up[1] = tr[2]; up[2] = tr[3];
-      zp = neighbour_z<R>(M, code, k2);
+      zp = sm[L::SZ + e * 6 + f];
     }
     R tp, tu, fp, fu;
     penalties(zm, zp, pen, tp, tu);
-    upwind_flux(own[0], um, pp, up, nrm, tp, tu, T.form == HW_FORM_SKEW, fp, fu);
+    upwind_flux(own[0], um, pp, up, nrm, tp, tu, TY.form == HW_FORM_SKEW, fp, fu);
     R* o = sf + (e * NFP + j) * 4;
     o[0] = fp * wJs;
     o[1] = nrm[0] * fu * wJs;
@@ -752,7 +694,7 @@ __global__ void __launch_bounds__(NT) hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi
       } else {
         w = sve[end * N1 + l];
       }
-      const int pt = __ldg(T.iop[1] + f * NP + n);
+      const int pt = __ldg(TY.iop[1] + f * NP + n);
       const R* o = fl + (f * NFQ + pt) * 4;
 #pragma unroll
       for (int c = 0; c < 4; ++c) lift[c] += w * o[c];
@@ -764,10 +706,11 @@ __global__ void __launch_bounds__(NT) hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi
     const R kap = smat[e * 4 + 0], irho = smat[e * 4 + 1];
     const size_t base = (size_t)sk[e] * 4 * NP + n;
     const R* qe = sq + e * 4 * NP + n;
-    epilogue<R>(E, HW_HEX, base, acc[s][0] * kap, qe[0]);
+    const R* re = sm + L::SRES + e * 4 * NP + n;
+    epilogue_s<R>(E, HW_HEX, base, acc[s][0] * kap, qe[0], re[0]);
 #pragma unroll
     for (int c = 1; c < 4; ++c)
-      epilogue<R>(E, HW_HEX, base + c * NP, acc[s][c] * irho, qe[c * NP]);
+      epilogue_s<R>(E, HW_HEX, base + c * NP, acc[s][c] * irho, qe[c * NP], re[c * NP]);
   }
 }
 

@@ -134,9 +134,8 @@ def _pack_ops(t, d):
     if t == "tet":
         return {0: np.stack([d["Dr"].T, d["Ds"].T, d["Dt"].T]), 1: d["LIFT"].T}
     if t == "wedge":
-        return {0: d["V"].T, 1: np.stack([d["Dr3"].T, d["Ds3"].T, d["Dt3"].T]),
-                2: d["V"], 3: np.stack([d["Dr3"], d["Ds3"], d["Dt3"]]), 4: d["wq"],
-                5: d["E"].T, 6: d["LIFT"].T}
+        # op[0][c][m][n] = S_c[n][m], op[1][c][m][n] = S_c[m][n]
+        return {0: np.stack([S.T for S in d["S"]]), 1: d["S"], 5: d["E"].T, 6: d["LIFT"].T}
     if t == "pyramid":
         return {0: np.stack([d["Dr"].T, d["Ds"].T, d["Dt"].T]),
                 1: np.stack([d["Dr"], d["Ds"], d["Dt"]]), 5: d["E"].T, 6: d["LIFT"].T}

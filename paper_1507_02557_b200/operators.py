@@ -281,6 +281,10 @@ def device_operators(elem_type, N, formulation, ops=None):
     elif elem_type == "wedge":
         out["V"], out["Dr3"], out["Ds3"], out["Dt3"] = ops.V, ops.Dr3, ops.Ds3, ops.Dt3
         out["wq"] = ops.cub.weights
+        # affine LSC wedge: the two cubature passes collapse to
+        # S_c = V^T W D3_c (test mode x trial mode), hybridwave/dg.py:423-444
+        W = ops.cub.weights[:, None]
+        out["S"] = np.stack([ops.V.T @ (W * D) for D in (ops.Dr3, ops.Ds3, ops.Dt3)])
     elif elem_type == "pyramid":
         out["Dr"], out["Ds"], out["Dt"] = ops.Dr, ops.Ds, ops.Dt
     return out

@@ -93,14 +93,12 @@ def rhs(pack, disc, state):
                 acc[:, 0] = -np.einsum("cmn,kcm->kn", DT, v)
             acc[:, 1:] = -np.einsum("kcx,kcn->kxn", G, dp)
         elif t == "wedge":
+            # affine LSC wedge: S_c = V^T W D3_c, same data flow as the skew pyramid
             G = geo[:, :9].reshape(K, 3, 3)
-            VT, D3T, V, D3, wq = P["op"][0], P["op"][1], P["op"][2], P["op"][3], P["op"][4]
-            U = q[t][:, 1:] @ VT                                  # (K,3,NQ)
-            dp = np.einsum("cmq,km->kcq", D3T, q[t][:, 0])
-            gp = np.einsum("kcx,kcq->kxq", G, dp) * wq
-            up = np.einsum("kcx,kxq->kcq", G, U) * wq
-            acc[:, 1:] = -(gp @ V)
-            acc[:, 0] = np.einsum("cqn,kcq->kn", D3, up)
+            v = np.einsum("kcx,kxn->kcn", G, q[t][:, 1:])
+            dp = np.einsum("cmn,km->kcn", P["op"][0], q[t][:, 0])
+            acc[:, 0] = np.einsum("cmn,kcm->kn", P["op"][1], v)
+            acc[:, 1:] = -np.einsum("kcx,kcn->kxn", G, dp)
         else:  # hex
             n1 = d["N1"]
             X = geo.reshape(K, 8, 3)
