@@ -1,15 +1,19 @@
 // C ABI of the sm_100a DG acoustic hot path (see include/hybridwave_b200.h).
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
 #include <unordered_set>
 
 #include "hw_kernels.cuh"
+#include "hw_tet_mma.cuh"
 
 namespace hw {
 
 static thread_local std::string g_err;
+// HW_DISABLE_MMA=1 selects the scalar dense_kernel for tets (A/B checks)
+static const bool g_disable_mma = getenv("HW_DISABLE_MMA") != nullptr;
 
 static int fail(const char* msg) {
   g_err = msg;
@@ -89,7 +93,17 @@ static int launch_rhs_all(const hw_mesh_t& M, const hw_fields_t& Q, const Epi& E
       }
       case HW_WEDGE: rc = launch_dense<N, HW_WEDGE, R>(M, Q, E, list, n, st); break;
       case HW_PYRAMID: rc = launch_dense<N, HW_PYRAMID, R>(M, Q, E, list, n, st); break;
-      case HW_TET: rc = launch_dense<N, HW_TET, R>(M, Q, E, list, n, st); break;
+      case HW_TET:
+        if (sizeof(R) == 8 && !g_disable_mma) {
+          using L = TetMma<N>;
+          if ((rc = set_smem(tet_mma_kernel<N>, L::BYTES))) return rc;
+          tet_mma_kernel<N><<<(unsigned)((n + L::E - 1) / L::E), L::NTH, L::BYTES, st>>>(
+              M, Q, E, list, n);
+          rc = check_launch("tet_mma_kernel");
+        } else {
+          rc = launch_dense<N, HW_TET, R>(M, Q, E, list, n, st);
+        }
+        break;
     }
     if (rc) return rc;
   }

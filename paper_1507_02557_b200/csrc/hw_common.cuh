@@ -24,7 +24,10 @@ struct Dims {
   static constexpr int NFP_PYR = NFQ + 4 * NFN;
 };
 
-constexpr int GEO_HEX = 24, GEO_WEDGE = 30, GEO_PYR = 29, GEO_TET = 25;
+// geometry record words per element; per face FS words (n_x, n_y, n_z,
+// Jacobian scale, avg(rho c) of the two sides) after GF (dense types) or
+// avg(rho c) at 24 + f (hex, after the 8 vertices)
+constexpr int GEO_HEX = 30, GEO_WEDGE = 35, GEO_PYR = 34, GEO_TET = 29, FS = 5;
 constexpr int NF_HEX = 6, NF_WEDGE = 5, NF_PYR = 5, NF_TET = 4;
 
 // epilogue of the fused RHS kernels
@@ -84,10 +87,10 @@ __device__ __forceinline__ void upwind_flux(R pm, const R um[3], R pp, const R u
   flux_un = R(0.5) * (tau_u * dun - dp);
 }
 
-// penalties from the two impedances rho*c (hybridwave/dg.py:61-69)
+// penalties from avg(rho c) of the two sides (hybridwave/dg.py:61-69,
+// 341-342); avg is precomputed per face on the host
 template <typename R>
-__device__ __forceinline__ void penalties(R zm, R zp, R scale, R& tp, R& tu) {
-  R avg = R(0.5) * (zm + zp);
+__device__ __forceinline__ void penalties(R avg, R scale, R& tp, R& tu) {
   tp = scale / avg;
   tu = scale * avg;
 }
@@ -147,12 +150,6 @@ __device__ __forceinline__ void neighbour_trace(const hw_mesh_t& M, const hw_fie
       for (int c = 0; c < 4; ++c) tr[c] *= s;
     }
   }
-}
-
-// neighbour impedance
-template <typename R>
-__device__ __forceinline__ R neighbour_z(const hw_mesh_t& M, int code, int k2) {
-  return ldg((const R*)M.t[HW_NBR_TYPE(code)].mat + (size_t)k2 * 4 + 2);
 }
 
 // Epilogue: value v = dU/dtau at (type t, flat index idx) with q_in value qv.

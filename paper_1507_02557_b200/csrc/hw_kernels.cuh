@@ -243,8 +243,7 @@ struct Smem {
   static constexpr int SF = SV + ((T == HW_HEX) ? 0 : EPB * 3 * NP);
   static constexpr int SG = SF + EPB * NFP * FLUXW;
   static constexpr int SMAT = SG + EPB * X::GEO;
-  static constexpr int SZ = SMAT + EPB * 4;                 // neighbour impedance per face
-  static constexpr int SST = SZ + EPB * NF;
+  static constexpr int SST = SMAT + EPB * 4;
   static constexpr int SOPS = SST + EPB * STG;              // hex: D1, nodes, w, Vend
   static constexpr int TOTAL = SOPS + ((T == HW_HEX) ? (N + 1) * (N + 1) + 4 * (N + 1) : 0);
   static constexpr size_t BYTES = sizeof(R) * TOTAL + sizeof(int) * (2 * EPB * NF + EPB);
@@ -277,7 +276,6 @@ __device__ __forceinline__ void prologue(const hw_mesh_t& M, const hw_fields_t& 
     const int k2 = __ldg(TY.nbr_elem + (size_t)sk[e] * X::NF + f);
     snc[i] = code;
     sne[i] = k2;
-    sm[L::SZ + i] = (code & HW_NBR_BOUNDARY) ? R(-1) : neighbour_z<R>(M, code, k2);
   }
   __syncthreads();
   // P1: asynchronous staging (neighbour data, LSRK residual)
@@ -429,22 +427,20 @@ __global__ void __launch_bounds__(NT) dense_kernel(hw_mesh_t M, hw_fields_t Q, E
       }
     }
     const R um[3] = {own[1], own[2], own[3]};
-    const R* g = sg + e * X::GEO + X::GF + 4 * f;
+    const R* g = sg + e * X::GEO + X::GF + FS * f;
     const R nrm[3] = {g[0], g[1], g[2]};
     const int code = snc[e * NF + f];
-    const R zm = smat[e * 4 + 2];
-    R pp, up[3], zp;
+    R pp, up[3];
     if (code & HW_NBR_BOUNDARY) {
-      pp = -own[0]; up[0] = um[0]; up[1] = um[1]; up[2] = um[2]; zp = zm;
+      pp = -own[0]; up[0] = um[0]; up[1] = um[1]; up[2] = um[2];
     } else {
       R tr[4];
       staged_trace<N, T, R>(M, Q, code, sne[e * NF + f], f, jj, sm + L::SST + e * L::STG, sem,
                             tr);
       pp = tr[0]; up[0] = tr[1]; up[1] = tr[2]; up[2] = tr[3];
-      zp = sm[L::SZ + e * NF + f];
     }
     R tp, tu, fp, fu;
-    penalties(zm, zp, pen, tp, tu);
+    penalties(g[4], pen, tp, tu);
     upwind_flux(own[0], um, pp, up, nrm, tp, tu, skew, fp, fu);
     sf[(e * NFP + j) * 2 + 0] = fp * g[3];
     sf[(e * NFP + j) * 2 + 1] = fu * g[3];
@@ -471,9 +467,9 @@ __global__ void __launch_bounds__(NT) dense_kernel(hw_mesh_t M, hw_fields_t Q, E
         tu += l * fl[2 * j + 1];
       }
       acc[s][0] += tp;
-      acc[s][1] += g[4 * f + 0] * tu;
-      acc[s][2] += g[4 * f + 1] * tu;
-      acc[s][3] += g[4 * f + 2] * tu;
+      acc[s][1] += g[FS * f + 0] * tu;
+      acc[s][2] += g[FS * f + 1] * tu;
+      acc[s][3] += g[FS * f + 2] * tu;
     }
     const R kap = smat[e * 4 + 0], irho = smat[e * 4 + 1];
     const size_t base = (size_t)sk[e] * 4 * NP + n;
@@ -653,19 +649,17 @@ __global__ void __launch_bounds__(NT) hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi
     const R wJs = sw1[a] * sw1[b] * Js;
     const R um[3] = {own[1], own[2], own[3]};
     const int code = snc[e * 6 + f];
-    const R zm = smat[e * 4 + 2];
-    R pp, up[3], zp;
+    R pp, up[3];
     if (code & HW_NBR_BOUNDARY) {
-      pp = -own[0]; up[0] = um[0]; up[1] = um[1]; up[2] = um[2]; zp = zm;
+      pp = -own[0]; up[0] = um[0]; up[1] = um[1]; up[2] = um[2];
     } else {
       R tr[4];
       staged_trace<N, HW_HEX, R>(M, Q, code, sne[e * 6 + f], f, jj, sm + L::SST + e * L::STG,
                                  sem, tr);
       pp = tr[0]; up[0] = tr[1]; up[1] = tr[2]; up[2] = tr[3];
-      zp = sm[L::SZ + e * 6 + f];
     }
     R tp, tu, fp, fu;
-    penalties(zm, zp, pen, tp, tu);
+    penalties(Xv[24 + f], pen, tp, tu);
     upwind_flux(own[0], um, pp, up, nrm, tp, tu, TY.form == HW_FORM_SKEW, fp, fu);
     R* o = sf + (e * NFP + j) * 4;
     o[0] = fp * wJs;

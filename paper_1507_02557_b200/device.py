@@ -39,11 +39,30 @@ def _affine_check(t, verts, N):
             "currently requires affine wedges and pyramids (DESIGN.md, scope)")
 
 
-def geometry_records(t, verts):
-    """Per-element geometry record (float64 numpy), layouts in the header."""
+def face_impedance_avg(mesh, t):
+    """avg(rho c) of the two sides of every face of type t, (K, nfaces); the
+    own side twice on the boundary (hybridwave/dg.py:249-276)."""
+    def z(tt):
+        m = np.asarray(mesh.materials[tt], dtype=float)
+        return m[:, 0] * np.sqrt(m[:, 1] / m[:, 0])
+    names = ["hex", "wedge", "pyramid", "tet"]
+    nbr = mesh.nbr[t]
+    zm = z(t)
+    zp = np.repeat(zm[:, None], nbr.shape[1], axis=1)
+    for tid, t2 in enumerate(names):
+        sel = nbr[:, :, 0] == tid
+        if sel.any():
+            zp[sel] = z(t2)[nbr[:, :, 1][sel]]
+    return 0.5 * (zm[:, None] + zp)
+
+
+def geometry_records(t, verts, zavg):
+    """Per-element geometry record (float64 numpy), layouts in the header:
+    dense types G(9) [, 1/sqrt(J)] then per face (n, Js-scale, avg(rho c));
+    hex: 8 vertices then avg(rho c) per face."""
     K = len(verts)
     if t == "hex":
-        return verts.reshape(K, 24).copy()
+        return np.hstack([verts.reshape(K, 24), zavg])
     _, J, G, _ = geometric_factors_batch(t, verts, _INTERIOR_ABC[t], label=t)
     J, G = J[:, 0], G[:, 0]
     cols = [G.reshape(K, 9)]
@@ -57,6 +76,7 @@ def geometry_records(t, verts):
         _, Js, nrm = face_geometry_batch(t, verts, f, _CENTROID2D[ftype])
         cols.append(nrm[:, 0, :])
         cols.append((Js[:, 0] * scale)[:, None])
+        cols.append(zavg[:, f:f + 1])
     return np.hstack(cols)
 
 
@@ -119,7 +139,7 @@ def pack_mesh(disc):
         elem, code = neighbour_codes(mesh, t)
         pack["types"][t] = {
             "K": disc.n_elems[t], "form": form, "dops": dops,
-            "geo": geometry_records(t, verts),
+            "geo": geometry_records(t, verts, face_impedance_avg(mesh, t)),
             "mat": material_records(np.asarray(mesh.materials[t], dtype=float)),
             "nbr_elem": elem, "nbr_code": code,
             "op": _pack_ops(t, dops), "iop": _pack_iops(t, dops, disc.N)}
@@ -132,7 +152,18 @@ def _pack_ops(t, d):
     if t == "hex":
         return {0: d["D1"], 1: d["Vend"], 2: d["w1"], 4: _hex_nodes(d)}
     if t == "tet":
-        return {0: np.stack([d["Dr"].T, d["Ds"].T, d["Dt"].T]), 1: d["LIFT"].T}
+        Np = d["Np"]
+        nfn = len(d["tri2d"])
+        rt8, npk, nfk = -(-Np // 8) * 8, -(-Np // 4) * 4, -(-nfn // 4) * 4
+        Dpad = np.zeros((3, rt8, npk))
+        for c, Dc in enumerate((d["Dr"], d["Ds"], d["Dt"])):
+            Dpad[c, :Np, :Np] = Dc
+        Lpad = np.zeros((4, rt8, nfk))
+        for f in range(4):
+            Lpad[f, :Np, :nfn] = d["LIFT"][:, f * nfn:(f + 1) * nfn]
+        # 0, 1: scalar kernel (transposed); 2, 3: DMMA kernel (row-major, padded)
+        return {0: np.stack([d["Dr"].T, d["Ds"].T, d["Dt"].T]), 1: d["LIFT"].T,
+                2: Dpad, 3: Lpad}
     if t == "wedge":
         # op[0][c][m][n] = S_c[n][m], op[1][c][m][n] = S_c[m][n]
         return {0: np.stack([S.T for S in d["S"]]), 1: d["S"], 5: d["E"].T, 6: d["LIFT"].T}

@@ -101,7 +101,7 @@ def rhs(pack, disc, state):
             acc[:, 1:] = -np.einsum("kcx,kcn->kxn", G, dp)
         else:  # hex
             n1 = d["N1"]
-            X = geo.reshape(K, 8, 3)
+            X = geo[:, :24].reshape(K, 8, 3)
             x1 = P["op"][4]
             D1 = P["op"][0]
             u = q[t].reshape(K, 4, n1, n1, n1)
@@ -126,7 +126,6 @@ def rhs(pack, disc, state):
             code = P["nbr_code"][:, f]
             k2 = P["nbr_elem"][:, f]
             oth = np.empty_like(own)
-            zp = zm.copy()
             b = (code & BND) != 0
             oth[b, 0] = -own[b, 0]
             oth[b, 1:] = own[b, 1:]
@@ -142,13 +141,12 @@ def rhs(pack, disc, state):
                 cols = off2[:, None] + perm
                 tr2 = traces[t2][k2[sel]]                                      # (n,4,nfp2)
                 oth[sel] = np.take_along_axis(tr2, np.repeat(cols[:, None, :], 4, axis=1), axis=2)
-                zp[sel] = pack["types"][t2]["mat"][k2[sel], 2]
-            avg = 0.5 * (zm + zp)
+            avg = geo[:, 24 + f] if t == "hex" else geo[:, (10 if t == "wedge" else 9) + 5 * f + 4]
             tp = disc.penalty_scale / avg
             tu = disc.penalty_scale * avg
             if t == "hex":
                 # per-point normal and Js from the face vertices
-                X = geo.reshape(K, 8, 3)[:, list(_HEX_FV[f])]
+                X = geo[:, :24].reshape(K, 8, 3)[:, list(_HEX_FV[f])]
                 x1 = P["op"][4]
                 n1 = d["N1"]
                 jj = np.arange(cnt)
@@ -164,8 +162,8 @@ def rhs(pack, disc, state):
                 scale = w1[jj // n1] * w1[jj % n1] * Js
             else:
                 base = 10 if t == "wedge" else 9
-                nrm = np.repeat(geo[:, base + 4 * f: base + 4 * f + 3][:, None, :], cnt, axis=1)
-                scale = np.repeat(geo[:, base + 4 * f + 3][:, None], cnt, axis=1)
+                nrm = np.repeat(geo[:, base + 5 * f: base + 5 * f + 3][:, None, :], cnt, axis=1)
+                scale = np.repeat(geo[:, base + 5 * f + 3][:, None], cnt, axis=1)
             unm = np.einsum("kpx,kxp->kp", nrm, own[:, 1:])
             unp = np.einsum("kpx,kxp->kp", nrm, oth[:, 1:])
             dp_ = oth[:, 0] - own[:, 0]
@@ -207,7 +205,7 @@ def rhs(pack, disc, state):
                 tp_ = flux[:, 0, off:off + cnt] @ LT[off:off + cnt]
                 tu_ = flux[:, 1, off:off + cnt] @ LT[off:off + cnt]
                 acc[:, 0] += tp_
-                acc[:, 1:] += geo[:, base + 4 * f: base + 4 * f + 3][:, :, None] * tu_[:, None, :]
+                acc[:, 1:] += geo[:, base + 5 * f: base + 5 * f + 3][:, :, None] * tu_[:, None, :]
         acc[:, 0] *= mat[:, 0][:, None]
         acc[:, 1:] *= mat[:, 1][:, None, None]
         out[t] = acc
