@@ -12,9 +12,6 @@
 namespace hw {
 
 static thread_local std::string g_err;
-// HW_DISABLE_MMA=1 selects the scalar dense_kernel for tets (A/B checks)
-static const bool g_disable_mma = getenv("HW_DISABLE_MMA") != nullptr;
-
 static int fail(const char* msg) {
   g_err = msg;
   return 1;
@@ -48,6 +45,17 @@ static int set_smem(KernelT kernel, size_t bytes) {
   }
   done.insert(key);
   return 0;
+}
+
+// HW_TET_KERNEL=scalar selects the scalar dense_kernel for fp64 tets (A/B
+// checks); default: the DMMA kernel
+static bool tet_scalar() {
+  static int v = -1;
+  if (v < 0) {
+    const char* s = getenv("HW_TET_KERNEL");
+    v = (s && !strcmp(s, "scalar")) ? 1 : 0;
+  }
+  return v == 1;
 }
 
 static void subset_of(const hw_subset_t* sub, int t, int64_t K, const int32_t** list,
@@ -94,7 +102,7 @@ static int launch_rhs_all(const hw_mesh_t& M, const hw_fields_t& Q, const Epi& E
       case HW_WEDGE: rc = launch_dense<N, HW_WEDGE, R>(M, Q, E, list, n, st); break;
       case HW_PYRAMID: rc = launch_dense<N, HW_PYRAMID, R>(M, Q, E, list, n, st); break;
       case HW_TET:
-        if (sizeof(R) == 8 && !g_disable_mma) {
+        if (sizeof(R) == 8 && !tet_scalar()) {
           using L = TetMma<N>;
           if ((rc = set_smem(tet_mma_kernel<N>, L::BYTES))) return rc;
           tet_mma_kernel<N><<<(unsigned)((n + L::E - 1) / L::E), L::NTH, L::BYTES, st>>>(

@@ -136,13 +136,15 @@ def pack_mesh(disc):
         _affine_check(t, verts, disc.N)
         dops = device_operators(t, disc.N, disc.formulation.kind, disc.ops[t])
         dops_any = dops
+        perm_tri = face_symmetry_perms("tri", dops["tri2d"])
         elem, code = neighbour_codes(mesh, t)
         pack["types"][t] = {
             "K": disc.n_elems[t], "form": form, "dops": dops,
             "geo": geometry_records(t, verts, face_impedance_avg(mesh, t)),
             "mat": material_records(np.asarray(mesh.materials[t], dtype=float)),
             "nbr_elem": elem, "nbr_code": code,
-            "op": _pack_ops(t, dops), "iop": _pack_iops(t, dops, disc.N)}
+            "op": _pack_ops(t, dops),
+            "iop": _pack_iops(t, dops, disc.N, mesh, perm_tri)}
     pack["perm_tri"] = face_symmetry_perms("tri", dops_any["tri2d"])
     pack["perm_quad"] = face_symmetry_perms("quad", dops_any["quad2d"])
     return pack
@@ -173,11 +175,34 @@ def _pack_ops(t, d):
     raise ValueError(t)
 
 
-def _pack_iops(t, d, N):
+def tet_gather_index(mesh, dops, perm_tri):
+    """(K, 4, NFN) int32: for each tet face node in my face-point order, the
+    flat offset in q (element-major (K,4,Np), field 0) of the coincident
+    node of the neighbour tet; -1 on the boundary, -2 for a non-tet
+    neighbour (direct path in the kernel)."""
+    nbr = mesh.nbr["tet"]
+    code = mesh.face_code["tet"]
+    K = len(nbr)
+    Np = dops["Np"]
+    nfn = len(dops["tri2d"])
+    fn = dops["face_nodes"].reshape(4, nfn)
+    out = np.full((K, 4, nfn), -2, dtype=np.int64)
+    for f in range(4):
+        bnd = nbr[:, f, 0] < 0
+        out[bnd, f, :] = -1
+        sel = nbr[:, f, 0] == 3
+        k2, f2, pc = nbr[sel, f, 1], nbr[sel, f, 2], code[sel, f]
+        out[sel, f, :] = k2[:, None] * 4 * Np + fn[f2[:, None], perm_tri[pc]]
+    if out.max(initial=0) >= 2 ** 31:
+        raise ValueError("tet gather offsets exceed int32")
+    return out.astype(np.int32)
+
+
+def _pack_iops(t, d, N, mesh=None, perm_tri=None):
     if t == "hex":
         return {0: d["face_tab"], 1: hex_node_face_points(d, N)}
     if t == "tet":
-        return {0: d["face_nodes"]}
+        return {0: d["face_nodes"], 1: tet_gather_index(mesh, d, perm_tri)}
     return {}
 
 
