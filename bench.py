@@ -32,7 +32,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "GDOF·stage/s per LSRK step (N=1..5, hybrid mesh, 1/2/4/8 B200); kernel GB/s vs HBM"
 UNIT = "GDOF*stage/s"
-GEO_WORDS = {"hex": 30, "wedge": 35, "pyramid": 34, "tet": 29}
+GEO_WORDS = {"hex": 71, "wedge": 40, "pyramid": 39, "tet": 33}
 NFACES = {"hex": 6, "wedge": 5, "pyramid": 5, "tet": 4}
 
 
@@ -173,12 +173,14 @@ class ClockSampler:
 
 # ------------------------------------------------------------------ GPU arm
 
-def alg_bytes_per_elem(t, Np, s):
+def alg_bytes_per_elem(t, Np, s, N):
     """Compulsory HBM traffic of one LSRK stage per element in this layout:
     read q, read res, write res, write q_out (4 x 4 Np words), geometry
-    record, material record, neighbour index + code per face.  Neighbour
+    record, material record, and the neighbour links (tets: the int32 gather
+    index per face node; other types: index + code per face).  Neighbour
     states are re-read from L2 (not counted)."""
-    return 4 * 4 * Np * s + GEO_WORDS[t] * s + 4 * s + 8 * NFACES[t]
+    links = 4 * 4 * (N + 1) * (N + 2) // 2 if t == "tet" else 8 * NFACES[t]
+    return 4 * 4 * Np * s + GEO_WORDS[t] * s + 4 * s + links
 
 
 def main():
@@ -276,7 +278,7 @@ def main():
         torch.cuda.synchronize()
         us = a.elapsed_time(b) * 1e3 / reps
         Np = disc.ops[t].Np
-        nbytes = disc.n_elems[t] * alg_bytes_per_elem(t, Np, s_bytes)
+        nbytes = disc.n_elems[t] * alg_bytes_per_elem(t, Np, s_bytes, args.order)
         per_type[t] = {"us_per_launch": us, "elements": disc.n_elems[t],
                        "alg_bytes": nbytes, "GBps": nbytes / (us * 1e-6) / 1e9}
     dom = max(per_type, key=lambda t: per_type[t]["us_per_launch"])

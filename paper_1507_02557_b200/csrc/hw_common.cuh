@@ -24,10 +24,14 @@ struct Dims {
   static constexpr int NFP_PYR = NFQ + 4 * NFN;
 };
 
-// geometry record words per element; per face FS words (n_x, n_y, n_z,
-// Jacobian scale, avg(rho c) of the two sides) after GF (dense types) or
-// avg(rho c) at 24 + f (hex, after the 8 vertices)
-constexpr int GEO_HEX = 30, GEO_WEDGE = 35, GEO_PYR = 34, GEO_TET = 29, FS = 5;
+// geometry record words per element.  Dense types: G[3][3] (+ 1/sqrt(J)
+// for wedges) then per face FS words (n_x, n_y, n_z, Jacobian scale,
+// avg(rho c), 1/avg(rho c)).  Hex: 8 vertices, per face (avg, 1/avg), an
+// affine flag, then for affine hexes G[3][3], J and per face (n, Js).
+constexpr int FS = 6;
+constexpr int GEO_HEX = 71, GEO_WEDGE = 10 + 5 * FS, GEO_PYR = 9 + 5 * FS,
+              GEO_TET = 9 + 4 * FS;
+constexpr int HX_Z = 24, HX_AFF = 36, HX_G = 37, HX_J = 46, HX_F = 47;
 constexpr int NF_HEX = 6, NF_WEDGE = 5, NF_PYR = 5, NF_TET = 4;
 
 // epilogue of the fused RHS kernels
@@ -90,8 +94,8 @@ __device__ __forceinline__ void upwind_flux(R pm, const R um[3], R pp, const R u
 // penalties from avg(rho c) of the two sides (hybridwave/dg.py:61-69,
 // 341-342); avg is precomputed per face on the host
 template <typename R>
-__device__ __forceinline__ void penalties(R avg, R scale, R& tp, R& tu) {
-  tp = scale / avg;
+__device__ __forceinline__ void penalties(R avg, R inv_avg, R scale, R& tp, R& tu) {
+  tp = scale * inv_avg;
   tu = scale * avg;
 }
 

@@ -440,7 +440,7 @@ __global__ void __launch_bounds__(NT) dense_kernel(hw_mesh_t M, hw_fields_t Q, E
       pp = tr[0]; up[0] = tr[1]; up[1] = tr[2]; up[2] = tr[3];
     }
     R tp, tu, fp, fu;
-    penalties(g[4], pen, tp, tu);
+    penalties(g[4], g[5], pen, tp, tu);
     upwind_flux(own[0], um, pp, up, nrm, tp, tu, skew, fp, fu);
     sf[(e * NFP + j) * 2 + 0] = fp * g[3];
     sf[(e * NFP + j) * 2 + 1] = fu * g[3];
@@ -584,7 +584,15 @@ __global__ void __launch_bounds__(NT) hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi
         d[f][0] = a0; d[f][1] = a1; d[f][2] = a2;
       }
       R G[9];
-      const R J = hex_metric<R>(sg + e * GEO_HEX, sx[ii], sx[jj], sx[kk], G);
+      R J;
+      const R* Xe = sg + e * GEO_HEX;
+      if (Xe[HX_AFF] != R(0)) {       // affine: constant metric from the record
+#pragma unroll
+        for (int a = 0; a < 9; ++a) G[a] = Xe[HX_G + a];
+        J = Xe[HX_J];
+      } else {
+        J = hex_metric<R>(Xe, sx[ii], sx[jj], sx[kk], G);
+      }
       R div = R(0);
 #pragma unroll
       for (int x = 0; x < 3; ++x) {
@@ -625,6 +633,12 @@ __global__ void __launch_bounds__(NT) hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi
     const int a = jj / N1, b = jj - a * N1;
     const R xi = sx[a], eta = sx[b];
     const R* Xv = sg + e * GEO_HEX;
+    R nrm[3], Js;
+    if (Xv[HX_AFF] != R(0)) {
+      const R* fr = Xv + HX_F + 4 * f;
+      nrm[0] = fr[0]; nrm[1] = fr[1]; nrm[2] = fr[2];
+      Js = fr[3];
+    } else {
     R t1[3], t2[3];
     {
       const R g1[4] = {-(R(1) - eta), (R(1) - eta), (R(1) + eta), -(R(1) + eta)};
@@ -644,8 +658,9 @@ __global__ void __launch_bounds__(NT) hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi
     }
     const R nv[3] = {t1[1] * t2[2] - t1[2] * t2[1], t1[2] * t2[0] - t1[0] * t2[2],
                      t1[0] * t2[1] - t1[1] * t2[0]};
-    const R Js = sqrt(nv[0] * nv[0] + nv[1] * nv[1] + nv[2] * nv[2]);
-    const R nrm[3] = {nv[0] / Js, nv[1] / Js, nv[2] / Js};
+    Js = sqrt(nv[0] * nv[0] + nv[1] * nv[1] + nv[2] * nv[2]);
+    nrm[0] = nv[0] / Js; nrm[1] = nv[1] / Js; nrm[2] = nv[2] / Js;
+    }
     const R wJs = sw1[a] * sw1[b] * Js;
     const R um[3] = {own[1], own[2], own[3]};
     const int code = snc[e * 6 + f];
@@ -659,7 +674,7 @@ __global__ void __launch_bounds__(NT) hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi
       pp = tr[0]; up[0] = tr[1]; up[1] = tr[2]; up[2] = tr[3];
     }
     R tp, tu, fp, fu;
-    penalties(Xv[24 + f], pen, tp, tu);
+    penalties(Xv[HX_Z + 2 * f], Xv[HX_Z + 2 * f + 1], pen, tp, tu);
     upwind_flux(own[0], um, pp, up, nrm, tp, tu, TY.form == HW_FORM_SKEW, fp, fu);
     R* o = sf + (e * NFP + j) * 4;
     o[0] = fp * wJs;

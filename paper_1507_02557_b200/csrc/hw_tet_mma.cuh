@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(TetMma<N>::NTH, TetMma<N>::MINB)
       pp = tr[0]; up[0] = tr[1]; up[1] = tr[2]; up[2] = tr[3];
     }
     R tp, tu, fp, fu;
-    penalties(g[4], pen, tp, tu);
+    penalties(g[4], g[5], pen, tp, tu);
     upwind_flux(pm, um, pp, up, nrm, tp, tu, false, fp, fu);
     sfp[e * EF + f * NFK + jj] = fp * g[3];
     sfu[e * EF + f * NFK + jj] = fu * g[3];

@@ -58,11 +58,28 @@ def face_impedance_avg(mesh, t):
 
 def geometry_records(t, verts, zavg):
     """Per-element geometry record (float64 numpy), layouts in the header:
-    dense types G(9) [, 1/sqrt(J)] then per face (n, Js-scale, avg(rho c));
-    hex: 8 vertices then avg(rho c) per face."""
+    dense types G(9) [, 1/sqrt(J)] then per face (n, Js-scale, avg(rho c),
+    1/avg(rho c)); hex: 8 vertices, per face (avg, 1/avg), affine flag, and
+    for affine hexes G(9), J, per face (n, Js)."""
     K = len(verts)
     if t == "hex":
-        return np.hstack([verts.reshape(K, 24), zavg])
+        out = np.zeros((K, 71))
+        out[:, :24] = verts.reshape(K, 24)
+        out[:, 24:36:2] = zavg
+        out[:, 25:36:2] = 1.0 / zavg
+        # affine hexes (parallelepipeds): constant metric and face geometry
+        c = np.array([[-0.9, -0.7, -0.8], [0.0, 0.0, 0.0], [0.6, 0.9, -0.5]])
+        _, J, G, _ = geometric_factors_batch("hex", verts, c, label=t)
+        aff = (np.abs(G - G[:, :1]).max(axis=(1, 2, 3)) <= 1e-13 * np.abs(G).max(axis=(1, 2, 3))) & \
+              (np.abs(J - J[:, :1]).max(axis=1) <= 1e-13 * J.max(axis=1))
+        out[:, 36] = aff.astype(float)
+        out[:, 37:46] = G[:, 1].reshape(K, 9)
+        out[:, 46] = J[:, 1]
+        for f in range(6):
+            _, Js, nrm = face_geometry_batch("hex", verts, f, _CENTROID2D["quad"])
+            out[:, 47 + 4 * f: 50 + 4 * f] = nrm[:, 0]
+            out[:, 50 + 4 * f] = Js[:, 0]
+        return out
     _, J, G, _ = geometric_factors_batch(t, verts, _INTERIOR_ABC[t], label=t)
     J, G = J[:, 0], G[:, 0]
     cols = [G.reshape(K, 9)]
@@ -77,6 +94,7 @@ def geometry_records(t, verts, zavg):
         cols.append(nrm[:, 0, :])
         cols.append((Js[:, 0] * scale)[:, None])
         cols.append(zavg[:, f:f + 1])
+        cols.append(1.0 / zavg[:, f:f + 1])
     return np.hstack(cols)
 
 

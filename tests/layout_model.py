@@ -141,8 +141,12 @@ def rhs(pack, disc, state):
                 cols = off2[:, None] + perm
                 tr2 = traces[t2][k2[sel]]                                      # (n,4,nfp2)
                 oth[sel] = np.take_along_axis(tr2, np.repeat(cols[:, None, :], 4, axis=1), axis=2)
-            avg = geo[:, 24 + f] if t == "hex" else geo[:, (10 if t == "wedge" else 9) + 5 * f + 4]
-            tp = disc.penalty_scale / avg
+            if t == "hex":
+                avg, inv = geo[:, 24 + 2 * f], geo[:, 25 + 2 * f]
+            else:
+                b0 = (10 if t == "wedge" else 9) + 6 * f
+                avg, inv = geo[:, b0 + 4], geo[:, b0 + 5]
+            tp = disc.penalty_scale * inv
             tu = disc.penalty_scale * avg
             if t == "hex":
                 # per-point normal and Js from the face vertices
@@ -162,8 +166,8 @@ def rhs(pack, disc, state):
                 scale = w1[jj // n1] * w1[jj % n1] * Js
             else:
                 base = 10 if t == "wedge" else 9
-                nrm = np.repeat(geo[:, base + 5 * f: base + 5 * f + 3][:, None, :], cnt, axis=1)
-                scale = np.repeat(geo[:, base + 5 * f + 3][:, None], cnt, axis=1)
+                nrm = np.repeat(geo[:, base + 6 * f: base + 6 * f + 3][:, None, :], cnt, axis=1)
+                scale = np.repeat(geo[:, base + 6 * f + 3][:, None], cnt, axis=1)
             unm = np.einsum("kpx,kxp->kp", nrm, own[:, 1:])
             unp = np.einsum("kpx,kxp->kp", nrm, oth[:, 1:])
             dp_ = oth[:, 0] - own[:, 0]
@@ -205,7 +209,7 @@ def rhs(pack, disc, state):
                 tp_ = flux[:, 0, off:off + cnt] @ LT[off:off + cnt]
                 tu_ = flux[:, 1, off:off + cnt] @ LT[off:off + cnt]
                 acc[:, 0] += tp_
-                acc[:, 1:] += geo[:, base + 5 * f: base + 5 * f + 3][:, :, None] * tu_[:, None, :]
+                acc[:, 1:] += geo[:, base + 6 * f: base + 6 * f + 3][:, :, None] * tu_[:, None, :]
         acc[:, 0] *= mat[:, 0][:, None]
         acc[:, 1:] *= mat[:, 1][:, None, None]
         out[t] = acc
