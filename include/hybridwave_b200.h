@@ -68,6 +68,13 @@ typedef struct {
   double penalty_scale;      /* hybridwave/dg.py:341-342                  */
   const int32_t* perm_tri;   /* (6, (N+1)(N+2)/2) face-point permutations */
   const int32_t* perm_quad;  /* (8, (N+1)^2)                              */
+  /* Face-trace buffers (K, 4, Nfp) of the publishing types (wedge, pyramid,
+   * and hex under GL; NULL for the others): tr_in holds the traces of the
+   * input state of a stage, tr_out receives those of its output state
+   * (LSRK / AB epilogue; may be NULL).  hw_rhs fills tr_in itself; before
+   * the first hw_lsrk_stage / hw_ab_step call hw_traces. */
+  void* tr_in[HW_NTYPES];
+  void* tr_out[HW_NTYPES];
   hw_type_t t[HW_NTYPES];
 } hw_mesh_t;
 
@@ -87,6 +94,11 @@ typedef struct {
  * Discretization.compute_rhs (hybridwave/dg.py:492-506, forcing = None). */
 int hw_rhs(const hw_mesh_t* mesh, const hw_fields_t* q, hw_fields_t* rhs,
            const hw_subset_t* subset, void* stream);
+
+/* Face traces of q for the publishing types into tr (same layout as
+ * mesh->tr_in); the state's traces at the device face points. */
+int hw_traces(const hw_mesh_t* mesh, const hw_fields_t* q, hw_fields_t* tr,
+              const hw_subset_t* subset, void* stream);
 
 /* One low-storage RK stage (Carpenter-Kennedy (4,5), 2N storage):
  *   res = a*res + dt*rhs(q_in);  q_out = q_in + b*res.

@@ -30,6 +30,7 @@ class HWMesh(ctypes.Structure):
     _fields_ = [("N", c_int32), ("dtype", c_int32), ("formulation", c_int32),
                 ("pad_", c_int32), ("penalty_scale", c_double),
                 ("perm_tri", c_void_p), ("perm_quad", c_void_p),
+                ("tr_in", c_void_p * 4), ("tr_out", c_void_p * 4),
                 ("t", HWType * 4)]
 
 
@@ -59,6 +60,7 @@ def lib():
         L = ctypes.CDLL(LIB_PATH)
         P = ctypes.POINTER
         L.hw_rhs.argtypes = [P(HWMesh), P(HWFields), P(HWFields), P(HWSubset), c_void_p]
+        L.hw_traces.argtypes = [P(HWMesh), P(HWFields), P(HWFields), P(HWSubset), c_void_p]
         L.hw_lsrk_stage.argtypes = [P(HWMesh), P(HWFields), P(HWFields), P(HWFields),
                                     c_double, c_double, c_double, P(HWSubset), c_void_p]
         L.hw_ab_step.argtypes = [P(HWMesh), P(HWFields), P(HWFields), P(HWFields),
@@ -73,7 +75,7 @@ def lib():
                                    c_void_p, c_void_p]
         L.hw_energy.argtypes = [P(HWMesh), P(HWFields), c_void_p, c_void_p]
         L.hw_last_error.restype = ctypes.c_char_p
-        for name in ("hw_rhs", "hw_lsrk_stage", "hw_ab_step", "hw_axpy3",
+        for name in ("hw_rhs", "hw_traces", "hw_lsrk_stage", "hw_ab_step", "hw_axpy3",
                      "hw_hist_push", "hw_halo_pack", "hw_energy", "hw_version",
                      "hw_supported_orders"):
             getattr(L, name).restype = c_int
@@ -81,7 +83,7 @@ def lib():
     return _lib
 
 
-EXPORTED_SYMBOLS = ("hw_rhs", "hw_lsrk_stage", "hw_ab_step", "hw_axpy3", "hw_hist_push",
+EXPORTED_SYMBOLS = ("hw_rhs", "hw_traces", "hw_lsrk_stage", "hw_ab_step", "hw_axpy3", "hw_hist_push",
                     "hw_halo_pack", "hw_energy", "hw_last_error", "hw_version",
                     "hw_supported_orders")
 

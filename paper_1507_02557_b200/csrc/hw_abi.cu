@@ -79,6 +79,38 @@ static int launch_dense(const hw_mesh_t& M, const hw_fields_t& Q, const Epi& E,
   return check_launch("dense_kernel");
 }
 
+template <int N, int T, typename R>
+static int launch_traces_t(const hw_mesh_t& M, const hw_fields_t& Q, const hw_fields_t& TR,
+                           const int32_t* list, int64_t n, cudaStream_t st) {
+  constexpr int NP = TT<N, T>::NP;
+  constexpr int EPB = (NT / NP) > 0 ? (NT / NP) : 1;
+  trace_kernel<N, T, R><<<(unsigned)((n + EPB - 1) / EPB), NT, 0, st>>>(M, Q, TR, list, n);
+  return check_launch("trace_kernel");
+}
+
+// face traces of every publishing type (wedge, pyramid, GL hex) of q -> TR
+template <int N, typename R>
+static int launch_traces_all(const hw_mesh_t& M, const hw_fields_t& Q, const hw_fields_t& TR,
+                             const hw_subset_t* sub, cudaStream_t st) {
+  int rc = 0;
+  for (int t = 0; t < HW_NTYPES; ++t) {
+    const int64_t K = M.t[t].K;
+    if (K <= 0) continue;
+    const bool pub = t == HW_WEDGE || t == HW_PYRAMID || (t == HW_HEX && M.formulation == HW_GL);
+    if (!pub) continue;
+    if (!TR.p[t]) return fail("missing trace buffer for a publishing element type");
+    const int32_t* list;
+    int64_t n;
+    subset_of(sub, t, K, &list, &n);
+    if (n <= 0) continue;
+    if (t == HW_HEX) rc = launch_traces_t<N, HW_HEX, R>(M, Q, TR, list, n, st);
+    else if (t == HW_WEDGE) rc = launch_traces_t<N, HW_WEDGE, R>(M, Q, TR, list, n, st);
+    else rc = launch_traces_t<N, HW_PYRAMID, R>(M, Q, TR, list, n, st);
+    if (rc) return rc;
+  }
+  return 0;
+}
+
 template <int N, typename R>
 static int launch_rhs_all(const hw_mesh_t& M, const hw_fields_t& Q, const Epi& E,
                           const hw_subset_t* sub, cudaStream_t st) {
@@ -139,6 +171,34 @@ static int dispatch_rhs(const hw_mesh_t& M, const hw_fields_t& Q, const Epi& E,
 #endif
     default: return fail("polynomial order not compiled into this library");
   }
+}
+
+template <typename R>
+static int dispatch_traces(const hw_mesh_t& M, const hw_fields_t& Q, const hw_fields_t& TR,
+                           const hw_subset_t* sub, cudaStream_t st) {
+  switch (M.N) {
+    case 1: return launch_traces_all<1, R>(M, Q, TR, sub, st);
+    case 2: return launch_traces_all<2, R>(M, Q, TR, sub, st);
+    case 3: return launch_traces_all<3, R>(M, Q, TR, sub, st);
+    case 4: return launch_traces_all<4, R>(M, Q, TR, sub, st);
+    case 5: return launch_traces_all<5, R>(M, Q, TR, sub, st);
+#if HW_MAX_ORDER >= 6
+    case 6: return launch_traces_all<6, R>(M, Q, TR, sub, st);
+#endif
+#if HW_MAX_ORDER >= 7
+    case 7: return launch_traces_all<7, R>(M, Q, TR, sub, st);
+#endif
+    default: return fail("polynomial order not compiled into this library");
+  }
+}
+
+static int run_traces(const hw_mesh_t* M, const hw_fields_t* Q, const hw_fields_t* TR,
+                      const hw_subset_t* sub, void* stream) {
+  if (!M || !Q || !TR) return fail("null mesh, fields or trace buffers");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (M->dtype == HW_F64) return dispatch_traces<double>(*M, *Q, *TR, sub, st);
+  if (M->dtype == HW_F32) return dispatch_traces<float>(*M, *Q, *TR, sub, st);
+  return fail("unknown dtype");
 }
 
 static int run_rhs(const hw_mesh_t* M, const hw_fields_t* Q, const Epi& E,
@@ -229,9 +289,22 @@ int hw_supported_orders(void) {
 
 const char* hw_last_error(void) { return g_err.c_str(); }
 
+int hw_traces(const hw_mesh_t* mesh, const hw_fields_t* q, hw_fields_t* tr,
+              const hw_subset_t* subset, void* stream) {
+  return run_traces(mesh, q, tr, subset, stream);
+}
+
 int hw_rhs(const hw_mesh_t* mesh, const hw_fields_t* q, hw_fields_t* rhs,
            const hw_subset_t* subset, void* stream) {
   if (!rhs) return fail("null rhs");
+  if (!mesh) return fail("null mesh");
+  {   // traces of q for the publishing types, on every element (neighbours of
+      // a subset need them too)
+    hw_fields_t tr;
+    for (int t = 0; t < HW_NTYPES; ++t) tr.p[t] = mesh->tr_in[t];
+    int rc = run_traces(mesh, q, &tr, nullptr, stream);
+    if (rc) return rc;
+  }
   Epi E;
   memset(&E, 0, sizeof(E));
   E.mode = MODE_RHS;

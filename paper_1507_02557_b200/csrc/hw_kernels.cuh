@@ -29,8 +29,6 @@ struct TT<N, HW_TET> {
   __host__ __device__ static constexpr bool tri(int) { return true; }
   __host__ __device__ static constexpr int off(int f) { return f * D::NFN; }
   __host__ __device__ static constexpr int cnt(int) { return D::NFN; }
-  // staging budget per face: tet neighbours only (the rare dense neighbours
-  // of a tet take the direct path, neighbour_trace)
   __host__ __device__ static constexpr int stage(int) { return 4 * D::NFN; }
 };
 
@@ -43,10 +41,7 @@ struct TT<N, HW_WEDGE> {
     return f < 2 ? f * D::NFN : 2 * D::NFN + (f - 2) * D::NFQ;
   }
   __host__ __device__ static constexpr int cnt(int f) { return f < 2 ? D::NFN : D::NFQ; }
-  __host__ __device__ static constexpr int stage(int f) {
-    return tri(f) ? 4 * cmax(D::NFN, cmax(D::NP_WEDGE, D::NP_PYR))
-                  : 4 * cmax(D::NFQ * D::N1, cmax(D::NP_WEDGE, D::NP_PYR));
-  }
+  __host__ __device__ static constexpr int stage(int f) { return 4 * cnt(f); }
 };
 
 template <int N>
@@ -58,10 +53,7 @@ struct TT<N, HW_PYRAMID> {
     return f == 0 ? 0 : D::NFQ + (f - 1) * D::NFN;
   }
   __host__ __device__ static constexpr int cnt(int f) { return f == 0 ? D::NFQ : D::NFN; }
-  __host__ __device__ static constexpr int stage(int f) {
-    return tri(f) ? 4 * cmax(D::NFN, cmax(D::NP_WEDGE, D::NP_PYR))
-                  : 4 * cmax(D::NFQ * D::N1, cmax(D::NP_WEDGE, D::NP_PYR));
-  }
+  __host__ __device__ static constexpr int stage(int f) { return 4 * cnt(f); }
 };
 
 template <int N>
@@ -71,9 +63,7 @@ struct TT<N, HW_HEX> {
   __host__ __device__ static constexpr bool tri(int) { return false; }
   __host__ __device__ static constexpr int off(int f) { return f * D::NFQ; }
   __host__ __device__ static constexpr int cnt(int) { return D::NFQ; }
-  __host__ __device__ static constexpr int stage(int) {
-    return 4 * cmax(D::NFQ * D::N1, cmax(D::NP_WEDGE, D::NP_PYR));
-  }
+  __host__ __device__ static constexpr int stage(int) { return 4 * D::NFQ; }
 };
 
 template <int N, int T>
@@ -109,21 +99,24 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_all;\n" ::: "memory");
 }
 
-// number of staged values for a neighbour of type t2
-template <int N>
-__device__ __forceinline__ int stage_count(int t2, bool sem) {
-  using D = Dims<N>;
-  switch (t2) {
-    case HW_TET: return 4 * D::NFN;
-    case HW_HEX: return sem ? 4 * D::NFQ : 4 * D::NFQ * D::N1;
-    case HW_WEDGE: return 4 * D::NP_WEDGE;
-    default: return 4 * D::NP_PYR;
-  }
+// Types whose face traces are published in the trace buffers (their traces
+// are dense contractions / interpolations); tets and SEM hexes are read
+// straight from the state (their traces are selections).
+__device__ __forceinline__ bool publishes(int t, bool sem) {
+  return t == HW_WEDGE || t == HW_PYRAMID || (t == HW_HEX && !sem);
 }
 
-// P1: one warp per (element, face) pair copies what the neighbour trace
-// needs: tet face-node values (4 x NFN), hex SEM face values (4 x NFQ), hex
-// GL normal lines (4 x NFQ x N1), or the whole wedge/pyramid state.
+template <int N>
+__device__ __forceinline__ int nfp_of(int t) {
+  using D = Dims<N>;
+  return t == HW_HEX ? D::NFP_HEX : t == HW_TET ? D::NFP_TET
+                     : t == HW_WEDGE ? D::NFP_WEDGE : D::NFP_PYR;
+}
+
+// P1: one warp per (element, face) pair copies the neighbour's face values
+// (4 fields x cnt points, in the neighbour's own point order): a contiguous
+// trace-buffer row for publishing neighbours, selected face nodes of the
+// state for tets and SEM hexes.
 template <int N, int T, typename R>
 __device__ __forceinline__ void stage_neighbours(const hw_mesh_t& M, const hw_fields_t& Q,
                                                  const int* snc, const int* sne, int ne,
@@ -136,94 +129,89 @@ __device__ __forceinline__ void stage_neighbours(const hw_mesh_t& M, const hw_fi
     const int code = snc[pr];
     if (code & HW_NBR_BOUNDARY) continue;
     const int t2 = HW_NBR_TYPE(code), f2 = HW_NBR_FACE(code);
-    if (stage_count<N>(t2, sem) > X::stage(f)) continue;   // direct path later
     const int k2 = sne[pr];
+    const int cnt = X::cnt(f);
     R* dst = st + e * stage_off<N, T>(X::NF) + stage_off<N, T>(f);
-    if (t2 == HW_TET) {
+    if (publishes(t2, sem)) {
+      const int nfp2 = nfp_of<N>(t2);
+      const R* src = (const R*)M.tr_in[t2] + (size_t)k2 * 4 * nfp2 + face_offset<N>(t2, f2);
+      for (int i = lane; i < 4 * cnt; i += 32) {
+        const int c = i / cnt, p = i - c * cnt;
+        cp_async(dst + i, src + c * nfp2 + p);
+      }
+    } else if (t2 == HW_TET) {
       const R* q2 = (const R*)Q.p[HW_TET] + (size_t)k2 * 4 * D::NP_TET;
       const int* fn = M.t[HW_TET].iop[0] + f2 * D::NFN;
       for (int i = lane; i < 4 * D::NFN; i += 32) {
         const int c = i / D::NFN, n = i - c * D::NFN;
         cp_async(dst + i, q2 + c * D::NP_TET + __ldg(fn + n));
       }
-    } else if (t2 == HW_HEX) {
+    } else {   // SEM hex: face nodes
       const R* q2 = (const R*)Q.p[HW_HEX] + (size_t)k2 * 4 * D::NP_HEX;
       const int* tab = M.t[HW_HEX].iop[0] + 3 * f2 * D::NFQ;
-      if (sem) {
-        for (int i = lane; i < 4 * D::NFQ; i += 32) {
-          const int c = i / D::NFQ, p = i - c * D::NFQ;
-          const int base = __ldg(tab + 3 * p), stride = __ldg(tab + 3 * p + 1),
-                    end = __ldg(tab + 3 * p + 2);
-          cp_async(dst + i, q2 + c * D::NP_HEX + base + (end ? N : 0) * stride);
-        }
-      } else {
-        for (int i = lane; i < 4 * D::NFQ * D::N1; i += 32) {
-          const int l = i % D::N1, cpi = i / D::N1;
-          const int c = cpi / D::NFQ, p = cpi - c * D::NFQ;
-          const int base = __ldg(tab + 3 * p), stride = __ldg(tab + 3 * p + 1);
-          cp_async(dst + i, q2 + c * D::NP_HEX + base + l * stride);
-        }
+      for (int i = lane; i < 4 * D::NFQ; i += 32) {
+        const int c = i / D::NFQ, p = i - c * D::NFQ;
+        const int base = __ldg(tab + 3 * p), stride = __ldg(tab + 3 * p + 1),
+                  end = __ldg(tab + 3 * p + 2);
+        cp_async(dst + i, q2 + c * D::NP_HEX + base + (end ? N : 0) * stride);
       }
-    } else {
-      const int np = (t2 == HW_WEDGE) ? D::NP_WEDGE : D::NP_PYR;
-      const R* q2 = (const R*)Q.p[t2] + (size_t)k2 * 4 * np;
-      for (int i = lane; i < 4 * np; i += 32) cp_async(dst + i, q2 + i);
     }
   }
 }
 
-// neighbour trace at my face point jj from the staged data (or the direct
-// global path when the neighbour was not staged)
+// neighbour trace at my face point jj from the staged face values
 template <int N, int T, typename R>
-__device__ __forceinline__ void staged_trace(const hw_mesh_t& M, const hw_fields_t& Q,
-                                             int code, int k2, int f, int jj, const R* st_e,
-                                             bool sem, R tr[4]) {
+__device__ __forceinline__ void staged_trace(const hw_mesh_t& M, int code, int f, int jj,
+                                             const R* st_e, R tr[4]) {
   using X = TT<N, T>;
   using D = Dims<N>;
-  const int t2 = HW_NBR_TYPE(code), f2 = HW_NBR_FACE(code), pc = HW_NBR_PERM(code);
-  if (stage_count<N>(t2, sem) > X::stage(f)) {
-    neighbour_trace<N, R>(M, Q, code, k2, jj, X::tri(f), tr);
-    return;
-  }
+  const int pc = HW_NBR_PERM(code);
+  const int cnt = X::cnt(f);
   const int p = X::tri(f) ? __ldg(M.perm_tri + pc * D::NFN + jj)
                           : __ldg(M.perm_quad + pc * D::NFQ + jj);
   const R* s = st_e + stage_off<N, T>(f);
-  if (t2 == HW_TET) {
 #pragma unroll
-    for (int c = 0; c < 4; ++c) tr[c] = s[c * D::NFN + p];
-  } else if (t2 == HW_HEX) {
-    if (sem) {
+  for (int c = 0; c < 4; ++c) tr[c] = s[c * cnt + p];
+}
+
+// Face traces of element states held element-major in smem (sq[e][c][n],
+// element stride 4*Np) -> trace buffer rows tr[k][c][j].  Dense types:
+// E q (wedge x 1/sqrt(J)); GL hex: 1-D endpoint interpolation.
+template <int N, int T, typename R>
+__device__ __forceinline__ void publish_traces(const hw_mesh_t& M, const R* sq, const R* sg,
+                                               const int* sk, int ne, R* tr) {
+  using X = TT<N, T>;
+  using D = Dims<N>;
+  constexpr int NP = X::NP, NFP = X::NFP;
+  const hw_type_t& TY = M.t[T];
+  for (int i = threadIdx.x; i < ne * NFP; i += blockDim.x) {
+    const int e = i / NFP, j = i - e * NFP;
+    const R* qe = sq + e * 4 * NP;
+    R a0 = R(0), a1 = R(0), a2 = R(0), a3 = R(0);
+    if (T == HW_HEX) {
+      const int* tab = TY.iop[0] + 3 * j;
+      const int base = __ldg(tab), stride = __ldg(tab + 1), end = __ldg(tab + 2);
+      const R* ve = (const R*)TY.op[1] + end * D::N1;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) tr[c] = s[c * D::NFQ + p];
+      for (int l = 0; l < D::N1; ++l) {
+        const R w = ldg(ve + l);
+        const int n = base + l * stride;
+        a0 += w * qe[n]; a1 += w * qe[NP + n]; a2 += w * qe[2 * NP + n]; a3 += w * qe[3 * NP + n];
+      }
     } else {
-      const R* ve = (const R*)M.t[HW_HEX].op[1] + (f2 & 1) * D::N1;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        R a = R(0);
-#pragma unroll
-        for (int l = 0; l < D::N1; ++l) a += ldg(ve + l) * s[(c * D::NFQ + p) * D::N1 + l];
-        tr[c] = a;
+      const R* ET = (const R*)TY.op[5];
+#pragma unroll 4
+      for (int m = 0; m < NP; ++m) {
+        const R ev = ldg(ET + m * NFP + j);
+        a0 += ev * qe[m]; a1 += ev * qe[NP + m]; a2 += ev * qe[2 * NP + m]; a3 += ev * qe[3 * NP + m];
+      }
+      if (T == HW_WEDGE) {
+        const R isj = sg[e * X::GEO + 9];
+        a0 *= isj; a1 *= isj; a2 *= isj; a3 *= isj;
       }
     }
-  } else {
-    const int np = (t2 == HW_WEDGE) ? D::NP_WEDGE : D::NP_PYR;
-    const int nfp = (t2 == HW_WEDGE) ? D::NFP_WEDGE : D::NFP_PYR;
-    const R* ET = (const R*)M.t[t2].op[5] + face_offset<N>(t2, f2) + p;
-    R a0 = R(0), a1 = R(0), a2 = R(0), a3 = R(0);
-#pragma unroll 4
-    for (int m = 0; m < np; ++m) {
-      const R e = ldg(ET + (size_t)m * nfp);
-      a0 += e * s[m];
-      a1 += e * s[np + m];
-      a2 += e * s[2 * np + m];
-      a3 += e * s[3 * np + m];
-    }
-    tr[0] = a0; tr[1] = a1; tr[2] = a2; tr[3] = a3;
-    if (t2 == HW_WEDGE) {
-      const R sc = ldg((const R*)M.t[HW_WEDGE].geo + (size_t)k2 * GEO_WEDGE + 9);
-#pragma unroll
-      for (int c = 0; c < 4; ++c) tr[c] *= sc;
-    }
+    R* o = tr + (size_t)sk[e] * 4 * NFP + j;
+    o[0] = a0; o[NFP] = a1; o[2 * NFP] = a2; o[3 * NFP] = a3;
   }
 }
 
@@ -244,7 +232,8 @@ struct Smem {
   static constexpr int SG = SF + EPB * NFP * FLUXW;
   static constexpr int SMAT = SG + EPB * X::GEO;
   static constexpr int SST = SMAT + EPB * 4;
-  static constexpr int SOPS = SST + EPB * STG;              // hex: D1, nodes, w, Vend
+  static constexpr int STR = SST + EPB * STG;               // own traces (publishing types)
+  static constexpr int SOPS = STR + ((T == HW_TET) ? 0 : EPB * 4 * NFP);  // hex: D1, x, w, Vend
   static constexpr int TOTAL = SOPS + ((T == HW_HEX) ? (N + 1) * (N + 1) + 4 * (N + 1) : 0);
   static constexpr size_t BYTES = sizeof(R) * TOTAL + sizeof(int) * (2 * EPB * NF + EPB);
 };
@@ -278,8 +267,16 @@ __device__ __forceinline__ void prologue(const hw_mesh_t& M, const hw_fields_t& 
     sne[i] = k2;
   }
   __syncthreads();
-  // P1: asynchronous staging (neighbour data, LSRK residual)
-  stage_neighbours<N, T, R>(M, Q, snc, sne, ne, sm + L::SST, M.formulation == HW_SEM);
+  // P1: asynchronous staging (neighbour face values, own traces, LSRK residual)
+  const bool sem = M.formulation == HW_SEM;
+  stage_neighbours<N, T, R>(M, Q, snc, sne, ne, sm + L::SST, sem);
+  if (T != HW_TET && publishes(T, sem)) {
+    const R* tr = (const R*)M.tr_in[T];
+    for (int i = tid; i < ne * 4 * L::NFP; i += NT) {
+      const int e = i / (4 * L::NFP), r = i - e * 4 * L::NFP;
+      cp_async(sm + L::STR + i, tr + (size_t)sk[e] * 4 * L::NFP + r);
+    }
+  }
   if (E.mode == MODE_LSRK) {
     const R* res = (const R*)E.res[T];
     for (int i = tid; i < ne * 4 * L::NP; i += NT) {
@@ -288,6 +285,29 @@ __device__ __forceinline__ void prologue(const hw_mesh_t& M, const hw_fields_t& 
     }
   }
   cp_async_commit();
+}
+
+// epilogue returning the new state value (LSRK / AB; RHS mode returns qv)
+template <typename R>
+__device__ __forceinline__ R epilogue_q(const Epi& E, int t, size_t idx, R v, R qv, R resv) {
+  if (E.mode == MODE_LSRK) {
+    const R r = R(E.a) * resv + R(E.dt) * v;
+    ((R*)E.res[t])[idx] = r;
+    const R qn = qv + R(E.b) * r;
+    ((R*)E.qout[t])[idx] = qn;
+    return qn;
+  }
+  if (E.mode == MODE_RHS) {
+    ((R*)E.out[t])[idx] = v;
+    return qv;
+  }
+  ((R*)E.out[t])[idx] = v;
+  R acc = R(E.c0) * v;
+  if (E.nhist > 1) acc += R(E.c1) * ((const R*)E.h1[t])[idx];
+  if (E.nhist > 2) acc += R(E.c2) * ((const R*)E.h2[t])[idx];
+  const R qn = qv + R(E.dt) * acc;
+  ((R*)E.qout[t])[idx] = qn;
+  return qn;
 }
 
 // epilogue for one value with the LSRK residual prefetched in smem
@@ -397,8 +417,6 @@ __global__ void __launch_bounds__(NT) dense_kernel(hw_mesh_t M, hw_fields_t Q, E
 
   // flux at the face points
   const R pen = R(M.penalty_scale);
-  const bool sem = M.formulation == HW_SEM;
-  const R* ET = (const R*)TY.op[5];
   for (int i = tid; i < ne * NFP; i += NT) {
     const int e = i / NFP, j = i - e * NFP;
     int jj;
@@ -409,22 +427,10 @@ __global__ void __launch_bounds__(NT) dense_kernel(hw_mesh_t M, hw_fields_t Q, E
       const int node = __ldg(TY.iop[0] + j);
 #pragma unroll
       for (int c = 0; c < 4; ++c) own[c] = qe[c * NP + node];
-    } else {
-      R a0 = R(0), a1 = R(0), a2 = R(0), a3 = R(0);
-#pragma unroll 4
-      for (int m = 0; m < NP; ++m) {
-        const R ev = ldg(ET + m * NFP + j);
-        a0 += ev * qe[m];
-        a1 += ev * qe[NP + m];
-        a2 += ev * qe[2 * NP + m];
-        a3 += ev * qe[3 * NP + m];
-      }
-      own[0] = a0; own[1] = a1; own[2] = a2; own[3] = a3;
-      if (T == HW_WEDGE) {
-        const R isj = sg[e * X::GEO + 9];
+    } else {   // published traces of the input state
+      const R* te = sm + L::STR + e * 4 * NFP + j;
 #pragma unroll
-        for (int c = 0; c < 4; ++c) own[c] *= isj;
-      }
+      for (int c = 0; c < 4; ++c) own[c] = te[c * NFP];
     }
     const R um[3] = {own[1], own[2], own[3]};
     const R* g = sg + e * X::GEO + X::GF + FS * f;
@@ -435,8 +441,7 @@ __global__ void __launch_bounds__(NT) dense_kernel(hw_mesh_t M, hw_fields_t Q, E
       pp = -own[0]; up[0] = um[0]; up[1] = um[1]; up[2] = um[2];
     } else {
       R tr[4];
-      staged_trace<N, T, R>(M, Q, code, sne[e * NF + f], f, jj, sm + L::SST + e * L::STG, sem,
-                            tr);
+      staged_trace<N, T, R>(M, code, f, jj, sm + L::SST + e * L::STG, tr);
       pp = tr[0]; up[0] = tr[1]; up[1] = tr[2]; up[2] = tr[3];
     }
     R tp, tu, fp, fu;
@@ -473,12 +478,18 @@ __global__ void __launch_bounds__(NT) dense_kernel(hw_mesh_t M, hw_fields_t Q, E
     }
     const R kap = smat[e * 4 + 0], irho = smat[e * 4 + 1];
     const size_t base = (size_t)sk[e] * 4 * NP + n;
-    const R* qe = sq + e * 4 * NP + n;
+    R* qe = sq + e * 4 * NP + n;
     const R* re = sm + L::SRES + e * 4 * NP + n;
-    epilogue_s<R>(E, T, base, acc[s][0] * kap, qe[0], re[0]);
 #pragma unroll
-    for (int c = 1; c < 4; ++c)
-      epilogue_s<R>(E, T, base + c * NP, acc[s][c] * irho, qe[c * NP], re[c * NP]);
+    for (int c = 0; c < 4; ++c) {
+      const R v = acc[s][c] * (c == 0 ? kap : irho);
+      const R qn = epilogue_q<R>(E, T, base + c * NP, v, qe[c * NP], re[c * NP]);
+      if (T != HW_TET) qe[c * NP] = qn;    // new state, for the published traces
+    }
+  }
+  if (T != HW_TET && E.mode != MODE_RHS && M.tr_out[T] != nullptr) {
+    __syncthreads();
+    publish_traces<N, T, R>(M, sq, sg, sk, ne, (R*)M.tr_out[T]);
   }
 }
 
@@ -619,15 +630,10 @@ __global__ void __launch_bounds__(NT) hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi
       const int node = base + (end ? N : 0) * stride;
 #pragma unroll
       for (int c = 0; c < 4; ++c) own[c] = qe[c * NP + node];
-    } else {
+    } else {   // GL: published traces of the input state
+      const R* te = sm + L::STR + e * 4 * NFP + j;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) own[c] = R(0);
-#pragma unroll
-      for (int l = 0; l < N1; ++l) {
-        const R w = sve[end * N1 + l];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) own[c] += w * qe[c * NP + base + l * stride];
-      }
+      for (int c = 0; c < 4; ++c) own[c] = te[c * NFP];
     }
     // face geometry at (xi, eta) = (x[a], x[b]) from the 4 face vertices
     const int a = jj / N1, b = jj - a * N1;
@@ -669,8 +675,7 @@ __global__ void __launch_bounds__(NT) hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi
       pp = -own[0]; up[0] = um[0]; up[1] = um[1]; up[2] = um[2];
     } else {
       R tr[4];
-      staged_trace<N, HW_HEX, R>(M, Q, code, sne[e * 6 + f], f, jj, sm + L::SST + e * L::STG,
-                                 sem, tr);
+      staged_trace<N, HW_HEX, R>(M, code, f, jj, sm + L::SST + e * L::STG, tr);
       pp = tr[0]; up[0] = tr[1]; up[1] = tr[2]; up[2] = tr[3];
     }
     R tp, tu, fp, fu;
@@ -714,13 +719,47 @@ __global__ void __launch_bounds__(NT) hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi
     for (int c = 0; c < 4; ++c) acc[s][c] += lift[c] * minv[s];
     const R kap = smat[e * 4 + 0], irho = smat[e * 4 + 1];
     const size_t base = (size_t)sk[e] * 4 * NP + n;
-    const R* qe = sq + e * 4 * NP + n;
+    R* qe = sq + e * 4 * NP + n;
     const R* re = sm + L::SRES + e * 4 * NP + n;
-    epilogue_s<R>(E, HW_HEX, base, acc[s][0] * kap, qe[0], re[0]);
 #pragma unroll
-    for (int c = 1; c < 4; ++c)
-      epilogue_s<R>(E, HW_HEX, base + c * NP, acc[s][c] * irho, qe[c * NP], re[c * NP]);
+    for (int c = 0; c < 4; ++c) {
+      const R v = acc[s][c] * (c == 0 ? kap : irho);
+      qe[c * NP] = epilogue_q<R>(E, HW_HEX, base + c * NP, v, qe[c * NP], re[c * NP]);
+    }
   }
+  if (!sem && E.mode != MODE_RHS && M.tr_out[HW_HEX] != nullptr) {
+    __syncthreads();
+    publish_traces<N, HW_HEX, R>(M, sq, sg, sk, ne, (R*)M.tr_out[HW_HEX]);
+  }
+}
+
+// Face traces of q for a publishing type (hw_traces): EPB elements per block.
+template <int N, int T, typename R>
+__global__ void __launch_bounds__(NT) trace_kernel(hw_mesh_t M, hw_fields_t Q, hw_fields_t TR,
+                                                   const int32_t* __restrict__ list,
+                                                   int64_t nwork) {
+  using X = TT<N, T>;
+  constexpr int NP = X::NP;
+  constexpr int EPB = (NT / NP) > 0 ? (NT / NP) : 1;
+  __shared__ R sq[EPB * 4 * NP];
+  __shared__ R sg[EPB * X::GEO];
+  __shared__ int sk[EPB];
+  const int tid = threadIdx.x;
+  const int64_t w0 = (int64_t)blockIdx.x * EPB;
+  const int ne = (int)((nwork - w0) < EPB ? (nwork - w0) : EPB);
+  if (tid < ne) sk[tid] = list ? list[w0 + tid] : (int)(w0 + tid);
+  __syncthreads();
+  const R* q = (const R*)Q.p[T];
+  for (int i = tid; i < ne * 4 * NP; i += NT) {
+    const int e = i / (4 * NP), r = i - e * 4 * NP;
+    sq[i] = ldg(q + (size_t)sk[e] * 4 * NP + r);
+  }
+  for (int i = tid; i < ne * X::GEO; i += NT) {
+    const int e = i / X::GEO, r = i - e * X::GEO;
+    sg[i] = ldg((const R*)M.t[T].geo + (size_t)sk[e] * X::GEO + r);
+  }
+  __syncthreads();
+  publish_traces<N, T, R>(M, sq, sg, sk, ne, (R*)TR.p[T]);
 }
 
 }  // namespace hw

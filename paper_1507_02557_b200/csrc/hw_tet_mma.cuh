@@ -91,18 +91,19 @@ __global__ void __launch_bounds__(TetMma<N>::NTH, TetMma<N>::MINB)
   if (tid < EB) sk[tid] = tid < ne ? (list ? list[w0 + tid] : (int)(w0 + tid)) : 0;
   for (int i = tid; i < NFP; i += NTH) sfn[i] = __ldg(TY.iop[0] + i);
   // K padding must be zero for the DMMA (rows are never written by copies)
+  constexpr int PADN = (NPK > NP) ? NPK - NP : 1, PADF = (NFK > NFN) ? NFK - NFN : 1;
   if (NPK > NP)
-    for (int i = tid; i < EB * 11 * (NPK - NP); i += NTH) {
-      const int e = i / (11 * (NPK - NP)), r = i - e * 11 * (NPK - NP);
-      const int fld = r / (NPK - NP), n = NP + r - fld * (NPK - NP);
+    for (int i = tid; i < EB * 11 * PADN; i += NTH) {
+      const int e = i / (11 * PADN), r = i - e * 11 * PADN;
+      const int fld = r / PADN, n = NP + r - fld * PADN;
       if (fld < 4) sq[e * EQ + fld * NPK + n] = R(0);
       else if (fld < 8) sres[e * EQ + (fld - 4) * NPK + n] = R(0);
       else sv[e * EV + (fld - 8) * NPK + n] = R(0);
     }
   if (NFK > NFN)
-    for (int i = tid; i < EB * 8 * (NFK - NFN); i += NTH) {
-      const int e = i / (8 * (NFK - NFN)), r = i - e * 8 * (NFK - NFN);
-      const int fld = r / (NFK - NFN), n = NFN + r - fld * (NFK - NFN);
+    for (int i = tid; i < EB * 8 * PADF; i += NTH) {
+      const int e = i / (8 * PADF), r = i - e * 8 * PADF;
+      const int fld = r / PADF, n = NFN + r - fld * PADF;
       (fld < 4 ? sfp : sfu)[e * EF + (fld & 3) * NFK + n] = R(0);
     }
   __syncthreads();
@@ -155,11 +156,20 @@ __global__ void __launch_bounds__(TetMma<N>::NTH, TetMma<N>::MINB)
   for (int i = tid; i < ne * NFP; i += NTH) {
     const int e = i / NFP, j = i - e * NFP;
     const int g = sgi[i];
-    if (g < 0) continue;
+    if (g == -1) continue;
     const int f = j / NFN, jj = j - f * NFN;
     R* dst = sst + e * ESG + f * 4 * NFN + jj;
+    if (g >= 0) {
 #pragma unroll
-    for (int c = 0; c < 4; ++c) cp_async(dst + c * NFN, q + (size_t)g + c * NP);
+      for (int c = 0; c < 4; ++c) cp_async(dst + c * NFN, q + (size_t)g + c * NP);
+    } else {   // pyramid / wedge neighbour: its published face trace
+      const unsigned v = (unsigned)(-3 - g);
+      const int t2 = (v & 1u) ? HW_WEDGE : HW_PYRAMID;
+      const int nfp2 = (v & 1u) ? Dims<N>::NFP_WEDGE : Dims<N>::NFP_PYR;
+      const R* src = (const R*)M.tr_in[t2] + (size_t)(v >> 1);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) cp_async(dst + c * NFN, src + c * nfp2);
+    }
   }
   cp_async_commit();
 
@@ -211,17 +221,11 @@ __global__ void __launch_bounds__(TetMma<N>::NTH, TetMma<N>::MINB)
     const R nrm[3] = {g[0], g[1], g[2]};
     const int gi = sgi[i];
     R pp, up[3];
-    if (gi >= 0) {
+    if (gi != -1) {
       const R* s = sst + e * ESG + f * 4 * NFN + jj;
       pp = s[0]; up[0] = s[NFN]; up[1] = s[2 * NFN]; up[2] = s[3 * NFN];
-    } else if (gi == -1) {
-      pp = -pm; up[0] = um[0]; up[1] = um[1]; up[2] = um[2];
     } else {
-      const int k = sk[e];
-      const int code = __ldg(TY.nbr_code + (size_t)k * 4 + f);
-      R tr[4];
-      neighbour_trace<N, R>(M, Q, code, __ldg(TY.nbr_elem + (size_t)k * 4 + f), jj, true, tr);
-      pp = tr[0]; up[0] = tr[1]; up[1] = tr[2]; up[2] = tr[3];
+      pp = -pm; up[0] = um[0]; up[1] = um[1]; up[2] = um[2];
     }
     R tp, tu, fp, fu;
     penalties(g[4], g[5], pen, tp, tu);

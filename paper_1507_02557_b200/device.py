@@ -144,6 +144,9 @@ def pack_mesh(disc):
     mesh = disc.mesh
     pack = {"types": {}}
     dops_any = None
+    dops_all = {t: device_operators(t, disc.N, disc.formulation.kind, disc.ops[t])
+                for t in disc.types}
+    face_offsets = {t: (d["face_offsets"], int(d["face_offsets"][-1])) for t, d in dops_all.items()}
     for t in disc.types:
         form = disc.forms[t]
         if t in ("hex", "tet") and form != "strong":
@@ -152,7 +155,7 @@ def pack_mesh(disc):
             raise NotImplementedError("device wedge kernel implements the skew form only")
         verts = mesh.element_vertices(t)
         _affine_check(t, verts, disc.N)
-        dops = device_operators(t, disc.N, disc.formulation.kind, disc.ops[t])
+        dops = dops_all[t]
         dops_any = dops
         perm_tri = face_symmetry_perms("tri", dops["tri2d"])
         elem, code = neighbour_codes(mesh, t)
@@ -162,7 +165,10 @@ def pack_mesh(disc):
             "mat": material_records(np.asarray(mesh.materials[t], dtype=float)),
             "nbr_elem": elem, "nbr_code": code,
             "op": _pack_ops(t, dops),
-            "iop": _pack_iops(t, dops, disc.N, mesh, perm_tri)}
+            "iop": _pack_iops(t, dops, disc.N, mesh, perm_tri, face_offsets),
+            "nfp": int(dops["face_offsets"][-1]),
+            "publishes": t in ("wedge", "pyramid") or (t == "hex"
+                                                       and disc.formulation.kind == "GL")}
     pack["perm_tri"] = face_symmetry_perms("tri", dops_any["tri2d"])
     pack["perm_quad"] = face_symmetry_perms("quad", dops_any["quad2d"])
     return pack
@@ -193,34 +199,43 @@ def _pack_ops(t, d):
     raise ValueError(t)
 
 
-def tet_gather_index(mesh, dops, perm_tri):
-    """(K, 4, NFN) int32: for each tet face node in my face-point order, the
-    flat offset in q (element-major (K,4,Np), field 0) of the coincident
-    node of the neighbour tet; -1 on the boundary, -2 for a non-tet
-    neighbour (direct path in the kernel)."""
+def tet_gather_index(mesh, dops, perm_tri, face_offsets):
+    """(K, 4, NFN) int32: for each tet face node in my face-point order where
+    the neighbour's value comes from: >= 0 the flat offset in the tet state
+    (element-major (K,4,Np), field 0) of the coincident neighbour node; -1
+    on the boundary; <= -3 a published pyramid/wedge trace,
+    -3 - (2*offset + is_wedge) with offset into that type's trace buffer
+    (K2, 4, Nfp2), field 0."""
     nbr = mesh.nbr["tet"]
     code = mesh.face_code["tet"]
     K = len(nbr)
     Np = dops["Np"]
     nfn = len(dops["tri2d"])
     fn = dops["face_nodes"].reshape(4, nfn)
-    out = np.full((K, 4, nfn), -2, dtype=np.int64)
+    out = np.full((K, 4, nfn), -1, dtype=np.int64)
     for f in range(4):
-        bnd = nbr[:, f, 0] < 0
-        out[bnd, f, :] = -1
-        sel = nbr[:, f, 0] == 3
-        k2, f2, pc = nbr[sel, f, 1], nbr[sel, f, 2], code[sel, f]
-        out[sel, f, :] = k2[:, None] * 4 * Np + fn[f2[:, None], perm_tri[pc]]
-    if out.max(initial=0) >= 2 ** 31:
+        for tid, name in ((3, "tet"), (1, "wedge"), (2, "pyramid")):
+            sel = nbr[:, f, 0] == tid
+            if not sel.any():
+                continue
+            k2, f2, pc = nbr[sel, f, 1], nbr[sel, f, 2], code[sel, f]
+            p = perm_tri[pc]
+            if name == "tet":
+                out[sel, f, :] = k2[:, None] * 4 * Np + fn[f2[:, None], p]
+            else:
+                offs, nfp2 = face_offsets[name]
+                off = k2[:, None] * 4 * nfp2 + offs[f2][:, None] + p
+                out[sel, f, :] = -3 - (2 * off + (1 if name == "wedge" else 0))
+    if np.abs(out).max(initial=0) >= 2 ** 31:
         raise ValueError("tet gather offsets exceed int32")
     return out.astype(np.int32)
 
 
-def _pack_iops(t, d, N, mesh=None, perm_tri=None):
+def _pack_iops(t, d, N, mesh=None, perm_tri=None, face_offsets=None):
     if t == "hex":
         return {0: d["face_tab"], 1: hex_node_face_points(d, N)}
     if t == "tet":
-        return {0: d["face_nodes"], 1: tet_gather_index(mesh, d, perm_tri)}
+        return {0: d["face_nodes"], 1: tet_gather_index(mesh, d, perm_tri, face_offsets)}
     return {}
 
 
@@ -255,10 +270,31 @@ class DeviceMesh:
                 T.iop[slot] = self._put(arr, torch.int32)
         S.perm_tri = self._put(pack["perm_tri"], torch.int32)
         S.perm_quad = self._put(pack["perm_quad"], torch.int32)
+        # face-trace buffers (ping-pong) of the publishing types
+        self.traces = [[None] * 4, [None] * 4]
+        for t, P in pack["types"].items():
+            if P["publishes"]:
+                for b in range(2):
+                    self.traces[b][TYPE_ID[t]] = torch.zeros((P["K"], 4, P["nfp"]),
+                                                             dtype=dtype, device=self.device)
         self.struct = S
+        self.set_traces(0, None)
         orders = nat.lib().hw_supported_orders()
         if not (orders >> disc.N) & 1:
             raise ValueError(f"order N={disc.N} not compiled into {nat.LIB_NAME}")
+
+    def set_traces(self, tin, tout):
+        """Point the struct's tr_in / tr_out at trace buffer sets (0/1/None)."""
+        for i in range(4):
+            a = self.traces[tin][i] if tin is not None else None
+            b = self.traces[tout][i] if tout is not None else None
+            self.struct.tr_in[i] = a.data_ptr() if a is not None else None
+            self.struct.tr_out[i] = b.data_ptr() if b is not None else None
+
+    def compute_traces(self, q_fields, buf, stream):
+        """hw_traces: face traces of q (HWFields) into trace set `buf`."""
+        nat.check(nat.lib().hw_traces(self.struct, q_fields, nat.fields(self.traces[buf]), None,
+                                      stream))
 
     def _put(self, arr, dtype=None):
         t = torch.as_tensor(np.ascontiguousarray(arr), dtype=dtype or self.dtype).to(self.device)

@@ -157,6 +157,7 @@ class Discretization:
     def rhs_device(self, q, out=None, subset=None):
         """Device RHS: q, out dicts of CUDA tensors (no host copies)."""
         dm = self.device_mesh
+        dm.set_traces(0, None)        # hw_rhs fills trace set 0 with q's traces
         out = out if out is not None else self.empty_state()
         sub = nat.subset(subset) if subset is not None else None
         nat.check(nat.lib().hw_rhs(dm.struct, nat.fields(self.slots(q)),

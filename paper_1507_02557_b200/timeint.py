@@ -87,6 +87,13 @@ class Stepper:
             self.hist = [disc.zeros_state() for _ in range(3)]
             self.n_steps = 0
         self.launches_per_stage = len(disc.types)
+        # traces of the initial state; stages then ping-pong the trace sets
+        self.tr = 0
+        self.dm.compute_traces(self._f(self.q), 0, disc.stream_ptr())
+
+    def _stage_traces(self):
+        self.dm.set_traces(self.tr, 1 - self.tr)
+        self.tr = 1 - self.tr
 
     def _f(self, s):
         return nat.fields(self.disc.slots(s))
@@ -95,6 +102,7 @@ class Stepper:
         L = nat.lib()
         st = self.disc.stream_ptr()
         for a, b in zip(LSRK_A, LSRK_B):
+            self._stage_traces()
             nat.check(L.hw_lsrk_stage(self.dm.struct, self._f(self.q), self._f(self.q2),
                                       self._f(self.res), a, b, h, None, st))
             self.q, self.q2 = self.q2, self.q
@@ -104,6 +112,7 @@ class Stepper:
         c = ab_coefficients(nh, theta)
         c = list(c) + [0.0] * (3 - len(c))
         new = self.hist[2]
+        self._stage_traces()
         nat.check(nat.lib().hw_ab_step(self.dm.struct, self._f(self.q), self._f(self.q2),
                                        self._f(new), self._f(self.hist[0]),
                                        self._f(self.hist[1]), nh, c[0], c[1], c[2], dt, None,
@@ -136,7 +145,11 @@ def lsrk_step(disc, q, res, dt, q_tmp=None):
     dm = disc.device_mesh
     q_tmp = q_tmp if q_tmp is not None else disc.empty_state()
     st = disc.stream_ptr()
+    dm.compute_traces(nat.fields(disc.slots(q)), 0, st)
+    tr = 0
     for a, b in zip(LSRK_A, LSRK_B):
+        dm.set_traces(tr, 1 - tr)
+        tr = 1 - tr
         nat.check(nat.lib().hw_lsrk_stage(dm.struct, nat.fields(disc.slots(q)),
                                           nat.fields(disc.slots(q_tmp)),
                                           nat.fields(disc.slots(res)), a, b, dt, None, st))
@@ -229,7 +242,10 @@ class MRABDriver:
                     nat.check(lib.hw_axpy3(dm.struct, F(q), F(eff), F(h[0]), F(h[1]), F(h[2]),
                                            nh, c[0], c[1], c[2], dt_min * period,
                                            sub_structs[lev], st))
-                # fused RHS + AB update of each stepping level
+                # traces of the effective state, then the fused RHS + AB update
+                # of each stepping level (no trace publishing)
+                dm.compute_traces(F(eff), 0, st)
+                dm.set_traces(0, None)
                 for lev in stepping:
                     n_hist[lev] = min(n_hist[lev] + 1, 3)
                     steps[lev] += 1
