@@ -6,8 +6,14 @@ import sys
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _ROOT = os.path.dirname(_HERE)
-SOURCES = [os.path.join(_HERE, "csrc", f) for f in
-           ("hw_abi.cu", "hw_kernels.cuh", "hw_common.cuh")]
+MAIN = os.path.join(_HERE, "csrc", "hw_abi.cu")
+
+
+def _sources():
+    d = os.path.join(_HERE, "csrc")
+    return sorted(os.path.join(d, f) for f in os.listdir(d) if f.endswith((".cu", ".cuh")))
+
+
 HEADER = os.path.join(_ROOT, "include", "hybridwave_b200.h")
 OUT = os.path.join(_HERE, "libhybridwave_b200.so")
 
@@ -23,12 +29,12 @@ def nvcc():
 
 
 def build_native(max_order=7, force=False, verbose=False):
-    deps = SOURCES + [HEADER]
+    deps = _sources() + [HEADER]
     if (not force and os.path.exists(OUT)
             and os.path.getmtime(OUT) >= max(os.path.getmtime(p) for p in deps)):
         return OUT
     cmd = [nvcc()] + NVCC_FLAGS + [f"-DHW_MAX_ORDER={max_order}", "-o", OUT + ".tmp",
-                                   SOURCES[0]]
+                                   MAIN]
     proc = subprocess.run(cmd, capture_output=True, text=True)
     log = os.path.join(_HERE, "csrc", "build.log")
     with open(log, "w") as fh:

@@ -8,6 +8,7 @@
 
 #include "hw_kernels.cuh"
 #include "hw_tet_mma.cuh"
+#include "hw_dense_mma.cuh"
 
 namespace hw {
 
@@ -47,8 +48,8 @@ static int set_smem(KernelT kernel, size_t bytes) {
   return 0;
 }
 
-// HW_TET_KERNEL=scalar selects the scalar dense_kernel for fp64 tets (A/B
-// checks); default: the DMMA kernel
+// HW_TET_KERNEL=scalar selects the scalar dense_kernel for the fp64 dense
+// types (tet, wedge, pyramid) for A/B checks; default: the DMMA kernels
 static bool tet_scalar() {
   static int v = -1;
   if (v < 0) {
@@ -77,6 +78,19 @@ static int launch_dense(const hw_mesh_t& M, const hw_fields_t& Q, const Epi& E,
   dense_kernel<N, T, R><<<(unsigned)((n + L::EPB - 1) / L::EPB), NT, L::BYTES, st>>>(M, Q, E,
                                                                                     list, n);
   return check_launch("dense_kernel");
+}
+
+template <int N, int T>
+static int launch_dense_mma(const hw_mesh_t& M, const hw_fields_t& Q, const Epi& E,
+                            const int32_t* list, int64_t n, cudaStream_t st) {
+  using L = DMma<N, T>;
+  if (L::BYTES > 220 * 1024)   // high orders: the scalar kernel fits, the DMMA one does not
+    return launch_dense<N, T, double>(M, Q, E, list, n, st);
+  int rc;
+  if ((rc = set_smem(dense_mma_kernel<N, T>, L::BYTES))) return rc;
+  dense_mma_kernel<N, T><<<(unsigned)((n + L::E - 1) / L::E), L::NTH, L::BYTES, st>>>(M, Q, E,
+                                                                                   list, n);
+  return check_launch("dense_mma_kernel");
 }
 
 template <int N, int T, typename R>
@@ -131,8 +145,15 @@ static int launch_rhs_all(const hw_mesh_t& M, const hw_fields_t& Q, const Epi& E
         rc = check_launch("hex_kernel");
         break;
       }
-      case HW_WEDGE: rc = launch_dense<N, HW_WEDGE, R>(M, Q, E, list, n, st); break;
-      case HW_PYRAMID: rc = launch_dense<N, HW_PYRAMID, R>(M, Q, E, list, n, st); break;
+      case HW_WEDGE:
+        rc = (sizeof(R) == 8 && !tet_scalar()) ? launch_dense_mma<N, HW_WEDGE>(M, Q, E, list, n, st)
+                                               : launch_dense<N, HW_WEDGE, R>(M, Q, E, list, n, st);
+        break;
+      case HW_PYRAMID:
+        rc = (sizeof(R) == 8 && !tet_scalar())
+                 ? launch_dense_mma<N, HW_PYRAMID>(M, Q, E, list, n, st)
+                 : launch_dense<N, HW_PYRAMID, R>(M, Q, E, list, n, st);
+        break;
       case HW_TET:
         if (sizeof(R) == 8 && !tet_scalar()) {
           using L = TetMma<N>;

@@ -1,0 +1,346 @@
+// Wedge / pyramid RHS + update with the dense contractions on the fp64
+// tensor cores (mma.sync.m8n8k4.f64), fp64 only.  Same organisation as
+// tet_mma_kernel; in addition these types publish the face traces of their
+// new state (trace buffer, see hw_kernels.cuh) with a third GEMM
+//   TR = E q_out    (face points x (element, field)),
+// and read their own traces of the input state from the trace buffer.
+//   volume  DP_c = A_c p;  DIV = sum_c A_c v_c (strong) | sum_c A_c^T v_c (skew)
+//   lift    P += LIFT_f fp_f,  TU_f = LIFT_f fu_f,  U_x += n_f,x TU_f
+// A_c = D_c (pyramid), S_c = V^T W D3_c (affine wedge); reference
+// arithmetic hybridwave/dg.py:423-463, 326-354, 479-490.
+#pragma once
+#include "hw_tet_mma.cuh"
+
+namespace hw {
+
+template <int N, int T>
+struct DMma {
+  using X = TT<N, T>;
+  using D = Dims<N>;
+  static constexpr int NP = X::NP, NF = X::NF, NFP = X::NFP, GEO = X::GEO, GF = X::GF;
+  static constexpr int E = 8;
+  static constexpr int RT = (NP + 7) / 8;
+  static constexpr int RT8 = RT * 8;
+  static constexpr int NPK = ((NP + 3) / 4) * 4;
+  static constexpr int W = RT;
+  static constexpr int NTH = 32 * W;
+  __host__ __device__ static constexpr int kf(int f) { return ((X::cnt(f) + 3) / 4) * 4; }
+  __host__ __device__ static constexpr int koff(int f) {
+    int s = 0;
+    for (int g = 0; g < f; ++g) s += kf(g);
+    return s;
+  }
+  static constexpr int NFKT = koff(NF);                 // padded, face-concatenated K of the lift
+  static constexpr int RTF = (NFP + 7) / 8;             // row tiles of the trace GEMM
+  static constexpr int EQ = stride4mod16(4 * NPK);
+  static constexpr int EV = stride4mod16(3 * NPK);
+  static constexpr int EF = stride4mod16(NFKT);
+  static constexpr int STG = stage_off<N, T>(NF);
+  static constexpr int ESG = STG + 1;
+  static constexpr int ETR = 4 * NFP + 1;
+  // storage shared by phase-disjoint buffers: v_c (volume) with fp/fu
+  // (flux, lift); own + neighbour traces (flux) with the residual (epilogue)
+  static constexpr int RA = cmax(EV, 2 * EF), RB = cmax(ETR + ESG, EQ);
+  static constexpr int SQ = 0, SV = SQ + E * EQ, SFP = SV, SFU = SFP + E * EF,
+                       STR = SV + E * RA, SST = STR + E * ETR, SRES = STR,
+                       SG = STR + E * RB, SMAT = SG + E * GEO, TOTAL = SMAT + E * 4;
+  static constexpr size_t BYTES = sizeof(double) * TOTAL + sizeof(int) * (E + 2 * E * NF);
+  static constexpr bool VEC = (NP % 2 == 0) && (NPK == NP);
+};
+
+template <int N, int T>
+__global__ void __launch_bounds__(DMma<N, T>::NTH)
+    dense_mma_kernel(hw_mesh_t M, hw_fields_t Q, Epi E, const int32_t* __restrict__ list,
+                     int64_t nwork) {
+  using L = DMma<N, T>;
+  using X = TT<N, T>;
+  using R = double;
+  constexpr int NP = L::NP, NF = L::NF, NFP = L::NFP, EB = L::E, NPK = L::NPK, NTH = L::NTH,
+                EQ = L::EQ, EV = L::EV, EF = L::EF, ESG = L::ESG, ETR = L::ETR, GEO = L::GEO,
+                GF = L::GF;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  R* sm = reinterpret_cast<R*>(smem_raw);
+  int* sk = reinterpret_cast<int*>(sm + L::TOTAL);
+  int* snc = sk + EB;
+  int* sne = snc + EB * NF;
+  R* sq = sm + L::SQ;
+  R* sres = sm + L::SRES;
+  R* sv = sm + L::SV;
+  R* sfp = sm + L::SFP;
+  R* sfu = sm + L::SFU;
+  R* str = sm + L::STR;
+  R* sst = sm + L::SST;
+  R* sg = sm + L::SG;
+  R* smat = sm + L::SMAT;
+
+  const hw_type_t& TY = M.t[T];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t w0 = (int64_t)blockIdx.x * EB;
+  const int ne = (int)((nwork - w0) < EB ? (nwork - w0) : EB);
+  const bool lsrk = E.mode == MODE_LSRK;
+  const bool skew = TY.form == HW_FORM_SKEW;
+
+  if (tid < EB) sk[tid] = tid < ne ? (list ? list[w0 + tid] : (int)(w0 + tid)) : 0;
+  // zero K paddings (node rows NP..NPK and the per-face lift padding)
+  constexpr int PADN = (NPK > NP) ? NPK - NP : 1;
+  if (NPK > NP)
+    for (int i = tid; i < EB * 11 * PADN; i += NTH) {
+      const int e = i / (11 * PADN), r = i - e * 11 * PADN;
+      const int fld = r / PADN, n = NP + r - fld * PADN;
+      if (fld < 4) sq[e * EQ + fld * NPK + n] = R(0);
+      else if (fld >= 8) sv[e * EV + (fld - 8) * NPK + n] = R(0);
+    }
+  __syncthreads();
+
+  // ---- P0: rows, records, links (all async), then neighbour staging
+  const R* q = (const R*)Q.p[T];
+  const R* resg = (const R*)E.res[T];
+  if (L::VEC) {
+    constexpr int CH = 4 * NP / 2;
+    for (int i = tid; i < ne * CH; i += NTH) {
+      const int e = i / CH, c = i - e * CH;
+      cp_async16(sq + e * EQ + 2 * c, q + (size_t)sk[e] * 4 * NP + 2 * c);
+    }
+  } else {
+    for (int i = tid; i < ne * 4 * NP; i += NTH) {
+      const int e = i / (4 * NP), r = i - e * 4 * NP;
+      const int fld = r / NP, n = r - fld * NP;
+      cp_async(sq + e * EQ + fld * NPK + n, q + (size_t)sk[e] * 4 * NP + r);
+    }
+  }
+  {
+    const R* tr = (const R*)M.tr_in[T];
+    for (int i = tid; i < ne * 4 * NFP; i += NTH) {
+      const int e = i / (4 * NFP), r = i - e * 4 * NFP;
+      cp_async(str + e * ETR + r, tr + (size_t)sk[e] * 4 * NFP + r);
+    }
+  }
+  for (int i = tid; i < ne * GEO; i += NTH) {
+    const int e = i / GEO, r = i - e * GEO;
+    cp_async(sg + i, (const R*)TY.geo + (size_t)sk[e] * GEO + r);
+  }
+  for (int i = tid; i < ne * 4; i += NTH)
+    cp_async(smat + i, (const R*)TY.mat + (size_t)sk[i >> 2] * 4 + (i & 3));
+  for (int i = tid; i < ne * NF; i += NTH) {
+    const int e = i / NF, f = i - e * NF;
+    snc[i] = __ldg(TY.nbr_code + (size_t)sk[e] * NF + f);
+    sne[i] = __ldg(TY.nbr_elem + (size_t)sk[e] * NF + f);
+  }
+  cp_async_commit();
+  __syncthreads();
+  {
+    // stage_neighbours uses NT/32 warps; emulate with this block's warps
+    using Dm = Dims<N>;
+    const bool sem = M.formulation == HW_SEM;
+    for (int pr = warp; pr < ne * NF; pr += L::W) {
+      const int e = pr / NF, f = pr - e * NF;
+      const int code = snc[pr];
+      if (code & HW_NBR_BOUNDARY) continue;
+      const int t2 = HW_NBR_TYPE(code), f2 = HW_NBR_FACE(code);
+      const int k2 = sne[pr];
+      const int cnt = X::cnt(f);
+      R* dst = sst + e * ESG + stage_off<N, T>(f);
+      if (publishes(t2, sem)) {
+        const int nfp2 = nfp_of<N>(t2);
+        const R* src = (const R*)M.tr_in[t2] + (size_t)k2 * 4 * nfp2 + face_offset<N>(t2, f2);
+        for (int i = lane; i < 4 * cnt; i += 32) {
+          const int c = i / cnt, p = i - c * cnt;
+          cp_async(dst + i, src + c * nfp2 + p);
+        }
+      } else if (t2 == HW_TET) {
+        const R* q2 = (const R*)Q.p[HW_TET] + (size_t)k2 * 4 * Dm::NP_TET;
+        const int* fn = M.t[HW_TET].iop[0] + f2 * Dm::NFN;
+        for (int i = lane; i < 4 * Dm::NFN; i += 32) {
+          const int c = i / Dm::NFN, n = i - c * Dm::NFN;
+          cp_async(dst + i, q2 + c * Dm::NP_TET + __ldg(fn + n));
+        }
+      } else {
+        const R* q2 = (const R*)Q.p[HW_HEX] + (size_t)k2 * 4 * Dm::NP_HEX;
+        const int* tab = M.t[HW_HEX].iop[0] + 3 * f2 * Dm::NFQ;
+        for (int i = lane; i < 4 * Dm::NFQ; i += 32) {
+          const int c = i / Dm::NFQ, p = i - c * Dm::NFQ;
+          const int base = __ldg(tab + 3 * p), stride = __ldg(tab + 3 * p + 1),
+                    end = __ldg(tab + 3 * p + 2);
+          cp_async(dst + i, q2 + c * Dm::NP_HEX + base + (end ? N : 0) * stride);
+        }
+      }
+    }
+    cp_async_commit();
+  }
+  asm volatile("cp.async.wait_group 1;\n" ::: "memory");   // rows, records, own traces
+  __syncthreads();
+
+  // v_c = sum_x G[c][x] u_x
+  for (int i = tid; i < ne * NP; i += NTH) {
+    const int e = i / NP, n = i - e * NP;
+    const R* G = sg + e * GEO;
+    const R* u = sq + e * EQ + n;
+    const R u0 = u[NPK], u1 = u[2 * NPK], u2 = u[3 * NPK];
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+      sv[e * EV + c * NPK + n] = G[c * 3] * u0 + G[c * 3 + 1] * u1 + G[c * 3 + 2] * u2;
+  }
+  __syncthreads();
+
+  // ---- volume GEMMs
+  const int rt = warp;
+  const int arow = rt * 8 + (lane >> 2), acol = lane & 3;
+  const int bk = lane & 3, bcol = lane >> 2;
+  R dp[3][2] = {{0, 0}, {0, 0}, {0, 0}}, dv[2] = {0, 0};
+  {
+    const R* A = (const R*)TY.op[2];    // [3][RT8][NPK]  A_c
+    const R* AT = (const R*)TY.op[3];   // [3][RT8][NPK]  A_c^T
+    const R* bq = sq + bcol * EQ + bk;
+    const R* bv = sv + bcol * EV + bk;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+#pragma unroll 5
+      for (int ks = 0; ks < NPK / 4; ++ks) {
+        const size_t ai = ((size_t)c * L::RT8 + arow) * NPK + ks * 4 + acol;
+        const R a = ldg(A + ai);
+        dmma884(dp[c][0], dp[c][1], a, bq[ks * 4]);
+        dmma884(dv[0], dv[1], skew ? ldg(AT + ai) : a, bv[c * NPK + ks * 4]);
+      }
+    }
+  }
+
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  __syncthreads();
+
+  // ---- flux at the face points (face point fastest across threads)
+  for (int i = tid; i < EB * L::NFKT; i += NTH) {   // lift K padding (storage held v_c)
+    const int e = i / L::NFKT, k = i - e * L::NFKT;
+    sfp[e * EF + k] = R(0);
+    sfu[e * EF + k] = R(0);
+  }
+  __syncthreads();
+  const R pen = R(M.penalty_scale);
+  for (int i = tid; i < ne * NFP; i += NTH) {
+    const int e = i / NFP, j = i - e * NFP;
+    int jj;
+    const int f = face_of_point<N, T>(j, jj);
+    const R* te = str + e * ETR + j;
+    const R own[4] = {te[0], te[NFP], te[2 * NFP], te[3 * NFP]};
+    const R um[3] = {own[1], own[2], own[3]};
+    const R* g = sg + e * GEO + GF + FS * f;
+    const R nrm[3] = {g[0], g[1], g[2]};
+    const int code = snc[e * NF + f];
+    R pp, up[3];
+    if (code & HW_NBR_BOUNDARY) {
+      pp = -own[0]; up[0] = um[0]; up[1] = um[1]; up[2] = um[2];
+    } else {
+      R tr[4];
+      staged_trace<N, T, R>(M, code, f, jj, sst + e * ESG, tr);
+      pp = tr[0]; up[0] = tr[1]; up[1] = tr[2]; up[2] = tr[3];
+    }
+    R tp, tu, fp, fu;
+    penalties(g[4], g[5], pen, tp, tu);
+    upwind_flux(own[0], um, pp, up, nrm, tp, tu, skew, fp, fu);
+    sfp[e * EF + L::koff(f) + jj] = fp * g[3];
+    sfu[e * EF + L::koff(f) + jj] = fu * g[3];
+  }
+  __syncthreads();
+  // residual rows into the (now free) trace storage, behind the lift GEMM
+  if (lsrk) {
+    if (L::VEC) {
+      constexpr int CH = 4 * NP / 2;
+      for (int i = tid; i < ne * CH; i += NTH) {
+        const int e = i / CH, c = i - e * CH;
+        cp_async16(sres + e * EQ + 2 * c, resg + (size_t)sk[e] * 4 * NP + 2 * c);
+      }
+    } else {
+      for (int i = tid; i < ne * 4 * NP; i += NTH) {
+        const int e = i / (4 * NP), r = i - e * 4 * NP;
+        const int fld = r / NP, n = r - fld * NP;
+        cp_async(sres + e * EQ + fld * NPK + n, resg + (size_t)sk[e] * 4 * NP + r);
+      }
+    }
+    cp_async_commit();
+  }
+
+  // ---- lift GEMMs, combine, epilogue
+  const int col0 = (lane & 3) * 2;
+  R accp[2] = {skew ? dv[0] : -dv[0], skew ? dv[1] : -dv[1]};
+  R accu[3][2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const R* G = sg + (col0 + i) * GEO;
+#pragma unroll
+    for (int x = 0; x < 3; ++x)
+      accu[x][i] = -(G[x] * dp[0][i] + G[3 + x] * dp[1][i] + G[6 + x] * dp[2][i]);
+  }
+  {
+    const R* LF = (const R*)TY.op[4];   // [RT8][NFKT]
+    const R* bp = sfp + bcol * EF + bk;
+    const R* bu = sfu + bcol * EF + bk;
+#pragma unroll
+    for (int f = 0; f < NF; ++f) {
+      R tu[2] = {0, 0};
+#pragma unroll
+      for (int ks = 0; ks < L::kf(f) / 4; ++ks) {
+        const int k = L::koff(f) + ks * 4;
+        const R a = ldg(LF + (size_t)arow * L::NFKT + k + acol);
+        dmma884(accp[0], accp[1], a, bp[k]);
+        dmma884(tu[0], tu[1], a, bu[k]);
+      }
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const R* g = sg + (col0 + i) * GEO + GF + FS * f;
+        accu[0][i] += g[0] * tu[i];
+        accu[1][i] += g[1] * tu[i];
+        accu[2][i] += g[2] * tu[i];
+      }
+    }
+  }
+  if (lsrk) {
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    __syncthreads();
+  }
+  const int n = rt * 8 + (lane >> 2);
+  if (n < NP) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int e = col0 + i;
+      if (e >= ne) continue;
+      const R kap = smat[e * 4 + 0], irho = smat[e * 4 + 1];
+      const size_t base = (size_t)sk[e] * 4 * NP + n;
+      R* qe = sq + e * EQ + n;
+      const R* re = sres + e * EQ + n;
+      qe[0] = epilogue_q<R>(E, T, base, accp[i] * kap, qe[0], re[0]);
+#pragma unroll
+      for (int x = 0; x < 3; ++x)
+        qe[(1 + x) * NPK] = epilogue_q<R>(E, T, base + (1 + x) * NP, accu[x][i] * irho,
+                                          qe[(1 + x) * NPK], re[(1 + x) * NPK]);
+    }
+  }
+
+  // ---- publish the traces of the new state: TR = E q_out
+  if (E.mode != MODE_RHS && M.tr_out[T] != nullptr) {
+    __syncthreads();
+    const R* Ep = (const R*)TY.op[7];   // [RTF*8][NPK]
+    R* tro = (R*)M.tr_out[T];
+    // columns: (element, field) pairs, col = e*4 + c; 4 column tiles for E = 8
+    for (int tile = warp; tile < L::RTF * 4; tile += L::W) {
+      const int rf = tile >> 2, cf = tile & 3;
+      const int col = cf * 8 + (lane >> 2);
+      const R* bsrc = sq + (col >> 2) * EQ + (col & 3) * NPK + bk;
+      const int er = rf * 8 + (lane >> 2);
+      R y[2] = {0, 0};
+#pragma unroll 5
+      for (int ks = 0; ks < NPK / 4; ++ks)
+        dmma884(y[0], y[1], ldg(Ep + (size_t)er * NPK + ks * 4 + acol), bsrc[ks * 4]);
+      const int j = er;
+      const int c0 = cf * 8 + (lane & 3) * 2;          // output columns c0, c0+1
+      const int e = c0 >> 2;
+      if (j < NFP && e < ne) {
+        R s = R(1);
+        if (T == HW_WEDGE) s = sg[e * GEO + 9];
+        R* o = tro + (size_t)sk[e] * 4 * NFP + j;
+        o[(c0 & 3) * NFP] = y[0] * s;
+        o[((c0 & 3) + 1) * NFP] = y[1] * s;
+      }
+    }
+  }
+}
+
+}  // namespace hw

@@ -52,8 +52,11 @@ struct TetMma {
   static constexpr int EV = stride4mod16(3 * NPK);          // v_c
   static constexpr int EF = stride4mod16(4 * NFK);          // fp / fu
   static constexpr int ESG = 16 * NFN + 1;                  // staged neighbour values
-  static constexpr int SQ = 0, SRES = SQ + E * EQ, SV = SRES + E * EQ, SFP = SV + E * EV,
-                       SFU = SFP + E * EF, SST = SFU + E * EF, SG = SST + E * ESG,
+  // buffers live in disjoint phases share storage: v_c (volume) with fp/fu
+  // (flux, lift); the neighbour staging (flux) with the residual (epilogue)
+  static constexpr int RA = cmax(EV, 2 * EF), RB = stride4mod16(cmax(16 * NFN, EQ));
+  static constexpr int SQ = 0, SV = SQ + E * EQ, SFP = SV, SFU = SFP + E * EF,
+                       SST = SV + E * RA, SRES = SST, SG = SST + E * RB,
                        SMAT = SG + E * GEO_TET, TOTAL = SMAT + E * 4;
   static constexpr size_t BYTES = sizeof(double) * TOTAL + sizeof(int) * (E + E * NFP + NFP);
   static constexpr int MINB = (W <= 8) ? 3 : 1;
@@ -97,14 +100,7 @@ __global__ void __launch_bounds__(TetMma<N>::NTH, TetMma<N>::MINB)
       const int e = i / (11 * PADN), r = i - e * 11 * PADN;
       const int fld = r / PADN, n = NP + r - fld * PADN;
       if (fld < 4) sq[e * EQ + fld * NPK + n] = R(0);
-      else if (fld < 8) sres[e * EQ + (fld - 4) * NPK + n] = R(0);
-      else sv[e * EV + (fld - 8) * NPK + n] = R(0);
-    }
-  if (NFK > NFN)
-    for (int i = tid; i < EB * 8 * PADF; i += NTH) {
-      const int e = i / (8 * PADF), r = i - e * 8 * PADF;
-      const int fld = r / PADF, n = NFN + r - fld * PADF;
-      (fld < 4 ? sfp : sfu)[e * EF + (fld & 3) * NFK + n] = R(0);
+      else if (fld >= 8) sv[e * EV + (fld - 8) * NPK + n] = R(0);
     }
   __syncthreads();
 
@@ -116,14 +112,12 @@ __global__ void __launch_bounds__(TetMma<N>::NTH, TetMma<N>::MINB)
     for (int i = tid; i < ne * CH; i += NTH) {
       const int e = i / CH, c = i - e * CH;
       cp_async16(sq + e * EQ + 2 * c, q + (size_t)sk[e] * 4 * NP + 2 * c);
-      if (lsrk) cp_async16(sres + e * EQ + 2 * c, resg + (size_t)sk[e] * 4 * NP + 2 * c);
     }
   } else {
     for (int i = tid; i < ne * 4 * NP; i += NTH) {
       const int e = i / (4 * NP), r = i - e * 4 * NP;
       const int fld = r / NP, n = r - fld * NP;
       cp_async(sq + e * EQ + fld * NPK + n, q + (size_t)sk[e] * 4 * NP + r);
-      if (lsrk) cp_async(sres + e * EQ + fld * NPK + n, resg + (size_t)sk[e] * 4 * NP + r);
     }
   }
   for (int i = tid; i < ne * GEO_TET; i += NTH) {
@@ -158,7 +152,7 @@ __global__ void __launch_bounds__(TetMma<N>::NTH, TetMma<N>::MINB)
     const int g = sgi[i];
     if (g == -1) continue;
     const int f = j / NFN, jj = j - f * NFN;
-    R* dst = sst + e * ESG + f * 4 * NFN + jj;
+    R* dst = sst + e * L::RB + f * 4 * NFN + jj;
     if (g >= 0) {
 #pragma unroll
       for (int c = 0; c < 4; ++c) cp_async(dst + c * NFN, q + (size_t)g + c * NP);
@@ -209,6 +203,12 @@ __global__ void __launch_bounds__(TetMma<N>::NTH, TetMma<N>::MINB)
   __syncthreads();
 
   // ---- P3: flux at the face nodes (face point fastest across threads)
+  if (NFK > NFN)      // K padding of fp/fu (their storage held v_c until now)
+    for (int i = tid; i < EB * 8 * PADF; i += NTH) {
+      const int e = i / (8 * PADF), r = i - e * 8 * PADF;
+      const int fld = r / PADF, n = NFN + r - fld * PADF;
+      (fld < 4 ? sfp : sfu)[e * EF + (fld & 3) * NFK + n] = R(0);
+    }
   const R pen = R(M.penalty_scale);
   for (int i = tid; i < ne * NFP; i += NTH) {
     const int e = i / NFP, j = i - e * NFP;
@@ -222,7 +222,7 @@ __global__ void __launch_bounds__(TetMma<N>::NTH, TetMma<N>::MINB)
     const int gi = sgi[i];
     R pp, up[3];
     if (gi != -1) {
-      const R* s = sst + e * ESG + f * 4 * NFN + jj;
+      const R* s = sst + e * L::RB + f * 4 * NFN + jj;
       pp = s[0]; up[0] = s[NFN]; up[1] = s[2 * NFN]; up[2] = s[3 * NFN];
     } else {
       pp = -pm; up[0] = um[0]; up[1] = um[1]; up[2] = um[2];
@@ -234,6 +234,23 @@ __global__ void __launch_bounds__(TetMma<N>::NTH, TetMma<N>::MINB)
     sfu[e * EF + f * NFK + jj] = fu * g[3];
   }
   __syncthreads();
+  // residual rows into the (now free) staging storage, behind the lift GEMM
+  if (lsrk) {
+    if (L::VEC) {
+      constexpr int CH = 4 * NP / 2;
+      for (int i = tid; i < ne * CH; i += NTH) {
+        const int e = i / CH, c = i - e * CH;
+        cp_async16(sres + e * L::RB + 2 * c, resg + (size_t)sk[e] * 4 * NP + 2 * c);
+      }
+    } else {
+      for (int i = tid; i < ne * 4 * NP; i += NTH) {
+        const int e = i / (4 * NP), r = i - e * 4 * NP;
+        const int fld = r / NP, n = r - fld * NP;
+        cp_async(sres + e * L::RB + fld * NPK + n, resg + (size_t)sk[e] * 4 * NP + r);
+      }
+    }
+    cp_async_commit();
+  }
 
   // ---- P4: lift on DMMA, combine, epilogue
   const int col0 = ct * 8 + (lane & 3) * 2;
@@ -268,6 +285,10 @@ __global__ void __launch_bounds__(TetMma<N>::NTH, TetMma<N>::MINB)
       }
     }
   }
+  if (lsrk) {
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    __syncthreads();
+  }
   const int n = rt * 8 + (lane >> 2);
   if (n < NP) {
 #pragma unroll
@@ -277,7 +298,7 @@ __global__ void __launch_bounds__(TetMma<N>::NTH, TetMma<N>::MINB)
       const R kap = smat[e * 4 + 0], irho = smat[e * 4 + 1];
       const size_t base = (size_t)sk[e] * 4 * NP + n;
       const R* qe = sq + e * EQ + n;
-      const R* re = sres + e * EQ + n;
+      const R* re = sres + e * L::RB + n;
       epilogue_s<R>(E, HW_TET, base, accp[i] * kap, qe[0], re[0]);
 #pragma unroll
       for (int x = 0; x < 3; ++x)

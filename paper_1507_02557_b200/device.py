@@ -190,13 +190,38 @@ def _pack_ops(t, d):
         # 0, 1: scalar kernel (transposed); 2, 3: DMMA kernel (row-major, padded)
         return {0: np.stack([d["Dr"].T, d["Ds"].T, d["Dt"].T]), 1: d["LIFT"].T,
                 2: Dpad, 3: Lpad}
-    if t == "wedge":
-        # op[0][c][m][n] = S_c[n][m], op[1][c][m][n] = S_c[m][n]
-        return {0: np.stack([S.T for S in d["S"]]), 1: d["S"], 5: d["E"].T, 6: d["LIFT"].T}
-    if t == "pyramid":
-        return {0: np.stack([d["Dr"].T, d["Ds"].T, d["Dt"].T]),
-                1: np.stack([d["Dr"], d["Ds"], d["Dt"]]), 5: d["E"].T, 6: d["LIFT"].T}
+    if t in ("wedge", "pyramid"):
+        A = d["S"] if t == "wedge" else np.stack([d["Dr"], d["Ds"], d["Dt"]])
+        # scalar kernel: op[0][c][m][n] = A_c[n][m], op[1][c][m][n] = A_c[m][n]
+        ops = {0: np.stack([a.T for a in A]), 1: A, 5: d["E"].T, 6: d["LIFT"].T}
+        ops.update(_mma_ops(t, d, A))
+        return ops
     raise ValueError(t)
+
+
+def _mma_ops(t, d, A):
+    """Zero-padded row-major operands of the DMMA kernels (hw_dense_mma.cuh):
+    op[2] A_c, op[3] A_c^T (3, RT8, NPK); op[4] LIFT with each face's K block
+    padded to a multiple of 4 (RT8, NFKT); op[7] E (RTF8, NPK)."""
+    Np = d["Np"]
+    rt8, npk = -(-Np // 8) * 8, -(-Np // 4) * 4
+    Ap = np.zeros((3, rt8, npk))
+    ATp = np.zeros((3, rt8, npk))
+    for c in range(3):
+        Ap[c, :Np, :Np] = A[c]
+        ATp[c, :Np, :Np] = A[c].T
+    offs = d["face_offsets"]
+    cnts = np.diff(offs)
+    kf = [-(-int(c) // 4) * 4 for c in cnts]
+    L = np.zeros((rt8, sum(kf)))
+    k0 = 0
+    for f, c in enumerate(cnts):
+        L[:Np, k0:k0 + c] = d["LIFT"][:, offs[f]:offs[f + 1]]
+        k0 += kf[f]
+    nfp = int(offs[-1])
+    Ep = np.zeros((-(-nfp // 8) * 8, npk))
+    Ep[:nfp, :Np] = d["E"]
+    return {2: Ap, 3: ATp, 4: L, 7: Ep}
 
 
 def tet_gather_index(mesh, dops, perm_tri, face_offsets):
