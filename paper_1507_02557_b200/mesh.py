@@ -231,25 +231,29 @@ def _orient_tets(conn, X):
     return conn
 
 
-def layered_hybrid_mesh(n, kinds, zs=None):
-    """Unit-cube mesh of n x n cells per z-layer; kinds[k] in {"hex",
+def layered_hybrid_mesh(n, kinds, zs=None, nx=None):
+    """Box mesh of nx x n cells per z-layer (unit cube when nx = n; for
+    nx = m n the box is [0, m] x [0, 1] x [0, 1] with the same cell size, the
+    weak-scaling extension of the reference's cube); kinds[k] in {"hex",
     "wedge", "pyrtop", "pyr", "tet"} selects the cell decomposition of layer
     k ("pyrtop" = 5 pyramids + the top pyramid split into 2 tets, the
     reference's transition layer; "pyr" = 6 pyramids).  Vertex and element
     numbering follow the reference's cell walk (k outer, then j, then i)."""
     nz = len(kinds)
     zs = np.linspace(0.0, 1.0, nz + 1) if zs is None else np.asarray(zs, dtype=float)
-    xs = np.linspace(0.0, 1.0, n + 1)
-    gx, gy, gz = np.meshgrid(xs, xs, zs, indexing="ij")
+    nx = n if nx is None else int(nx)
+    xs = np.linspace(0.0, nx / n, nx + 1)
+    ys = np.linspace(0.0, 1.0, n + 1)
+    gx, gy, gz = np.meshgrid(xs, ys, zs, indexing="ij")
     # pool order: z outer, y, x inner
     grid = np.column_stack([gx.transpose(2, 1, 0).ravel(), gy.transpose(2, 1, 0).ravel(),
                             gz.transpose(2, 1, 0).ravel()])
     nv = len(grid)
 
     def vid(i, j, k):
-        return (k * (n + 1) + j) * (n + 1) + i
+        return (k * (n + 1) + j) * (nx + 1) + i
 
-    jj, ii = np.meshgrid(np.arange(n), np.arange(n), indexing="ij")
+    jj, ii = np.meshgrid(np.arange(n), np.arange(nx), indexing="ij")
     ii, jj = ii.ravel(), jj.ravel()                 # cell order within a layer: j outer, i inner
     blocks = {t: [] for t in ELEMENT_TYPES}
     extra = []
@@ -308,13 +312,15 @@ def hybrid_band_layout(n):
     return nz - t_l - 1 - w_l, w_l, 1, t_l
 
 
-def structured_hybrid_mesh(n):
+def structured_hybrid_mesh(n, nx=None):
     """The reference's hybrid cube: hex slab, wedge slab, one pyramid
-    transition layer, Kuhn tets (hybridwave/mesh.py:310-340)."""
+    transition layer, Kuhn tets (hybridwave/mesh.py:310-340).  nx > n
+    extends the box along x with the same cells (weak scaling)."""
     if n < 2:
         raise ValueError("hybrid cube needs n >= 2")
     h, w, p, t = hybrid_band_layout(n)
-    return layered_hybrid_mesh(n, ["hex"] * h + ["wedge"] * w + ["pyrtop"] * p + ["tet"] * t)
+    return layered_hybrid_mesh(n, ["hex"] * h + ["wedge"] * w + ["pyrtop"] * p + ["tet"] * t,
+                               nx=nx)
 
 
 def hex_dominant_mesh(n, layers=(110, 4, 1, 5)):
