@@ -49,6 +49,9 @@ def parse():
     ap.add_argument("--cpu-mesh", default=None, help="reference-arm sample mesh")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--scheme", default="lsrk", choices=["lsrk", "mrab"],
+                    help="mrab: multi-rate AB3 (active levels only), --levels levels")
+    ap.add_argument("--levels", type=int, default=3)
     ap.add_argument("--partitioned", action="store_true",
                     help="use the element-partitioned path even on one rank")
     return ap.parse_args()
@@ -220,6 +223,8 @@ def main():
     dt = min(float(v.min()) for v in local_timesteps(disc, 0.5).values())
     _ = disc.device_mesh
     setup_s = time.perf_counter() - t_setup
+    if args.scheme == "mrab":
+        return mrab_bench(args, disc, mesh, host_state, dev, setup_s)
     S = Stepper(disc, host_state, "lsrk")
     stream = torch.cuda.current_stream(dev)
 
@@ -350,6 +355,50 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+    return 0
+
+
+def mrab_bench(args, disc, mesh, host_state, dev, setup_s):
+    """Multi-rate AB3 (config 5): one step = one macro step; the unit of work
+    is an element RHS + update, so the metric counts the DOFs of the elements
+    that step at each tick (the reference evaluates the whole mesh every tick
+    and discards the rest, hybridwave/timeint.py:120)."""
+    import torch
+    from paper_1507_02557_b200.stability import assign_mrab_levels, local_timesteps
+    from paper_1507_02557_b200.timeint import MRABDriver
+    L = args.levels
+    plan = assign_mrab_levels(local_timesteps(disc, 0.5), L, mesh)
+    drv = MRABDriver(disc, plan)
+    macro = 2 ** (L - 1) * plan.dt_min
+    q = disc.to_device(host_state)
+    drv.run(q, macro * args.warmup)
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
+        e0.record(stream)
+        drv.run(q, macro * args.steps)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    active = sum(int((plan.levels[t] == lev).sum()) * 4 * disc.ops[t].Np * 2 ** (lev - 1)
+                 for t in disc.types for lev in range(1, L + 1))
+    full = disc.n_dof * 2 ** (L - 1)
+    value = active * args.steps / (ms * 1e-3) / 1e9
+    occ = {lev: sum(int((plan.levels[t] == lev).sum()) for t in disc.types)
+           for lev in range(1, L + 1)}
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": args.dtype,
+            "data": "synthetic (cavity eigenmode projected on the mesh)",
+            "config": {"workload": f"{args.mesh} N={args.order} {args.form} MRAB-AB3 "
+                                   f"{L} levels (configs[4]); step = macro step",
+                       "level_occupancy": occ, "active_dof_per_macro": active,
+                       "full_mesh_dof_per_macro": full, "dt_min": plan.dt_min,
+                       "setup_s": setup_s},
+            "gpu_launches": None, "clocks": clk.summary(), "roofline": None, "e2e": None,
+            "cpu_baseline": None}
+    print(json.dumps(line), flush=True)
     return 0
 
 

@@ -27,16 +27,14 @@ _INTERIOR_ABC = {"tet": np.array([[-0.5, -0.5, -0.5]]), "wedge": np.array([[0.0,
 def _affine_check(t, verts, N):
     """The nodal-face representation needs affine wedges/pyramids (constant
     J); tets are always affine."""
-    from .quadrature import element_rule
+    from .refelem import affine_mask
     if t not in ("wedge", "pyramid") or len(verts) == 0:
         return
-    rule = element_rule(t, max(N, 1))
-    _, J, _, _ = geometric_factors_batch(t, verts, rule.collapsed, label=t)
-    spread = (J.max(axis=1) - J.min(axis=1)) / J.max(axis=1)
-    if spread.max() > 1e-9:
+    bad = ~affine_mask(t, verts, tol=1e-10)
+    if bad.any():
         raise NotImplementedError(
-            f"non-affine {t} elements (J varies by {spread.max():.2e}); the device path "
-            "currently requires affine wedges and pyramids (DESIGN.md, scope)")
+            f"{int(bad.sum())} non-affine {t} elements; the device path currently requires "
+            "affine wedges and pyramids (DESIGN.md, scope)")
 
 
 def face_impedance_avg(mesh, t):
@@ -68,13 +66,11 @@ def geometry_records(t, verts, zavg):
         out[:, 24:36:2] = zavg
         out[:, 25:36:2] = 1.0 / zavg
         # affine hexes (parallelepipeds): constant metric and face geometry
-        c = np.array([[-0.9, -0.7, -0.8], [0.0, 0.0, 0.0], [0.6, 0.9, -0.5]])
-        _, J, G, _ = geometric_factors_batch("hex", verts, c, label=t)
-        aff = (np.abs(G - G[:, :1]).max(axis=(1, 2, 3)) <= 1e-13 * np.abs(G).max(axis=(1, 2, 3))) & \
-              (np.abs(J - J[:, :1]).max(axis=1) <= 1e-13 * J.max(axis=1))
-        out[:, 36] = aff.astype(float)
-        out[:, 37:46] = G[:, 1].reshape(K, 9)
-        out[:, 46] = J[:, 1]
+        from .refelem import affine_mask
+        _, J, G, _ = geometric_factors_batch("hex", verts, np.zeros((1, 3)), label=t)
+        out[:, 36] = affine_mask("hex", verts).astype(float)
+        out[:, 37:46] = G[:, 0].reshape(K, 9)
+        out[:, 46] = J[:, 0]
         for f in range(6):
             _, Js, nrm = face_geometry_batch("hex", verts, f, _CENTROID2D["quad"])
             out[:, 47 + 4 * f: 50 + 4 * f] = nrm[:, 0]

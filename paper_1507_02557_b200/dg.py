@@ -24,7 +24,7 @@ from . import _native as nat
 from .operators import TYPE_ID, build_operators, face_symmetry_perms
 from .quadrature import element_rule
 from .refelem import (FACES, duffy_map, face_geometry_batch, geometric_factors_batch,
-                      inverse_duffy_map, jacobian_det, map_points)
+                      inverse_duffy_map, jacobian_det, jacobian_det_fast, map_points)
 
 __all__ = ["Formulation", "TABLE_FORMS", "flux_penalties", "Discretization",
            "discrete_energy", "zero_state", "FIELDS"]
@@ -254,11 +254,7 @@ class Discretization:
             rule = element_rule(t, self.N if which == "cub" else self.N + 2)
             verts = self.mesh.element_vertices(t)
             x = map_points(t, verts, rule.collapsed)
-            if t == "tet":   # affine: one determinant per element
-                J = np.repeat(jacobian_det(t, verts, rule.collapsed[:1]), len(rule.weights),
-                              axis=1)
-            else:
-                J = jacobian_det(t, verts, rule.collapsed)
+            J = jacobian_det_fast(t, verts, rule.collapsed)
             self._cub[key] = (rule.weights, self._basis_values(t, rule.collapsed), x, J)
         return self._cub[key]
 
@@ -292,7 +288,7 @@ class Discretization:
                 state[t] = (vals * (w[None, :] * np.sqrt(J))[:, None, :]) @ V
             else:
                 raw = (vals * (w[None, :] * J)[:, None, :]) @ V
-                Jr = jacobian_det(t, self.mesh.element_vertices(t), self.ops[t].level_abc)
+                Jr = jacobian_det_fast(t, self.mesh.element_vertices(t), self.ops[t].level_abc)
                 state[t] = raw / Jr[:, None, :]
         return state
 

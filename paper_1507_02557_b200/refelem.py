@@ -14,7 +14,7 @@ __all__ = [
     "duffy_map", "inverse_duffy_map", "shape_functions_abc",
     "shape_gradients_rst", "geometric_factors_batch",
     "face_quadrature_points", "face_geometry_batch", "face_shape2d",
-    "map_points", "jacobian_det",
+    "map_points", "jacobian_det", "jacobian_det_fast", "affine_mask",
 ]
 
 ELEMENT_TYPES = ("hex", "wedge", "pyramid", "tet")
@@ -190,21 +190,59 @@ def geometric_factors_batch(elem_type, verts, abc, label="element"):
 
 
 def map_points(elem_type, verts, abc):
-    """Physical positions (K, P, 3) of collapsed points (no metric work)."""
-    return np.einsum("kvx,pv->kpx", np.asarray(verts, dtype=float),
-                     shape_functions_abc(elem_type, abc))
+    """Physical positions (K, P, 3) of collapsed points (no metric work;
+    batched GEMM instead of einsum)."""
+    verts = np.asarray(verts, dtype=float)
+    return np.matmul(shape_functions_abc(elem_type, abc)[None], verts)
+
+
+def affine_mask(elem_type, verts, tol=1e-12):
+    """(K,) bool: the vertex map is affine (tets always; parallelepiped hexes,
+    prism wedges with a translated top triangle, parallelogram-based
+    pyramids)."""
+    X = np.asarray(verts, dtype=float)
+    scale = np.abs(X).max(axis=(1, 2)) + 1e-300
+    if elem_type == "tet":
+        return np.ones(len(X), dtype=bool)
+    if elem_type == "hex":
+        e = [X[:, 1] - X[:, 0] - (X[:, 2] - X[:, 3]), X[:, 1] - X[:, 0] - (X[:, 5] - X[:, 4]),
+             X[:, 1] - X[:, 0] - (X[:, 6] - X[:, 7]), X[:, 4] - X[:, 0] - (X[:, 7] - X[:, 3])]
+    elif elem_type == "wedge":
+        e = [X[:, 3] - X[:, 0] - (X[:, 4] - X[:, 1]), X[:, 3] - X[:, 0] - (X[:, 5] - X[:, 2])]
+    elif elem_type == "pyramid":
+        e = [X[:, 1] - X[:, 0] - (X[:, 2] - X[:, 3])]
+    else:
+        raise ValueError(elem_type)
+    err = np.max([np.abs(v).max(axis=1) for v in e], axis=0)
+    return err <= tol * scale
 
 
 def jacobian_det(elem_type, verts, abc):
-    """det(dx/dr) (K, P) without forming the inverse."""
-    F = np.einsum("kvx,pvr->kpxr", np.asarray(verts, dtype=float),
-                  shape_gradients_rst(elem_type, abc))
-    J = (F[..., 0, 0] * (F[..., 1, 1] * F[..., 2, 2] - F[..., 1, 2] * F[..., 2, 1])
-         - F[..., 0, 1] * (F[..., 1, 0] * F[..., 2, 2] - F[..., 1, 2] * F[..., 2, 0])
-         + F[..., 0, 2] * (F[..., 1, 0] * F[..., 2, 1] - F[..., 1, 1] * F[..., 2, 0]))
+    """det(dx/dr) (K, P) without forming the inverse (batched GEMMs)."""
+    verts = np.asarray(verts, dtype=float)
+    g = shape_gradients_rst(elem_type, abc)                  # (P, nv, 3)
+    Fc = [np.matmul(g[None, :, :, r], verts) for r in range(3)]   # (K, P, 3) = dx/dr_r
+    a, b, c = Fc
+    J = (a[..., 0] * (b[..., 1] * c[..., 2] - b[..., 2] * c[..., 1])
+         - b[..., 0] * (a[..., 1] * c[..., 2] - a[..., 2] * c[..., 1])
+         + c[..., 0] * (a[..., 1] * b[..., 2] - a[..., 2] * b[..., 1]))
     if np.any(J <= 0):
         raise InvalidElementError(f"nonpositive Jacobian in {elem_type} (min J = {J.min():.3e})")
     return J
+
+
+def jacobian_det_fast(elem_type, verts, abc):
+    """jacobian_det, evaluated once per affine element and broadcast."""
+    verts = np.asarray(verts, dtype=float)
+    aff = affine_mask(elem_type, verts)
+    P = len(np.atleast_2d(abc))
+    out = np.empty((len(verts), P))
+    if aff.any():
+        interior = np.atleast_2d(abc)[:1]
+        out[aff] = jacobian_det(elem_type, verts[aff], interior)
+    if (~aff).any():
+        out[~aff] = jacobian_det(elem_type, verts[~aff], abc)
+    return out
 
 
 def face_shape2d(face_type, p):
