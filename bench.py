@@ -178,14 +178,24 @@ class ClockSampler:
 
 # ------------------------------------------------------------------ GPU arm
 
-def alg_bytes_per_elem(t, Np, s, N):
+def face_points(t, N):
+    nfn, nfq = (N + 1) * (N + 2) // 2, (N + 1) ** 2
+    return {"hex": 6 * nfq, "tet": 4 * nfn, "wedge": 2 * nfn + 3 * nfq,
+            "pyramid": nfq + 4 * nfn}[t]
+
+
+def alg_bytes_per_elem(t, Np, s, N, gl=True):
     """Compulsory HBM traffic of one LSRK stage per element in this layout:
     read q, read res, write res, write q_out (4 x 4 Np words), geometry
-    record, material record, and the neighbour links (tets: the int32 gather
-    index per face node; other types: index + code per face).  Neighbour
-    states are re-read from L2 (not counted)."""
+    record, material record, the neighbour links (tets: the int32 gather
+    index per face node; other types: index + code per face), and for the
+    trace-publishing types (wedge, pyramid, GL hex) reading the own face
+    traces of q_in and writing those of q_out (2 x 4 x Nfp words).
+    Neighbour states / traces are re-read from L2 (not counted)."""
     links = 4 * 4 * (N + 1) * (N + 2) // 2 if t == "tet" else 8 * NFACES[t]
-    return 4 * 4 * Np * s + GEO_WORDS[t] * s + 4 * s + links
+    pub = t in ("wedge", "pyramid") or (t == "hex" and gl)
+    tr = 2 * 4 * face_points(t, N) * s if pub else 0
+    return 4 * 4 * Np * s + GEO_WORDS[t] * s + 4 * s + links + tr
 
 
 def main():
@@ -291,7 +301,8 @@ def main():
         torch.cuda.synchronize()
         us = a.elapsed_time(b) * 1e3 / reps
         Np = disc.ops[t].Np
-        nbytes = disc.n_elems[t] * alg_bytes_per_elem(t, Np, s_bytes, args.order)
+        nbytes = disc.n_elems[t] * alg_bytes_per_elem(t, Np, s_bytes, args.order,
+                                                     args.form == "GL")
         per_type[t] = {"us_per_launch": us, "elements": disc.n_elems[t],
                        "alg_bytes": nbytes, "GBps": nbytes / (us * 1e-6) / 1e9}
     dom = max(per_type, key=lambda t: per_type[t]["us_per_launch"])
@@ -306,7 +317,8 @@ def main():
         prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
     except Exception:
         pass
-    traffic = prof.get(f"{args.mesh}/N{args.order}/{args.form}/{args.dtype}/{dom}")
+    tr_ent = prof.get(f"{args.mesh}/N{args.order}/{args.form}/{args.dtype}/{dom}")
+    traffic = tr_ent["bytes"] if isinstance(tr_ent, dict) else tr_ent
     roof = {"bound": "hbm", "kernel": f"{dom}_kernel<{args.order},{'double' if s_bytes == 8 else 'float'}>",
             "achieved": per_type[dom]["GBps"], "peak": hbm, "unit": "GB/s",
             "frac": per_type[dom]["GBps"] / hbm, "traffic": traffic,
