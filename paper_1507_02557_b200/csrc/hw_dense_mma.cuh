@@ -35,16 +35,17 @@ struct DMma {
   static constexpr int EQ = stride4mod16(4 * NPK);
   static constexpr int EV = stride4mod16(3 * NPK);
   static constexpr int EF = stride4mod16(NFKT);
-  static constexpr int STG = stage_off<N, T>(NF);
-  static constexpr int ESG = STG + 1;
-  static constexpr int ETR = 4 * NFP + 1;
+  // own traces and neighbour values, both [4][NFP] in my face-point order
+  // (even stride: 16-byte copies)
+  static constexpr int ETR = 4 * NFP + 2;
+  static constexpr int ESG = ETR;
   // storage shared by phase-disjoint buffers: v_c (volume) with fp/fu
   // (flux, lift); own + neighbour traces (flux) with the residual (epilogue)
   static constexpr int RA = cmax(EV, 2 * EF), RB = cmax(ETR + ESG, EQ);
   static constexpr int SQ = 0, SV = SQ + E * EQ, SFP = SV, SFU = SFP + E * EF,
                        STR = SV + E * RA, SST = STR + E * ETR, SRES = STR,
                        SG = STR + E * RB, SMAT = SG + E * GEO, TOTAL = SMAT + E * 4;
-  static constexpr size_t BYTES = sizeof(double) * TOTAL + sizeof(int) * (E + 2 * E * NF);
+  static constexpr size_t BYTES = sizeof(double) * TOTAL + sizeof(int) * (E + E * NF);
   static constexpr bool VEC = (NP % 2 == 0) && (NPK == NP);
 };
 
@@ -62,7 +63,6 @@ __global__ void __launch_bounds__(DMma<N, T>::NTH)
   R* sm = reinterpret_cast<R*>(smem_raw);
   int* sk = reinterpret_cast<int*>(sm + L::TOTAL);
   int* snc = sk + EB;
-  int* sne = snc + EB * NF;
   R* sq = sm + L::SQ;
   R* sres = sm + L::SRES;
   R* sv = sm + L::SV;
@@ -108,11 +108,12 @@ __global__ void __launch_bounds__(DMma<N, T>::NTH)
       cp_async(sq + e * EQ + fld * NPK + n, q + (size_t)sk[e] * 4 * NP + r);
     }
   }
-  {
+  {   // own traces of the input state (published by the previous stage)
     const R* tr = (const R*)M.tr_in[T];
-    for (int i = tid; i < ne * 4 * NFP; i += NTH) {
-      const int e = i / (4 * NFP), r = i - e * 4 * NFP;
-      cp_async(str + e * ETR + r, tr + (size_t)sk[e] * 4 * NFP + r);
+    constexpr int CT = 2 * NFP;                     // 16-byte chunks per element
+    for (int i = tid; i < ne * CT; i += NTH) {
+      const int e = i / CT, c = i - e * CT;
+      cp_async16(str + e * ETR + 2 * c, tr + (size_t)sk[e] * 4 * NFP + 2 * c);
     }
   }
   for (int i = tid; i < ne * GEO; i += NTH) {
@@ -121,49 +122,46 @@ __global__ void __launch_bounds__(DMma<N, T>::NTH)
   }
   for (int i = tid; i < ne * 4; i += NTH)
     cp_async(smat + i, (const R*)TY.mat + (size_t)sk[i >> 2] * 4 + (i & 3));
-  for (int i = tid; i < ne * NF; i += NTH) {
-    const int e = i / NF, f = i - e * NF;
-    snc[i] = __ldg(TY.nbr_code + (size_t)sk[e] * NF + f);
-    sne[i] = __ldg(TY.nbr_elem + (size_t)sk[e] * NF + f);
-  }
+  for (int i = tid; i < ne * NF; i += NTH)
+    snc[i] = __ldg(TY.nbr_code + (size_t)sk[i / NF] * NF + i % NF);
   cp_async_commit();
-  __syncthreads();
   {
-    // stage_neighbours uses NT/32 warps; emulate with this block's warps
-    using Dm = Dims<N>;
+    // neighbour values at my face points through the host gather index
+    // (already in my point order): index loads batched, then cp.async
     const bool sem = M.formulation == HW_SEM;
-    for (int pr = warp; pr < ne * NF; pr += L::W) {
-      const int e = pr / NF, f = pr - e * NF;
-      const int code = snc[pr];
-      if (code & HW_NBR_BOUNDARY) continue;
-      const int t2 = HW_NBR_TYPE(code), f2 = HW_NBR_FACE(code);
-      const int k2 = sne[pr];
-      const int cnt = X::cnt(f);
-      R* dst = sst + e * ESG + stage_off<N, T>(f);
+    constexpr int IT = (EB * NFP + NTH - 1) / NTH;
+    int gv[IT];
+#pragma unroll
+    for (int u = 0; u < IT; ++u) {
+      const int i = tid + u * NTH;
+      gv[u] = -1;
+      if (i < ne * NFP) gv[u] = __ldg(TY.iop[1] + (size_t)sk[i / NFP] * NFP + i % NFP);
+    }
+    __syncthreads();                                // snc
+#pragma unroll
+    for (int u = 0; u < IT; ++u) {
+      const int i = tid + u * NTH;
+      if (i >= ne * NFP || gv[u] < 0) continue;
+      const int e = i / NFP, j = i - e * NFP;
+      int jj;
+      const int f = face_of_point<N, T>(j, jj);
+      const int t2 = HW_NBR_TYPE(snc[e * NF + f]);
+      const R* src;
+      int stride;
       if (publishes(t2, sem)) {
-        const int nfp2 = nfp_of<N>(t2);
-        const R* src = (const R*)M.tr_in[t2] + (size_t)k2 * 4 * nfp2 + face_offset<N>(t2, f2);
-        for (int i = lane; i < 4 * cnt; i += 32) {
-          const int c = i / cnt, p = i - c * cnt;
-          cp_async(dst + i, src + c * nfp2 + p);
-        }
+        src = (const R*)M.tr_in[t2];
+        stride = nfp_of<N>(t2);
       } else if (t2 == HW_TET) {
-        const R* q2 = (const R*)Q.p[HW_TET] + (size_t)k2 * 4 * Dm::NP_TET;
-        const int* fn = M.t[HW_TET].iop[0] + f2 * Dm::NFN;
-        for (int i = lane; i < 4 * Dm::NFN; i += 32) {
-          const int c = i / Dm::NFN, n = i - c * Dm::NFN;
-          cp_async(dst + i, q2 + c * Dm::NP_TET + __ldg(fn + n));
-        }
+        src = (const R*)Q.p[HW_TET];
+        stride = Dims<N>::NP_TET;
       } else {
-        const R* q2 = (const R*)Q.p[HW_HEX] + (size_t)k2 * 4 * Dm::NP_HEX;
-        const int* tab = M.t[HW_HEX].iop[0] + 3 * f2 * Dm::NFQ;
-        for (int i = lane; i < 4 * Dm::NFQ; i += 32) {
-          const int c = i / Dm::NFQ, p = i - c * Dm::NFQ;
-          const int base = __ldg(tab + 3 * p), stride = __ldg(tab + 3 * p + 1),
-                    end = __ldg(tab + 3 * p + 2);
-          cp_async(dst + i, q2 + c * Dm::NP_HEX + base + (end ? N : 0) * stride);
-        }
+        src = (const R*)Q.p[HW_HEX];
+        stride = Dims<N>::NP_HEX;
       }
+      src += gv[u];
+      R* dst = sst + e * ESG + j;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) cp_async(dst + c * NFP, src + c * stride);
     }
     cp_async_commit();
   }
@@ -229,9 +227,8 @@ __global__ void __launch_bounds__(DMma<N, T>::NTH)
     if (code & HW_NBR_BOUNDARY) {
       pp = -own[0]; up[0] = um[0]; up[1] = um[1]; up[2] = um[2];
     } else {
-      R tr[4];
-      staged_trace<N, T, R>(M, code, f, jj, sst + e * ESG, tr);
-      pp = tr[0]; up[0] = tr[1]; up[1] = tr[2]; up[2] = tr[3];
+      const R* se = sst + e * ESG + j;
+      pp = se[0]; up[0] = se[NFP]; up[1] = se[2 * NFP]; up[2] = se[3 * NFP];
     }
     R tp, tu, fp, fu;
     penalties(g[4], g[5], pen, tp, tu);
@@ -319,25 +316,34 @@ __global__ void __launch_bounds__(DMma<N, T>::NTH)
     __syncthreads();
     const R* Ep = (const R*)TY.op[7];   // [RTF*8][NPK]
     R* tro = (R*)M.tr_out[T];
-    // columns: (element, field) pairs, col = e*4 + c; 4 column tiles for E = 8
-    for (int tile = warp; tile < L::RTF * 4; tile += L::W) {
-      const int rf = tile >> 2, cf = tile & 3;
-      const int col = cf * 8 + (lane >> 2);
-      const R* bsrc = sq + (col >> 2) * EQ + (col & 3) * NPK + bk;
-      const int er = rf * 8 + (lane >> 2);
-      R y[2] = {0, 0};
+    // columns: (element, field) pairs, col = e*4 + c; 4 column tiles for
+    // E = 8.  One row tile per warp pass, each A fragment feeds 4 MMAs.
+    const int er = lane >> 2;
+    for (int rf = warp; rf < L::RTF; rf += L::W) {
+      R y[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
+      const R* arow_p = Ep + (size_t)(rf * 8 + er) * NPK + acol;
 #pragma unroll 5
-      for (int ks = 0; ks < NPK / 4; ++ks)
-        dmma884(y[0], y[1], ldg(Ep + (size_t)er * NPK + ks * 4 + acol), bsrc[ks * 4]);
-      const int j = er;
-      const int c0 = cf * 8 + (lane & 3) * 2;          // output columns c0, c0+1
-      const int e = c0 >> 2;
-      if (j < NFP && e < ne) {
-        R s = R(1);
-        if (T == HW_WEDGE) s = sg[e * GEO + 9];
-        R* o = tro + (size_t)sk[e] * 4 * NFP + j;
-        o[(c0 & 3) * NFP] = y[0] * s;
-        o[((c0 & 3) + 1) * NFP] = y[1] * s;
+      for (int ks = 0; ks < NPK / 4; ++ks) {
+        const R a = ldg(arow_p + ks * 4);
+#pragma unroll
+        for (int cf = 0; cf < 4; ++cf) {
+          const int col = cf * 8 + er;
+          dmma884(y[cf][0], y[cf][1], a, sq[(col >> 2) * EQ + (col & 3) * NPK + bk + ks * 4]);
+        }
+      }
+      const int j = rf * 8 + er;
+      if (j < NFP) {
+#pragma unroll
+        for (int cf = 0; cf < 4; ++cf) {
+          const int c0 = cf * 8 + (lane & 3) * 2;      // output columns c0, c0+1
+          const int e = c0 >> 2;
+          if (e >= ne) continue;
+          R s = R(1);
+          if (T == HW_WEDGE) s = sg[e * GEO + 9];
+          R* o = tro + (size_t)sk[e] * 4 * NFP + j;
+          o[(c0 & 3) * NFP] = y[cf][0] * s;
+          o[((c0 & 3) + 1) * NFP] = y[cf][1] * s;
+        }
       }
     }
   }

@@ -154,6 +154,7 @@ def pack_mesh(disc):
         dops = dops_all[t]
         dops_any = dops
         perm_tri = face_symmetry_perms("tri", dops["tri2d"])
+        perm_quad = face_symmetry_perms("quad", dops["quad2d"])
         elem, code = neighbour_codes(mesh, t)
         pack["types"][t] = {
             "K": disc.n_elems[t], "form": form, "dops": dops,
@@ -161,7 +162,8 @@ def pack_mesh(disc):
             "mat": material_records(np.asarray(mesh.materials[t], dtype=float)),
             "nbr_elem": elem, "nbr_code": code,
             "op": _pack_ops(t, dops),
-            "iop": _pack_iops(t, dops, disc.N, mesh, perm_tri, face_offsets),
+            "iop": _pack_iops(t, dops, disc.N, mesh, perm_tri, face_offsets, dops_all,
+                              perm_quad, disc.formulation.kind == "SEM"),
             "nfp": int(dops["face_offsets"][-1]),
             "publishes": t in ("wedge", "pyramid") or (t == "hex"
                                                        and disc.formulation.kind == "GL")}
@@ -252,12 +254,57 @@ def tet_gather_index(mesh, dops, perm_tri, face_offsets):
     return out.astype(np.int32)
 
 
-def _pack_iops(t, d, N, mesh=None, perm_tri=None, face_offsets=None):
+def face_gather_index(mesh, t, dops_all, perm_tri, perm_quad, face_offsets, N, sem):
+    """(K, Nfp) int32 for the wedge / pyramid kernels: for each of my face
+    points (device order, hybridwave/dg.py:258-300 neighbour trace, already
+    permuted into my point order) the field-0 offset of the coincident
+    neighbour value in its source array; the source (and its field stride)
+    follows from the face's neighbour code: a publishing type's trace buffer
+    (K2, 4, Nfp2), else the tet / SEM-hex state (K2, 4, Np2).  -1 on the
+    boundary."""
+    nbr = mesh.nbr[t]
+    code = mesh.face_code[t]
+    offs, nfp = face_offsets[t]
+    K = len(nbr)
+    nfn = (N + 1) * (N + 2) // 2
+    out = np.full((K, nfp), -1, dtype=np.int64)
+    names = ("hex", "wedge", "pyramid", "tet")
+    for f in range(len(offs) - 1):
+        a, b = int(offs[f]), int(offs[f + 1])
+        perm = perm_tri if b - a == nfn else perm_quad
+        for tid2, t2 in enumerate(names):
+            sel = nbr[:, f, 0] == tid2
+            if not sel.any():
+                continue
+            k2, f2, pc = nbr[sel, f, 1], nbr[sel, f, 2], code[sel, f]
+            p = perm[pc]                                   # (n, cnt) neighbour face point
+            if t2 in ("wedge", "pyramid") or (t2 == "hex" and not sem):
+                offs2, nfp2 = face_offsets[t2]
+                val = k2[:, None] * 4 * nfp2 + offs2[f2][:, None] + p
+            elif t2 == "tet":
+                d2 = dops_all["tet"]
+                fn = d2["face_nodes"].reshape(4, nfn)
+                val = k2[:, None] * 4 * d2["Np"] + fn[f2[:, None], p]
+            else:                                          # SEM hex: face node of the point
+                d2 = dops_all["hex"]
+                nfq = (N + 1) ** 2
+                tab = d2["face_tab"]
+                row = f2[:, None] * nfq + p
+                node = tab[row, 0] + np.where(tab[row, 2] != 0, N, 0) * tab[row, 1]
+                val = k2[:, None] * 4 * d2["Np"] + node
+            out[sel, a:b] = val
+    if out.max(initial=0) >= 2 ** 31:
+        raise ValueError("face gather offsets exceed int32")
+    return out.astype(np.int32)
+
+
+def _pack_iops(t, d, N, mesh=None, perm_tri=None, face_offsets=None, dops_all=None,
+               perm_quad=None, sem=False):
     if t == "hex":
         return {0: d["face_tab"], 1: hex_node_face_points(d, N)}
     if t == "tet":
         return {0: d["face_nodes"], 1: tet_gather_index(mesh, d, perm_tri, face_offsets)}
-    return {}
+    return {1: face_gather_index(mesh, t, dops_all, perm_tri, perm_quad, face_offsets, N, sem)}
 
 
 class DeviceMesh:
