@@ -80,17 +80,31 @@ static int launch_dense(const hw_mesh_t& M, const hw_fields_t& Q, const Epi& E,
   return check_launch("dense_kernel");
 }
 
+// shared-memory floor per CTA (bytes, env HW_SMEM_FLOOR; tuning experiments:
+// fewer resident CTAs leave more of the SM's L1 for the operator matrices)
+static size_t smem_floor() {
+  static const size_t v = [] {
+    const char* e = getenv("HW_SMEM_FLOOR");
+    return e ? (size_t)atol(e) : (size_t)0;
+  }();
+  return v;
+}
+
 template <int N, int T>
 static int launch_dense_mma(const hw_mesh_t& M, const hw_fields_t& Q, const Epi& E,
                             const int32_t* list, int64_t n, cudaStream_t st) {
   using L = DMma<N, T>;
-  if (L::BYTES > 220 * 1024)   // high orders: the scalar kernel fits, the DMMA one does not
+  // high orders (N >= 6): the DMMA kernel exceeds the CTA's thread / smem limits
+  if constexpr (L::BYTES > 220 * 1024 || L::NTH > 1024) {
     return launch_dense<N, T, double>(M, Q, E, list, n, st);
+  } else {
   int rc;
-  if ((rc = set_smem(dense_mma_kernel<N, T>, L::BYTES))) return rc;
-  dense_mma_kernel<N, T><<<(unsigned)((n + L::E - 1) / L::E), L::NTH, L::BYTES, st>>>(M, Q, E,
-                                                                                   list, n);
+  const size_t bytes = L::BYTES > smem_floor() ? L::BYTES : smem_floor();
+  if ((rc = set_smem(dense_mma_kernel<N, T>, bytes))) return rc;
+  dense_mma_kernel<N, T><<<(unsigned)((n + L::E - 1) / L::E), L::NTH, bytes, st>>>(M, Q, E,
+                                                                                 list, n);
   return check_launch("dense_mma_kernel");
+  }
 }
 
 template <int N, int T, typename R>

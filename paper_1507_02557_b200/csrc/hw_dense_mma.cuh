@@ -22,7 +22,9 @@ struct DMma {
   static constexpr int RT = (NP + 7) / 8;
   static constexpr int RT8 = RT * 8;
   static constexpr int NPK = ((NP + 3) / 4) * 4;
-  static constexpr int W = RT;
+  // two warp groups of RT warps: group 0 grad p + the u lift (u rows),
+  // group 1 div v + the p lift (p rows)
+  static constexpr int W = 2 * RT;
   static constexpr int NTH = 32 * W;
   __host__ __device__ static constexpr int kf(int f) { return ((X::cnt(f) + 3) / 4) * 4; }
   __host__ __device__ static constexpr int koff(int f) {
@@ -181,23 +183,30 @@ __global__ void __launch_bounds__(DMma<N, T>::NTH)
   __syncthreads();
 
   // ---- volume GEMMs
-  const int rt = warp;
+  const int grp = warp / L::RT, rt = warp - grp * L::RT;   // grp is warp-uniform
   const int arow = rt * 8 + (lane >> 2), acol = lane & 3;
   const int bk = lane & 3, bcol = lane >> 2;
   R dp[3][2] = {{0, 0}, {0, 0}, {0, 0}}, dv[2] = {0, 0};
   {
     const R* A = (const R*)TY.op[2];    // [3][RT8][NPK]  A_c
     const R* AT = (const R*)TY.op[3];   // [3][RT8][NPK]  A_c^T
-    const R* bq = sq + bcol * EQ + bk;
-    const R* bv = sv + bcol * EV + bk;
+    if (grp == 0) {
+      const R* bq = sq + bcol * EQ + bk;
 #pragma unroll
-    for (int c = 0; c < 3; ++c) {
-#pragma unroll 5
-      for (int ks = 0; ks < NPK / 4; ++ks) {
-        const size_t ai = ((size_t)c * L::RT8 + arow) * NPK + ks * 4 + acol;
-        const R a = ldg(A + ai);
-        dmma884(dp[c][0], dp[c][1], a, bq[ks * 4]);
-        dmma884(dv[0], dv[1], skew ? ldg(AT + ai) : a, bv[c * NPK + ks * 4]);
+      for (int c = 0; c < 3; ++c) {
+        const R* ac = A + ((size_t)c * L::RT8 + arow) * NPK + acol;
+#pragma unroll 10
+        for (int ks = 0; ks < NPK / 4; ++ks) dmma884(dp[c][0], dp[c][1], ldg(ac + ks * 4), bq[ks * 4]);
+      }
+    } else {
+      const R* bv = sv + bcol * EV + bk;
+      const R* AV = skew ? AT : A;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const R* ac = AV + ((size_t)c * L::RT8 + arow) * NPK + acol;
+#pragma unroll 10
+        for (int ks = 0; ks < NPK / 4; ++ks)
+          dmma884(dv[0], dv[1], ldg(ac + ks * 4), bv[c * NPK + ks * 4]);
       }
     }
   }
@@ -255,20 +264,25 @@ __global__ void __launch_bounds__(DMma<N, T>::NTH)
     cp_async_commit();
   }
 
-  // ---- lift GEMMs, combine, epilogue
+  // ---- lift GEMMs, combine, epilogue (group 1: p rows, group 0: u rows)
   const int col0 = (lane & 3) * 2;
-  R accp[2] = {skew ? dv[0] : -dv[0], skew ? dv[1] : -dv[1]};
-  R accu[3][2];
-#pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    const R* G = sg + (col0 + i) * GEO;
-#pragma unroll
-    for (int x = 0; x < 3; ++x)
-      accu[x][i] = -(G[x] * dp[0][i] + G[3 + x] * dp[1][i] + G[6 + x] * dp[2][i]);
-  }
-  {
-    const R* LF = (const R*)TY.op[4];   // [RT8][NFKT]
+  const R* LF = (const R*)TY.op[4];     // [RT8][NFKT]
+  R acc[3][2];
+  if (grp == 1) {
+    acc[0][0] = skew ? dv[0] : -dv[0];
+    acc[0][1] = skew ? dv[1] : -dv[1];
     const R* bp = sfp + bcol * EF + bk;
+#pragma unroll
+    for (int k = 0; k < L::NFKT; k += 4)
+      dmma884(acc[0][0], acc[0][1], ldg(LF + (size_t)arow * L::NFKT + k + acol), bp[k]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const R* G = sg + (col0 + i) * GEO;
+#pragma unroll
+      for (int x = 0; x < 3; ++x)
+        acc[x][i] = -(G[x] * dp[0][i] + G[3 + x] * dp[1][i] + G[6 + x] * dp[2][i]);
+    }
     const R* bu = sfu + bcol * EF + bk;
 #pragma unroll
     for (int f = 0; f < NF; ++f) {
@@ -276,16 +290,14 @@ __global__ void __launch_bounds__(DMma<N, T>::NTH)
 #pragma unroll
       for (int ks = 0; ks < L::kf(f) / 4; ++ks) {
         const int k = L::koff(f) + ks * 4;
-        const R a = ldg(LF + (size_t)arow * L::NFKT + k + acol);
-        dmma884(accp[0], accp[1], a, bp[k]);
-        dmma884(tu[0], tu[1], a, bu[k]);
+        dmma884(tu[0], tu[1], ldg(LF + (size_t)arow * L::NFKT + k + acol), bu[k]);
       }
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
         const R* g = sg + (col0 + i) * GEO + GF + FS * f;
-        accu[0][i] += g[0] * tu[i];
-        accu[1][i] += g[1] * tu[i];
-        accu[2][i] += g[2] * tu[i];
+        acc[0][i] += g[0] * tu[i];
+        acc[1][i] += g[1] * tu[i];
+        acc[2][i] += g[2] * tu[i];
       }
     }
   }
@@ -299,15 +311,18 @@ __global__ void __launch_bounds__(DMma<N, T>::NTH)
     for (int i = 0; i < 2; ++i) {
       const int e = col0 + i;
       if (e >= ne) continue;
-      const R kap = smat[e * 4 + 0], irho = smat[e * 4 + 1];
       const size_t base = (size_t)sk[e] * 4 * NP + n;
       R* qe = sq + e * EQ + n;
       const R* re = sres + e * EQ + n;
-      qe[0] = epilogue_q<R>(E, T, base, accp[i] * kap, qe[0], re[0]);
+      if (grp == 1) {
+        qe[0] = epilogue_q<R>(E, T, base, acc[0][i] * smat[e * 4 + 0], qe[0], re[0]);
+      } else {
+        const R irho = smat[e * 4 + 1];
 #pragma unroll
-      for (int x = 0; x < 3; ++x)
-        qe[(1 + x) * NPK] = epilogue_q<R>(E, T, base + (1 + x) * NP, accu[x][i] * irho,
-                                          qe[(1 + x) * NPK], re[(1 + x) * NPK]);
+        for (int x = 0; x < 3; ++x)
+          qe[(1 + x) * NPK] = epilogue_q<R>(E, T, base + (1 + x) * NP, acc[x][i] * irho,
+                                            qe[(1 + x) * NPK], re[(1 + x) * NPK]);
+      }
     }
   }
 
