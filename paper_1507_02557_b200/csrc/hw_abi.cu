@@ -80,6 +80,53 @@ static int launch_dense(const hw_mesh_t& M, const hw_fields_t& Q, const Epi& E,
   return check_launch("dense_kernel");
 }
 
+// Per-device side streams for running the element types' kernels
+// concurrently within one stage (env HW_CONCURRENT=0 disables).  Fork/join
+// through events, so the pattern is legal inside CUDA-graph capture.
+struct SideStreams {
+  cudaStream_t s[HW_NTYPES];
+  cudaEvent_t fork_ev, join_ev[HW_NTYPES];
+  int fork(cudaStream_t st0) {
+    cudaError_t e = cudaEventRecord(fork_ev, st0);
+    for (int i = 0; i < HW_NTYPES && e == cudaSuccess; ++i) e = cudaStreamWaitEvent(s[i], fork_ev, 0);
+    if (e != cudaSuccess) return fail((std::string("side stream fork: ") + cudaGetErrorString(e)).c_str());
+    return 0;
+  }
+  int join(cudaStream_t st0, int n) {
+    cudaError_t e = cudaSuccess;
+    for (int i = 0; i < HW_NTYPES && e == cudaSuccess; ++i) {
+      e = cudaEventRecord(join_ev[i], s[i]);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(st0, join_ev[i], 0);
+    }
+    (void)n;
+    if (e != cudaSuccess) return fail((std::string("side stream join: ") + cudaGetErrorString(e)).c_str());
+    return 0;
+  }
+};
+
+static SideStreams* side_streams() {
+  static const bool on = [] {
+    const char* e = getenv("HW_CONCURRENT");
+    return !(e && e[0] == '0');
+  }();
+  if (!on) return nullptr;
+  static std::mutex mu;
+  static SideStreams* per_dev[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  if (!per_dev[dev]) {
+    SideStreams* ss = new SideStreams;
+    bool ok = cudaEventCreateWithFlags(&ss->fork_ev, cudaEventDisableTiming) == cudaSuccess;
+    for (int i = 0; i < HW_NTYPES && ok; ++i)
+      ok = cudaStreamCreateWithFlags(&ss->s[i], cudaStreamNonBlocking) == cudaSuccess &&
+           cudaEventCreateWithFlags(&ss->join_ev[i], cudaEventDisableTiming) == cudaSuccess;
+    if (!ok) return nullptr;
+    per_dev[dev] = ss;
+  }
+  return per_dev[dev];
+}
+
 // shared-memory floor per CTA (bytes, env HW_SMEM_FLOOR; tuning experiments:
 // fewer resident CTAs leave more of the SM's L1 for the operator matrices)
 static size_t smem_floor() {
@@ -141,15 +188,26 @@ static int launch_traces_all(const hw_mesh_t& M, const hw_fields_t& Q, const hw_
 
 template <int N, typename R>
 static int launch_rhs_all(const hw_mesh_t& M, const hw_fields_t& Q, const Epi& E,
-                          const hw_subset_t* sub, cudaStream_t st) {
+                          const hw_subset_t* sub, cudaStream_t st0) {
   int rc = 0;
+  int active[HW_NTYPES], na = 0;
   for (int t = 0; t < HW_NTYPES; ++t) {
+    const int32_t* list;
+    int64_t n = 0;
+    if (M.t[t].K > 0) subset_of(sub, t, M.t[t].K, &list, &n);
+    if (n > 0) active[na++] = t;
+  }
+  SideStreams* ss = na > 1 ? side_streams() : nullptr;
+  if (ss && (rc = ss->fork(st0))) return rc;
+  for (int a = 0; a < na; ++a) {
+    const int t = active[a];
     const int64_t K = M.t[t].K;
-    if (K <= 0) continue;
     const int32_t* list;
     int64_t n;
     subset_of(sub, t, K, &list, &n);
-    if (n <= 0) continue;
+    // the element types are independent within a stage: with side streams
+    // their kernels run concurrently (fills the SMs past each kernel's tail)
+    cudaStream_t st = ss ? ss->s[a] : st0;
     switch (t) {
       case HW_HEX: {
         using L = Smem<N, HW_HEX, R>;
@@ -182,6 +240,7 @@ static int launch_rhs_all(const hw_mesh_t& M, const hw_fields_t& Q, const Epi& E
     }
     if (rc) return rc;
   }
+  if (ss && (rc = ss->join(st0, na))) return rc;
   return 0;
 }
 
