@@ -39,7 +39,10 @@ template <int N>
 struct TetMma {
   using D = Dims<N>;
   static constexpr int NP = D::NP_TET, NFN = D::NFN, NFP = 4 * D::NFN;
-  static constexpr int E = (N == 1) ? 32 : (N <= 4 ? 16 : 8);
+#ifndef HW_TET_E3
+#define HW_TET_E3 8
+#endif
+  static constexpr int E = (N == 1) ? 32 : (N == 3 ? HW_TET_E3 : (N <= 4 ? 16 : 8));
   static constexpr int CT = E / 8;
   static constexpr int RT = (NP + 7) / 8;
   static constexpr int RT8 = RT * 8;
@@ -59,7 +62,7 @@ struct TetMma {
                        SST = SV + E * RA, SRES = SST, SG = SST + E * RB,
                        SMAT = SG + E * GEO_TET, TOTAL = SMAT + E * 4;
   static constexpr size_t BYTES = sizeof(double) * TOTAL + sizeof(int) * (E + E * NFP + NFP);
-  static constexpr int MINB = (W <= 8) ? 3 : 1;
+  static constexpr int MINB = (W <= 4) ? 6 : ((W <= 8) ? 3 : 1);
 };
 
 template <int N>
