@@ -94,6 +94,22 @@ __device__ __forceinline__ void cp_async(R* smem, const R* gmem) {
   else
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem));
 }
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+
+// ne element rows of W scalars (W * sizeof(R) a multiple of 16), element k
+// of the block at src + sk[k] * W, into dst + k * W, 16 bytes per copy
+template <int W, int NTHR, typename R>
+__device__ __forceinline__ void copy_rows16(R* dst, const R* src, const int* sk, int ne) {
+  constexpr int V = 16 / sizeof(R), CH = W / V;
+  for (int i = threadIdx.x; i < ne * CH; i += NTHR) {
+    const int e = i / CH, c = i - e * CH;
+    cp_async16(dst + e * W + c * V, src + (size_t)sk[e] * W + c * V);
+  }
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_all;\n" ::: "memory");
@@ -225,15 +241,16 @@ struct Smem {
   static constexpr int S = (EPB * NP + NT - 1) / NT;
   static constexpr int FLUXW = (T == HW_HEX) ? 4 : 2;       // flux words per face point
   static constexpr int STG = stage_off<N, T>(NF);           // staged values per element
+  // rows copied with 16-byte cp.async first (even sizes keep them aligned)
   static constexpr int SQ = 0;
   static constexpr int SRES = SQ + EPB * 4 * NP;
   static constexpr int SV = SRES + EPB * 4 * NP;
   static constexpr int SF = SV + ((T == HW_HEX) ? 0 : EPB * 3 * NP);
-  static constexpr int SG = SF + EPB * NFP * FLUXW;
-  static constexpr int SMAT = SG + EPB * X::GEO;
-  static constexpr int SST = SMAT + EPB * 4;
+  static constexpr int SST = SF + EPB * NFP * FLUXW;
   static constexpr int STR = SST + EPB * STG;               // own traces (publishing types)
-  static constexpr int SOPS = STR + ((T == HW_TET) ? 0 : EPB * 4 * NFP);  // hex: D1, x, w, Vend
+  static constexpr int SG = STR + ((T == HW_TET) ? 0 : EPB * 4 * NFP);
+  static constexpr int SMAT = SG + EPB * X::GEO;
+  static constexpr int SOPS = SMAT + EPB * 4;               // hex: D1, x, w, Vend
   static constexpr int TOTAL = SOPS + ((T == HW_HEX) ? (N + 1) * (N + 1) + 4 * (N + 1) : 0);
   static constexpr size_t BYTES = sizeof(R) * TOTAL + sizeof(int) * (2 * EPB * NF + EPB);
 };
@@ -548,7 +565,6 @@ __global__ void __launch_bounds__(NT) hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi
   R* sm = reinterpret_cast<R*>(smem_raw);
   int* sk = reinterpret_cast<int*>(sm + L::TOTAL);
   int* snc = sk + EPB;
-  int* sne = snc + EPB * 6;
   R* sq = sm + L::SQ;
   R* sf = sm + L::SF;
   R* sg = sm + L::SG;
@@ -569,7 +585,56 @@ __global__ void __launch_bounds__(NT) hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi
     sw1[tid] = ldg((const R*)TY.op[2] + tid);
     sx[tid] = ldg((const R*)TY.op[4] + tid);
   }
-  prologue<N, HW_HEX, R>(M, Q, E, list, w0, ne, sm, sk, snc, sne);
+  if (tid < ne) sk[tid] = list ? list[w0 + tid] : (int)(w0 + tid);
+  __syncthreads();
+  // group 1 (volume inputs): state rows, records, links
+  copy_rows16<4 * NP, NT>(sq, (const R*)Q.p[HW_HEX], sk, ne);
+  for (int i = tid; i < ne * GEO_HEX; i += NT) {
+    const int e = i / GEO_HEX, r = i - e * GEO_HEX;
+    cp_async(sg + i, (const R*)TY.geo + (size_t)sk[e] * GEO_HEX + r);
+  }
+  for (int i = tid; i < ne * 4; i += NT)
+    cp_async(smat + i, (const R*)TY.mat + (size_t)sk[i >> 2] * 4 + (i & 3));
+  for (int i = tid; i < ne * 6; i += NT)
+    snc[i] = __ldg(TY.nbr_code + (size_t)sk[i / 6] * 6 + i % 6);
+  cp_async_commit();
+  // group 2 (flux / epilogue inputs): own traces (GL), LSRK residual, and the
+  // neighbour values at my face points through the host gather index
+  if (!sem) copy_rows16<4 * NFP, NT>(sm + L::STR, (const R*)M.tr_in[HW_HEX], sk, ne);
+  if (E.mode == MODE_LSRK) copy_rows16<4 * NP, NT>(sm + L::SRES, (const R*)E.res[HW_HEX], sk, ne);
+  {
+    constexpr int IT = (EPB * NFP + NT - 1) / NT;
+    int gv[IT];
+#pragma unroll
+    for (int u = 0; u < IT; ++u) {
+      const int i = tid + u * NT;
+      gv[u] = -1;
+      if (i < ne * NFP) gv[u] = __ldg(TY.iop[2] + (size_t)sk[i / NFP] * NFP + i % NFP);
+    }
+#pragma unroll
+    for (int u = 0; u < IT; ++u) {
+      const int i = tid + u * NT;
+      if (i >= ne * NFP || gv[u] < 0) continue;
+      const int e = i / NFP, j = i - e * NFP;
+      const int t2 = HW_NBR_TYPE(__ldg(TY.nbr_code + (size_t)sk[e] * 6 + j / NFQ));
+      const R* src;
+      int stride;
+      if (publishes(t2, sem)) {
+        src = (const R*)M.tr_in[t2];
+        stride = nfp_of<N>(t2);
+      } else {
+        src = (const R*)Q.p[HW_HEX];
+        stride = NP;
+      }
+      src += gv[u];
+      R* dst = sm + L::SST + e * 4 * NFP + j;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) cp_async(dst + c * NFP, src + c * stride);
+    }
+  }
+  cp_async_commit();
+  asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+  __syncthreads();
 
   R acc[S][4], minv[S];
 #pragma unroll
@@ -673,10 +738,9 @@ __global__ void __launch_bounds__(NT) hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi
     R pp, up[3];
     if (code & HW_NBR_BOUNDARY) {
       pp = -own[0]; up[0] = um[0]; up[1] = um[1]; up[2] = um[2];
-    } else {
-      R tr[4];
-      staged_trace<N, HW_HEX, R>(M, code, f, jj, sm + L::SST + e * L::STG, tr);
-      pp = tr[0]; up[0] = tr[1]; up[1] = tr[2]; up[2] = tr[3];
+    } else {   // neighbour values staged in my point order
+      const R* se = sm + L::SST + e * 4 * NFP + j;
+      pp = se[0]; up[0] = se[NFP]; up[1] = se[2 * NFP]; up[2] = se[3 * NFP];
     }
     R tp, tu, fp, fu;
     penalties(Xv[HX_Z + 2 * f], Xv[HX_Z + 2 * f + 1], pen, tp, tu);

@@ -30,10 +30,6 @@ __host__ __device__ constexpr int stride4mod16(int n) {   // smallest s >= n, s 
   return n + ((4 - n % 16) + 16) % 16;
 }
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
-}
 
 template <int N>
 struct TetMma {

@@ -255,7 +255,7 @@ def tet_gather_index(mesh, dops, perm_tri, face_offsets):
 
 
 def face_gather_index(mesh, t, dops_all, perm_tri, perm_quad, face_offsets, N, sem):
-    """(K, Nfp) int32 for the wedge / pyramid kernels: for each of my face
+    """(K, Nfp) int32 for the hex / wedge / pyramid kernels: for each of my face
     points (device order, hybridwave/dg.py:258-300 neighbour trace, already
     permuted into my point order) the field-0 offset of the coincident
     neighbour value in its source array; the source (and its field stride)
@@ -301,7 +301,8 @@ def face_gather_index(mesh, t, dops_all, perm_tri, perm_quad, face_offsets, N, s
 def _pack_iops(t, d, N, mesh=None, perm_tri=None, face_offsets=None, dops_all=None,
                perm_quad=None, sem=False):
     if t == "hex":
-        return {0: d["face_tab"], 1: hex_node_face_points(d, N)}
+        return {0: d["face_tab"], 1: hex_node_face_points(d, N),
+                2: face_gather_index(mesh, t, dops_all, perm_tri, perm_quad, face_offsets, N, sem)}
     if t == "tet":
         return {0: d["face_nodes"], 1: tet_gather_index(mesh, d, perm_tri, face_offsets)}
     return {1: face_gather_index(mesh, t, dops_all, perm_tri, perm_quad, face_offsets, N, sem)}

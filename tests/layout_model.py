@@ -141,11 +141,11 @@ def rhs(pack, disc, state):
                 cols = off2[:, None] + perm
                 tr2 = traces[t2][k2[sel]]                                      # (n,4,nfp2)
                 oth[sel] = np.take_along_axis(tr2, np.repeat(cols[:, None, :], 4, axis=1), axis=2)
-                if t in ("wedge", "pyramid"):
+                if t in ("wedge", "pyramid", "hex"):
                     # the kernels' path: host gather index into the source array
                     direct = t2 in ("hex", "tet") and (t2 == "tet" or sem)
                     src = q[t2] if direct else traces[t2]
-                    g = P["iop"][1][sel, off:off + cnt]
+                    g = P["iop"][2 if t == "hex" else 1][sel, off:off + cnt]
                     got = np.stack([src.reshape(-1)[g + c * src.shape[2]] for c in range(4)],
                                    axis=1)
                     assert np.array_equal(got, oth[sel]), (t, f, t2)
