@@ -191,7 +191,11 @@ static int launch_rhs_all(const hw_mesh_t& M, const hw_fields_t& Q, const Epi& E
                           const hw_subset_t* sub, cudaStream_t st0) {
   int rc = 0;
   int active[HW_NTYPES], na = 0;
-  for (int t = 0; t < HW_NTYPES; ++t) {
+  // longest kernels first (tet, wedge, hex, pyramid): the short ones fill
+  // the SMs the long ones leave idle in their tails
+  static const int order[HW_NTYPES] = {HW_TET, HW_WEDGE, HW_HEX, HW_PYRAMID};
+  for (int o = 0; o < HW_NTYPES; ++o) {
+    const int t = order[o];
     const int32_t* list;
     int64_t n = 0;
     if (M.t[t].K > 0) subset_of(sub, t, M.t[t].K, &list, &n);
