@@ -150,18 +150,17 @@ __global__ void __launch_bounds__(TetMma<N>::NTH, TetMma<N>::MINB)
     const int e = i / NFP, j = i - e * NFP;
     const int g = sgi[i];
     if (g == -1) continue;
-    const int f = j / NFN, jj = j - f * NFN;
-    R* dst = sst + e * L::RB + f * 4 * NFN + jj;
+    R* dst = sst + e * L::RB + j;            // [field][face point]: conflict-free
     if (g >= 0) {
 #pragma unroll
-      for (int c = 0; c < 4; ++c) cp_async(dst + c * NFN, q + (size_t)g + c * NP);
+      for (int c = 0; c < 4; ++c) cp_async(dst + c * NFP, q + (size_t)g + c * NP);
     } else {   // pyramid / wedge neighbour: its published face trace
       const unsigned v = (unsigned)(-3 - g);
       const int t2 = (v & 1u) ? HW_WEDGE : HW_PYRAMID;
       const int nfp2 = (v & 1u) ? Dims<N>::NFP_WEDGE : Dims<N>::NFP_PYR;
       const R* src = (const R*)M.tr_in[t2] + (size_t)(v >> 1);
 #pragma unroll
-      for (int c = 0; c < 4; ++c) cp_async(dst + c * NFN, src + c * nfp2);
+      for (int c = 0; c < 4; ++c) cp_async(dst + c * NFP, src + c * nfp2);
     }
   }
   cp_async_commit();
@@ -221,8 +220,8 @@ __global__ void __launch_bounds__(TetMma<N>::NTH, TetMma<N>::MINB)
     const int gi = sgi[i];
     R pp, up[3];
     if (gi != -1) {
-      const R* s = sst + e * L::RB + f * 4 * NFN + jj;
-      pp = s[0]; up[0] = s[NFN]; up[1] = s[2 * NFN]; up[2] = s[3 * NFN];
+      const R* s = sst + e * L::RB + j;
+      pp = s[0]; up[0] = s[NFP]; up[1] = s[2 * NFP]; up[2] = s[3 * NFP];
     } else {
       pp = -pm; up[0] = um[0]; up[1] = um[1]; up[2] = um[2];
     }
