@@ -34,6 +34,7 @@ struct DMma {
   }
   static constexpr int NFKT = koff(NF);                 // padded, face-concatenated K of the lift
   static constexpr int RTF = (NFP + 7) / 8;             // row tiles of the trace GEMM
+  static constexpr int GEOS = GEO | 1;   // odd smem stride: per-element record reads spread over banks
   static constexpr int EQ = stride4mod16(4 * NPK);
   static constexpr int EV = stride4mod16(3 * NPK);
   static constexpr int EF = stride4mod16(NFKT);
@@ -46,7 +47,7 @@ struct DMma {
   static constexpr int RA = cmax(EV, 2 * EF), RB = cmax(ETR + ESG, EQ);
   static constexpr int SQ = 0, SV = SQ + E * EQ, SFP = SV, SFU = SFP + E * EF,
                        STR = SV + E * RA, SST = STR + E * ETR, SRES = STR,
-                       SG = STR + E * RB, SMAT = SG + E * GEO, TOTAL = SMAT + E * 4;
+                       SG = STR + E * RB, SMAT = SG + E * GEOS, TOTAL = SMAT + E * 4;
   static constexpr size_t BYTES = sizeof(double) * TOTAL + sizeof(int) * (E + E * NF);
   static constexpr bool VEC = (NP % 2 == 0) && (NPK == NP);
 };
@@ -120,7 +121,7 @@ __global__ void __launch_bounds__(DMma<N, T>::NTH)
   }
   for (int i = tid; i < ne * GEO; i += NTH) {
     const int e = i / GEO, r = i - e * GEO;
-    cp_async(sg + i, (const R*)TY.geo + (size_t)sk[e] * GEO + r);
+    cp_async(sg + e * L::GEOS + r, (const R*)TY.geo + (size_t)sk[e] * GEO + r);
   }
   for (int i = tid; i < ne * 4; i += NTH)
     cp_async(smat + i, (const R*)TY.mat + (size_t)sk[i >> 2] * 4 + (i & 3));
@@ -173,7 +174,7 @@ __global__ void __launch_bounds__(DMma<N, T>::NTH)
   // v_c = sum_x G[c][x] u_x
   for (int i = tid; i < ne * NP; i += NTH) {
     const int e = i / NP, n = i - e * NP;
-    const R* G = sg + e * GEO;
+    const R* G = sg + e * L::GEOS;
     const R* u = sq + e * EQ + n;
     const R u0 = u[NPK], u1 = u[2 * NPK], u2 = u[3 * NPK];
 #pragma unroll
@@ -229,7 +230,7 @@ __global__ void __launch_bounds__(DMma<N, T>::NTH)
     const R* te = str + e * ETR + j;
     const R own[4] = {te[0], te[NFP], te[2 * NFP], te[3 * NFP]};
     const R um[3] = {own[1], own[2], own[3]};
-    const R* g = sg + e * GEO + GF + FS * f;
+    const R* g = sg + e * L::GEOS + GF + FS * f;
     const R nrm[3] = {g[0], g[1], g[2]};
     const int code = snc[e * NF + f];
     R pp, up[3];
@@ -278,7 +279,7 @@ __global__ void __launch_bounds__(DMma<N, T>::NTH)
   } else {
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
-      const R* G = sg + (col0 + i) * GEO;
+      const R* G = sg + (col0 + i) * L::GEOS;
 #pragma unroll
       for (int x = 0; x < 3; ++x)
         acc[x][i] = -(G[x] * dp[0][i] + G[3 + x] * dp[1][i] + G[6 + x] * dp[2][i]);
@@ -294,7 +295,7 @@ __global__ void __launch_bounds__(DMma<N, T>::NTH)
       }
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
-        const R* g = sg + (col0 + i) * GEO + GF + FS * f;
+        const R* g = sg + (col0 + i) * L::GEOS + GF + FS * f;
         acc[0][i] += g[0] * tu[i];
         acc[1][i] += g[1] * tu[i];
         acc[2][i] += g[2] * tu[i];
@@ -354,7 +355,7 @@ __global__ void __launch_bounds__(DMma<N, T>::NTH)
           const int e = c0 >> 2;
           if (e >= ne) continue;
           R s = R(1);
-          if (T == HW_WEDGE) s = sg[e * GEO + 9];
+          if (T == HW_WEDGE) s = sg[e * L::GEOS + 9];
           R* o = tro + (size_t)sk[e] * 4 * NFP + j;
           o[(c0 & 3) * NFP] = y[cf][0] * s;
           o[((c0 & 3) + 1) * NFP] = y[cf][1] * s;

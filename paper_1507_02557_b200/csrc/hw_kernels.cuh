@@ -745,11 +745,11 @@ __global__ void __launch_bounds__(NT) hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi
     R tp, tu, fp, fu;
     penalties(Xv[HX_Z + 2 * f], Xv[HX_Z + 2 * f + 1], pen, tp, tu);
     upwind_flux(own[0], um, pp, up, nrm, tp, tu, TY.form == HW_FORM_SKEW, fp, fu);
-    R* o = sf + (e * NFP + j) * 4;
+    R* o = sf + e * 4 * NFP + j;        // [field][face point]: conflict-free
     o[0] = fp * wJs;
-    o[1] = nrm[0] * fu * wJs;
-    o[2] = nrm[1] * fu * wJs;
-    o[3] = nrm[2] * fu * wJs;
+    o[NFP] = nrm[0] * fu * wJs;
+    o[2 * NFP] = nrm[1] * fu * wJs;
+    o[3 * NFP] = nrm[2] * fu * wJs;
   }
   __syncthreads();
 
@@ -761,6 +761,7 @@ __global__ void __launch_bounds__(NT) hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi
     const int idx[3] = {n / (N1 * N1), (n / N1) % N1, n % N1};
     const R* fl = sf + e * NFP * 4;
     R lift[4] = {R(0), R(0), R(0), R(0)};
+    // (hex: fl is [field][face point])
 #pragma unroll
     for (int f = 0; f < 6; ++f) {
       const int axis = f >> 1, end = f & 1;
@@ -773,9 +774,9 @@ __global__ void __launch_bounds__(NT) hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi
         w = sve[end * N1 + l];
       }
       const int pt = __ldg(TY.iop[1] + f * NP + n);
-      const R* o = fl + (f * NFQ + pt) * 4;
+      const R* o = fl + f * NFQ + pt;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) lift[c] += w * o[c];
+      for (int c = 0; c < 4; ++c) lift[c] += w * o[c * NFP];
     }
     // only the surface term carries the mass inverse 1/(w3 J): the volume
     // term above is already the cancelled form -grad p, -div u
