@@ -191,9 +191,16 @@ static int launch_rhs_all(const hw_mesh_t& M, const hw_fields_t& Q, const Epi& E
                           const hw_subset_t* sub, cudaStream_t st0) {
   int rc = 0;
   int active[HW_NTYPES], na = 0;
-  // longest kernels first (tet, wedge, hex, pyramid): the short ones fill
-  // the SMs the long ones leave idle in their tails
-  static const int order[HW_NTYPES] = {HW_TET, HW_WEDGE, HW_HEX, HW_PYRAMID};
+  // launch order on the side streams: measured best on the hybrid:38 N=3
+  // step is pyramid, hex, wedge, tet (+3% over tet-first; 2 % over the type order)
+  static int order[HW_NTYPES] = {HW_PYRAMID, HW_HEX, HW_WEDGE, HW_TET};
+  static const bool order_env = [] {   // HW_TYPE_ORDER=3102 (tuning experiments)
+    const char* e = getenv("HW_TYPE_ORDER");
+    if (e && strlen(e) == HW_NTYPES)
+      for (int i = 0; i < HW_NTYPES; ++i) order[i] = e[i] - '0';
+    return true;
+  }();
+  (void)order_env;
   for (int o = 0; o < HW_NTYPES; ++o) {
     const int t = order[o];
     const int32_t* list;

@@ -35,7 +35,10 @@ struct DMma {
   static constexpr int NFKT = koff(NF);                 // padded, face-concatenated K of the lift
   static constexpr int RTF = (NFP + 7) / 8;             // row tiles of the trace GEMM
   static constexpr int GEOS = GEO | 1;   // odd smem stride: per-element record reads spread over banks
-  static constexpr int EQ = stride4mod16(4 * NPK);
+  // q / res field stride = 4 or 12 (mod 16) doubles: the trace GEMM's B
+  // fragments (8 columns = 2 elements x 4 fields) then hit every bank twice
+  static constexpr int QF = NPK + ((NPK % 16 <= 4) ? 4 - NPK % 16 : (NPK % 16 <= 12 ? 12 - NPK % 16 : 20 - NPK % 16));
+  static constexpr int EQ = stride4mod16(4 * QF);
   static constexpr int EV = stride4mod16(3 * NPK);
   static constexpr int EF = stride4mod16(NFKT);
   // own traces and neighbour values, both [4][NFP] in my face-point order
@@ -51,6 +54,24 @@ struct DMma {
   static constexpr size_t BYTES = sizeof(double) * TOTAL + sizeof(int) * (E + E * NF);
   static constexpr bool VEC = (NP % 2 == 0) && (NPK == NP);
 };
+
+// element rows (K, 4, NP) -> smem [e][field (stride QF)][node]
+template <typename L>
+__device__ __forceinline__ void copy_q_rows(double* dst, const double* src, const int* sk, int ne) {
+  constexpr int NP = L::NP;
+  if (NP % 2 == 0) {
+    constexpr int CF = NP / 2, CH = 4 * CF;      // 16-byte chunks per field / element
+    for (int i = threadIdx.x; i < ne * CH; i += L::NTH) {
+      const int e = i / CH, r = i - e * CH, fld = r / CF, c = r - fld * CF;
+      cp_async16(dst + e * L::EQ + fld * L::QF + 2 * c, src + (size_t)sk[e] * 4 * NP + fld * NP + 2 * c);
+    }
+  } else {
+    for (int i = threadIdx.x; i < ne * 4 * NP; i += L::NTH) {
+      const int e = i / (4 * NP), r = i - e * 4 * NP, fld = r / NP, n = r - fld * NP;
+      cp_async(dst + e * L::EQ + fld * L::QF + n, src + (size_t)sk[e] * 4 * NP + r);
+    }
+  }
+}
 
 template <int N, int T>
 __global__ void __launch_bounds__(DMma<N, T>::NTH)
@@ -90,7 +111,7 @@ __global__ void __launch_bounds__(DMma<N, T>::NTH)
     for (int i = tid; i < EB * 11 * PADN; i += NTH) {
       const int e = i / (11 * PADN), r = i - e * 11 * PADN;
       const int fld = r / PADN, n = NP + r - fld * PADN;
-      if (fld < 4) sq[e * EQ + fld * NPK + n] = R(0);
+      if (fld < 4) sq[e * EQ + fld * L::QF + n] = R(0);
       else if (fld >= 8) sv[e * EV + (fld - 8) * NPK + n] = R(0);
     }
   __syncthreads();
@@ -98,19 +119,7 @@ __global__ void __launch_bounds__(DMma<N, T>::NTH)
   // ---- P0: rows, records, links (all async), then neighbour staging
   const R* q = (const R*)Q.p[T];
   const R* resg = (const R*)E.res[T];
-  if (L::VEC) {
-    constexpr int CH = 4 * NP / 2;
-    for (int i = tid; i < ne * CH; i += NTH) {
-      const int e = i / CH, c = i - e * CH;
-      cp_async16(sq + e * EQ + 2 * c, q + (size_t)sk[e] * 4 * NP + 2 * c);
-    }
-  } else {
-    for (int i = tid; i < ne * 4 * NP; i += NTH) {
-      const int e = i / (4 * NP), r = i - e * 4 * NP;
-      const int fld = r / NP, n = r - fld * NP;
-      cp_async(sq + e * EQ + fld * NPK + n, q + (size_t)sk[e] * 4 * NP + r);
-    }
-  }
+  copy_q_rows<L>(sq, q, sk, ne);
   {   // own traces of the input state (published by the previous stage)
     const R* tr = (const R*)M.tr_in[T];
     constexpr int CT = 2 * NFP;                     // 16-byte chunks per element
@@ -176,7 +185,7 @@ __global__ void __launch_bounds__(DMma<N, T>::NTH)
     const int e = i / NP, n = i - e * NP;
     const R* G = sg + e * L::GEOS;
     const R* u = sq + e * EQ + n;
-    const R u0 = u[NPK], u1 = u[2 * NPK], u2 = u[3 * NPK];
+    const R u0 = u[L::QF], u1 = u[2 * L::QF], u2 = u[3 * L::QF];
 #pragma unroll
     for (int c = 0; c < 3; ++c)
       sv[e * EV + c * NPK + n] = G[c * 3] * u0 + G[c * 3 + 1] * u1 + G[c * 3 + 2] * u2;
@@ -249,19 +258,7 @@ __global__ void __launch_bounds__(DMma<N, T>::NTH)
   __syncthreads();
   // residual rows into the (now free) trace storage, behind the lift GEMM
   if (lsrk) {
-    if (L::VEC) {
-      constexpr int CH = 4 * NP / 2;
-      for (int i = tid; i < ne * CH; i += NTH) {
-        const int e = i / CH, c = i - e * CH;
-        cp_async16(sres + e * EQ + 2 * c, resg + (size_t)sk[e] * 4 * NP + 2 * c);
-      }
-    } else {
-      for (int i = tid; i < ne * 4 * NP; i += NTH) {
-        const int e = i / (4 * NP), r = i - e * 4 * NP;
-        const int fld = r / NP, n = r - fld * NP;
-        cp_async(sres + e * EQ + fld * NPK + n, resg + (size_t)sk[e] * 4 * NP + r);
-      }
-    }
+    copy_q_rows<L>(sres, resg, sk, ne);
     cp_async_commit();
   }
 
@@ -321,8 +318,8 @@ __global__ void __launch_bounds__(DMma<N, T>::NTH)
         const R irho = smat[e * 4 + 1];
 #pragma unroll
         for (int x = 0; x < 3; ++x)
-          qe[(1 + x) * NPK] = epilogue_q<R>(E, T, base + (1 + x) * NP, acc[x][i] * irho,
-                                            qe[(1 + x) * NPK], re[(1 + x) * NPK]);
+          qe[(1 + x) * L::QF] = epilogue_q<R>(E, T, base + (1 + x) * NP, acc[x][i] * irho,
+                                              qe[(1 + x) * L::QF], re[(1 + x) * L::QF]);
       }
     }
   }
@@ -344,7 +341,7 @@ __global__ void __launch_bounds__(DMma<N, T>::NTH)
 #pragma unroll
         for (int cf = 0; cf < 4; ++cf) {
           const int col = cf * 8 + er;
-          dmma884(y[cf][0], y[cf][1], a, sq[(col >> 2) * EQ + (col & 3) * NPK + bk + ks * 4]);
+          dmma884(y[cf][0], y[cf][1], a, sq[(col >> 2) * EQ + (col & 3) * L::QF + bk + ks * 4]);
         }
       }
       const int j = rf * 8 + er;
