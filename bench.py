@@ -383,13 +383,15 @@ def mrab_bench(args, disc, mesh, host_state, dev, setup_s):
     drv = MRABDriver(disc, plan)
     macro = 2 ** (L - 1) * plan.dt_min
     q = disc.to_device(host_state)
-    drv.run(q, macro * args.warmup)
+    graph = not args.no_graph
+    drv.run(q, macro * args.warmup, graph=graph)
+    drv.run(q, macro * args.steps, graph=graph)      # same T: captures the replay graph
     torch.cuda.synchronize()
     stream = torch.cuda.current_stream(dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
         e0.record(stream)
-        drv.run(q, macro * args.steps)
+        drv.run(q, macro * args.steps, graph=graph)
         e1.record(stream)
         torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
