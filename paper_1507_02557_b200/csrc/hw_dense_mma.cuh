@@ -60,9 +60,13 @@ template <typename L>
 __device__ __forceinline__ void copy_q_rows(double* dst, const double* src, const int* sk, int ne) {
   constexpr int NP = L::NP;
   if (NP % 2 == 0) {
-    constexpr int CF = NP / 2, CH = 4 * CF;      // 16-byte chunks per field / element
-    for (int i = threadIdx.x; i < ne * CH; i += L::NTH) {
+    constexpr int CF = NP / 2, CH = 4 * CF, TOT = L::E * CH;   // 16-byte chunks
+#pragma unroll
+    for (int u = 0; u < (TOT + L::NTH - 1) / L::NTH; ++u) {
+      const int i = (int)threadIdx.x + u * L::NTH;
+      if ((TOT % L::NTH) && i >= TOT) break;
       const int e = i / CH, r = i - e * CH, fld = r / CF, c = r - fld * CF;
+      if (e >= ne) break;
       cp_async16(dst + e * L::EQ + fld * L::QF + 2 * c, src + (size_t)sk[e] * 4 * NP + fld * NP + 2 * c);
     }
   } else {
@@ -121,19 +125,10 @@ __global__ void __launch_bounds__(DMma<N, T>::NTH)
   const R* resg = (const R*)E.res[T];
   copy_q_rows<L>(sq, q, sk, ne);
   {   // own traces of the input state (published by the previous stage)
-    const R* tr = (const R*)M.tr_in[T];
-    constexpr int CT = 2 * NFP;                     // 16-byte chunks per element
-    for (int i = tid; i < ne * CT; i += NTH) {
-      const int e = i / CT, c = i - e * CT;
-      cp_async16(str + e * ETR + 2 * c, tr + (size_t)sk[e] * 4 * NFP + 2 * c);
-    }
+    copy_rows16<4 * NFP, ETR, NTH, EB>(str, (const R*)M.tr_in[T], sk, ne);
   }
-  for (int i = tid; i < ne * GEO; i += NTH) {
-    const int e = i / GEO, r = i - e * GEO;
-    cp_async(sg + e * L::GEOS + r, (const R*)TY.geo + (size_t)sk[e] * GEO + r);
-  }
-  for (int i = tid; i < ne * 4; i += NTH)
-    cp_async(smat + i, (const R*)TY.mat + (size_t)sk[i >> 2] * 4 + (i & 3));
+  copy_rows<GEO, L::GEOS, NTH, EB>(sg, (const R*)TY.geo, sk, ne);
+  copy_rows<4, 4, NTH, EB>(smat, (const R*)TY.mat, sk, ne);
   for (int i = tid; i < ne * NF; i += NTH)
     snc[i] = __ldg(TY.nbr_code + (size_t)sk[i / NF] * NF + i % NF);
   cp_async_commit();

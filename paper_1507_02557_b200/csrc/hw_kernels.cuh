@@ -100,14 +100,33 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
 }
 
-// ne element rows of W scalars (W * sizeof(R) a multiple of 16), element k
-// of the block at src + sk[k] * W, into dst + k * W, 16 bytes per copy
-template <int W, int NTHR, typename R>
+// ne (<= EMAX) element rows of W scalars (W * sizeof(R) a multiple of 16),
+// element k of the block at src + sk[k] * W, into dst + k * DW; 16 bytes
+// per copy, loop fully unrolled over the compile-time trip count
+template <int W, int DW, int NTHR, int EMAX, typename R>
 __device__ __forceinline__ void copy_rows16(R* dst, const R* src, const int* sk, int ne) {
-  constexpr int V = 16 / sizeof(R), CH = W / V;
-  for (int i = threadIdx.x; i < ne * CH; i += NTHR) {
+  constexpr int V = 16 / sizeof(R), CH = W / V, TOT = EMAX * CH;
+#pragma unroll
+  for (int u = 0; u < (TOT + NTHR - 1) / NTHR; ++u) {
+    const int i = (int)threadIdx.x + u * NTHR;
+    if ((TOT % NTHR) && i >= TOT) break;
     const int e = i / CH, c = i - e * CH;
-    cp_async16(dst + e * W + c * V, src + (size_t)sk[e] * W + c * V);
+    if (e >= ne) break;
+    cp_async16(dst + e * DW + c * V, src + (size_t)sk[e] * W + c * V);
+  }
+}
+
+// the same with one scalar per copy (rows of odd length, e.g. records)
+template <int W, int DW, int NTHR, int EMAX, typename R>
+__device__ __forceinline__ void copy_rows(R* dst, const R* src, const int* sk, int ne) {
+  constexpr int TOT = EMAX * W;
+#pragma unroll
+  for (int u = 0; u < (TOT + NTHR - 1) / NTHR; ++u) {
+    const int i = (int)threadIdx.x + u * NTHR;
+    if ((TOT % NTHR) && i >= TOT) break;
+    const int e = i / W, c = i - e * W;
+    if (e >= ne) break;
+    cp_async(dst + e * DW + c, src + (size_t)sk[e] * W + c);
   }
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
@@ -588,20 +607,17 @@ __global__ void __launch_bounds__(NT) hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi
   if (tid < ne) sk[tid] = list ? list[w0 + tid] : (int)(w0 + tid);
   __syncthreads();
   // group 1 (volume inputs): state rows, records, links
-  copy_rows16<4 * NP, NT>(sq, (const R*)Q.p[HW_HEX], sk, ne);
-  for (int i = tid; i < ne * GEO_HEX; i += NT) {
-    const int e = i / GEO_HEX, r = i - e * GEO_HEX;
-    cp_async(sg + i, (const R*)TY.geo + (size_t)sk[e] * GEO_HEX + r);
-  }
-  for (int i = tid; i < ne * 4; i += NT)
-    cp_async(smat + i, (const R*)TY.mat + (size_t)sk[i >> 2] * 4 + (i & 3));
+  copy_rows16<4 * NP, 4 * NP, NT, EPB>(sq, (const R*)Q.p[HW_HEX], sk, ne);
+  copy_rows<GEO_HEX, GEO_HEX, NT, EPB>(sg, (const R*)TY.geo, sk, ne);
+  copy_rows<4, 4, NT, EPB>(smat, (const R*)TY.mat, sk, ne);
   for (int i = tid; i < ne * 6; i += NT)
     snc[i] = __ldg(TY.nbr_code + (size_t)sk[i / 6] * 6 + i % 6);
   cp_async_commit();
   // group 2 (flux / epilogue inputs): own traces (GL), LSRK residual, and the
   // neighbour values at my face points through the host gather index
-  if (!sem) copy_rows16<4 * NFP, NT>(sm + L::STR, (const R*)M.tr_in[HW_HEX], sk, ne);
-  if (E.mode == MODE_LSRK) copy_rows16<4 * NP, NT>(sm + L::SRES, (const R*)E.res[HW_HEX], sk, ne);
+  if (!sem) copy_rows16<4 * NFP, 4 * NFP, NT, EPB>(sm + L::STR, (const R*)M.tr_in[HW_HEX], sk, ne);
+  if (E.mode == MODE_LSRK)
+    copy_rows16<4 * NP, 4 * NP, NT, EPB>(sm + L::SRES, (const R*)E.res[HW_HEX], sk, ne);
   {
     constexpr int IT = (EPB * NFP + NT - 1) / NT;
     int gv[IT];

@@ -107,11 +107,7 @@ __global__ void __launch_bounds__(TetMma<N>::NTH, TetMma<N>::MINB)
   const R* q = (const R*)Q.p[HW_TET];
   const R* resg = (const R*)E.res[HW_TET];
   if (L::VEC) {
-    constexpr int CH = 4 * NP / 2;                  // 16-byte chunks per element row
-    for (int i = tid; i < ne * CH; i += NTH) {
-      const int e = i / CH, c = i - e * CH;
-      cp_async16(sq + e * EQ + 2 * c, q + (size_t)sk[e] * 4 * NP + 2 * c);
-    }
+    copy_rows16<4 * NP, EQ, NTH, EB>(sq, q, sk, ne);
   } else {
     for (int i = tid; i < ne * 4 * NP; i += NTH) {
       const int e = i / (4 * NP), r = i - e * 4 * NP;
@@ -119,28 +115,12 @@ __global__ void __launch_bounds__(TetMma<N>::NTH, TetMma<N>::MINB)
       cp_async(sq + e * EQ + fld * NPK + n, q + (size_t)sk[e] * 4 * NP + r);
     }
   }
-  for (int i = tid; i < ne * GEO_TET; i += NTH) {
-    const int e = i / GEO_TET, r = i - e * GEO_TET;
-    cp_async(sg + i, (const R*)TY.geo + (size_t)sk[e] * GEO_TET + r);
-  }
-  for (int i = tid; i < ne * 4; i += NTH)
-    cp_async(smat + i, (const R*)TY.mat + (size_t)sk[i >> 2] * 4 + (i & 3));
-  {
-    constexpr int CI = NFP / 4;                      // 16-byte chunks of gather ints
-    if (NFP % 4 == 0) {
-      for (int i = tid; i < ne * CI; i += NTH) {
-        const int e = i / CI, c = i - e * CI;
-        cp_async16(sgi + e * NFP + 4 * c, TY.iop[1] + (size_t)sk[e] * NFP + 4 * c);
-      }
-    } else {
-      for (int i = tid; i < ne * NFP; i += NTH) {
-        const int e = i / NFP, r = i - e * NFP;
-        const unsigned s = (unsigned)__cvta_generic_to_shared(sgi + i);
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s),
-                     "l"(TY.iop[1] + (size_t)sk[e] * NFP + r));
-      }
-    }
-  }
+  copy_rows<GEO_TET, GEO_TET, NTH, EB>(sg, (const R*)TY.geo, sk, ne);
+  copy_rows<4, 4, NTH, EB>(smat, (const R*)TY.mat, sk, ne);
+  if (NFP % 4 == 0)   // gather ints
+    copy_rows16<NFP, NFP, NTH, EB>(sgi, TY.iop[1], sk, ne);
+  else
+    copy_rows<NFP, NFP, NTH, EB>(sgi, TY.iop[1], sk, ne);
   cp_async_commit();
   asm volatile("cp.async.wait_group 0;\n" ::: "memory");
   __syncthreads();
