@@ -39,15 +39,17 @@ enum { HW_GL = 0, HW_SEM = 1 };
 /* One element type present in the mesh.  Geometry record per element
  * (scalar type = dtype); dense types carry per face FS = 6 words (n_x, n_y,
  * n_z, Jacobian scale, avg(rho c), 1/avg(rho c)):
- *   hex      71: 8 vertices (x, y, z); per face (avg, 1/avg); affine flag;
- *                if affine: G[3][3], J, per face (n_x, n_y, n_z, Js)
+ *   hex      72: 8 vertices (x, y, z); per face (avg, 1/avg); affine flag;
+ *                if affine: G[3][3], J, per face (n_x, n_y, n_z, Js), 1/J
  *   wedge    40: G[3][3] (G[c][x] = d r_c / d x_x), 1/sqrt(J), 5 faces x FS
  *                (scale = Js/sqrt(J))
  *   pyramid  39: G[3][3], 5 faces x FS (scale = Js/J)
  *   tet      33: G[3][3], 4 faces x FS (scale = Js/J)
  * mat: per element (kappa, 1/rho, rho*c, 0).
- * op/iop: constant operators, layouts documented in
- *   paper_1507_02557_b200/dg.py (_pack_type_operators). */
+ * op/iop: constant operators and index tables, layouts documented in
+ *   paper_1507_02557_b200/device.py (_pack_ops, _mma_ops, _pack_iops):
+ *   iop hex {0 face table, 1 node->face point, 2 face gather index},
+ *   tet {0 face nodes, 1 gather index}, wedge/pyramid {1 gather index}. */
 typedef struct {
   int64_t K;
   const void* geo;

@@ -29,9 +29,9 @@ struct Dims {
 // avg(rho c), 1/avg(rho c)).  Hex: 8 vertices, per face (avg, 1/avg), an
 // affine flag, then for affine hexes G[3][3], J and per face (n, Js).
 constexpr int FS = 6;
-constexpr int GEO_HEX = 71, GEO_WEDGE = 10 + 5 * FS, GEO_PYR = 9 + 5 * FS,
+constexpr int GEO_HEX = 72, GEO_WEDGE = 10 + 5 * FS, GEO_PYR = 9 + 5 * FS,
               GEO_TET = 9 + 4 * FS;
-constexpr int HX_Z = 24, HX_AFF = 36, HX_G = 37, HX_J = 46, HX_F = 47;
+constexpr int HX_Z = 24, HX_AFF = 36, HX_G = 37, HX_J = 46, HX_F = 47, HX_IJ = 71;
 constexpr int NF_HEX = 6, NF_WEDGE = 5, NF_PYR = 5, NF_TET = 4;
 
 // epilogue of the fused RHS kernels

@@ -269,9 +269,11 @@ struct Smem {
   static constexpr int STR = SST + EPB * STG;               // own traces (publishing types)
   static constexpr int SG = STR + ((T == HW_TET) ? 0 : EPB * 4 * NFP);
   static constexpr int SMAT = SG + EPB * X::GEO;
-  static constexpr int SOPS = SMAT + EPB * 4;               // hex: D1, x, w, Vend
-  static constexpr int TOTAL = SOPS + ((T == HW_HEX) ? (N + 1) * (N + 1) + 4 * (N + 1) : 0);
-  static constexpr size_t BYTES = sizeof(R) * TOTAL + sizeof(int) * (2 * EPB * NF + EPB);
+  static constexpr int SOPS = SMAT + EPB * 4;   // hex: D1, x, w, Vend, 1/(w_i w_j w_k)
+  static constexpr int TOTAL = SOPS + ((T == HW_HEX) ? (N + 1) * (N + 1) + 4 * (N + 1) + NP : 0);
+  // ints: element ids, links (x2); hex: node -> face point table (6 x NP)
+  static constexpr size_t BYTES =
+      sizeof(R) * TOTAL + sizeof(int) * (2 * EPB * NF + EPB + ((T == HW_HEX) ? 6 * NP : 0));
 };
 
 template <int N, int T, typename R>
@@ -584,6 +586,7 @@ __global__ void __launch_bounds__(NT) hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi
   R* sm = reinterpret_cast<R*>(smem_raw);
   int* sk = reinterpret_cast<int*>(sm + L::TOTAL);
   int* snc = sk + EPB;
+  int* spt = snc + 2 * EPB * 6;  // node -> face point (6 x NP)
   R* sq = sm + L::SQ;
   R* sf = sm + L::SF;
   R* sg = sm + L::SG;
@@ -592,6 +595,7 @@ __global__ void __launch_bounds__(NT) hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi
   R* sx = sD + N1 * N1;          // 1-D nodes
   R* sw1 = sx + N1;              // 1-D weights
   R* sve = sw1 + N1;             // endpoint rows (2 x N1)
+  R* siw3 = sve + 2 * N1;        // 1 / (w_i w_j w_k) per node
 
   const hw_type_t& TY = M.t[HW_HEX];
   const bool sem = M.formulation == HW_SEM;
@@ -604,6 +608,11 @@ __global__ void __launch_bounds__(NT) hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi
     sw1[tid] = ldg((const R*)TY.op[2] + tid);
     sx[tid] = ldg((const R*)TY.op[4] + tid);
   }
+  for (int i = tid; i < NP; i += NT) {
+    const R* w = (const R*)TY.op[2];
+    siw3[i] = R(1) / (ldg(w + i / (N1 * N1)) * ldg(w + (i / N1) % N1) * ldg(w + i % N1));
+  }
+  for (int i = tid; i < 6 * NP; i += NT) spt[i] = __ldg(TY.iop[1] + i);
   if (tid < ne) sk[tid] = list ? list[w0 + tid] : (int)(w0 + tid);
   __syncthreads();
   // group 1 (volume inputs): state rows, records, links
@@ -676,14 +685,14 @@ __global__ void __launch_bounds__(NT) hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi
         d[f][0] = a0; d[f][1] = a1; d[f][2] = a2;
       }
       R G[9];
-      R J;
+      R iJ;
       const R* Xe = sg + e * GEO_HEX;
       if (Xe[HX_AFF] != R(0)) {       // affine: constant metric from the record
 #pragma unroll
         for (int a = 0; a < 9; ++a) G[a] = Xe[HX_G + a];
-        J = Xe[HX_J];
+        iJ = Xe[HX_IJ];
       } else {
-        J = hex_metric<R>(Xe, sx[ii], sx[jj], sx[kk], G);
+        iJ = R(1) / hex_metric<R>(Xe, sx[ii], sx[jj], sx[kk], G);
       }
       R div = R(0);
 #pragma unroll
@@ -692,7 +701,7 @@ __global__ void __launch_bounds__(NT) hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi
         div += G[x] * d[1 + x][0] + G[3 + x] * d[1 + x][1] + G[6 + x] * d[1 + x][2];
       }
       acc[s][0] = -div;
-      minv[s] = R(1) / (sw1[ii] * sw1[jj] * sw1[kk] * J);
+      minv[s] = siw3[n] * iJ;
     }
   }
 
@@ -789,7 +798,7 @@ __global__ void __launch_bounds__(NT) hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi
       } else {
         w = sve[end * N1 + l];
       }
-      const int pt = __ldg(TY.iop[1] + f * NP + n);
+      const int pt = spt[f * NP + n];
       const R* o = fl + f * NFQ + pt;
 #pragma unroll
       for (int c = 0; c < 4; ++c) lift[c] += w * o[c * NFP];

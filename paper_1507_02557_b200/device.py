@@ -58,10 +58,10 @@ def geometry_records(t, verts, zavg):
     """Per-element geometry record (float64 numpy), layouts in the header:
     dense types G(9) [, 1/sqrt(J)] then per face (n, Js-scale, avg(rho c),
     1/avg(rho c)); hex: 8 vertices, per face (avg, 1/avg), affine flag, and
-    for affine hexes G(9), J, per face (n, Js)."""
+    for affine hexes G(9), J, per face (n, Js), 1/J."""
     K = len(verts)
     if t == "hex":
-        out = np.zeros((K, 71))
+        out = np.zeros((K, 72))
         out[:, :24] = verts.reshape(K, 24)
         out[:, 24:36:2] = zavg
         out[:, 25:36:2] = 1.0 / zavg
@@ -71,6 +71,7 @@ def geometry_records(t, verts, zavg):
         out[:, 36] = affine_mask("hex", verts).astype(float)
         out[:, 37:46] = G[:, 0].reshape(K, 9)
         out[:, 46] = J[:, 0]
+        out[:, 71] = 1.0 / J[:, 0]
         for f in range(6):
             _, Js, nrm = face_geometry_batch("hex", verts, f, _CENTROID2D["quad"])
             out[:, 47 + 4 * f: 50 + 4 * f] = nrm[:, 0]
