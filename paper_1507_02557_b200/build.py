@@ -33,8 +33,10 @@ def build_native(max_order=7, force=False, verbose=False):
     if (not force and os.path.exists(OUT)
             and os.path.getmtime(OUT) >= max(os.path.getmtime(p) for p in deps)):
         return OUT
-    cmd = [nvcc()] + NVCC_FLAGS + [f"-DHW_MAX_ORDER={max_order}", "-o", OUT + ".tmp",
-                                   MAIN]
+    # HW_NVCC_DEFS: extra -D flags for tuning experiments (e.g. -DHW_TET_MINB=8)
+    extra = os.environ.get("HW_NVCC_DEFS", "").split()
+    cmd = [nvcc()] + NVCC_FLAGS + extra + [f"-DHW_MAX_ORDER={max_order}", "-o", OUT + ".tmp",
+                                           MAIN]
     proc = subprocess.run(cmd, capture_output=True, text=True)
     log = os.path.join(_HERE, "csrc", "build.log")
     with open(log, "w") as fh:

@@ -189,29 +189,29 @@ __global__ void __launch_bounds__(DMma<N, T>::NTH)
 
   // ---- volume GEMMs
   const int grp = warp / L::RT, rt = warp - grp * L::RT;   // grp is warp-uniform
-  const int arow = rt * 8 + (lane >> 2), acol = lane & 3;
+
   const int bk = lane & 3, bcol = lane >> 2;
   R dp[3][2] = {{0, 0}, {0, 0}, {0, 0}}, dv[2] = {0, 0};
   {
-    const R* A = (const R*)TY.op[2];    // [3][RT8][NPK]  A_c
-    const R* AT = (const R*)TY.op[3];   // [3][RT8][NPK]  A_c^T
+    const R* A = (const R*)TY.op[2];    // [3][RT][NPK/4][32] A_c fragments
+    const R* AT = (const R*)TY.op[3];   // A_c^T fragments
     if (grp == 0) {
       const R* bq = sq + bcol * EQ + bk;
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        const R* ac = A + ((size_t)c * L::RT8 + arow) * NPK + acol;
+        const R* ac = A + (((c * L::RT + rt) * (NPK / 4)) << 5) + lane;
 #pragma unroll 10
-        for (int ks = 0; ks < NPK / 4; ++ks) dmma884(dp[c][0], dp[c][1], ldg(ac + ks * 4), bq[ks * 4]);
+        for (int ks = 0; ks < NPK / 4; ++ks) dmma884(dp[c][0], dp[c][1], ldg(ac + (ks << 5)), bq[ks * 4]);
       }
     } else {
       const R* bv = sv + bcol * EV + bk;
       const R* AV = skew ? AT : A;
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        const R* ac = AV + ((size_t)c * L::RT8 + arow) * NPK + acol;
+        const R* ac = AV + (((c * L::RT + rt) * (NPK / 4)) << 5) + lane;
 #pragma unroll 10
         for (int ks = 0; ks < NPK / 4; ++ks)
-          dmma884(dv[0], dv[1], ldg(ac + ks * 4), bv[c * NPK + ks * 4]);
+          dmma884(dv[0], dv[1], ldg(ac + (ks << 5)), bv[c * NPK + ks * 4]);
       }
     }
   }
@@ -259,7 +259,7 @@ __global__ void __launch_bounds__(DMma<N, T>::NTH)
 
   // ---- lift GEMMs, combine, epilogue (group 1: p rows, group 0: u rows)
   const int col0 = (lane & 3) * 2;
-  const R* LF = (const R*)TY.op[4];     // [RT8][NFKT]
+  const R* LF = (const R*)TY.op[4];     // [RT][NFKT/4][32] lift fragments
   R acc[3][2];
   if (grp == 1) {
     acc[0][0] = skew ? dv[0] : -dv[0];
@@ -267,7 +267,7 @@ __global__ void __launch_bounds__(DMma<N, T>::NTH)
     const R* bp = sfp + bcol * EF + bk;
 #pragma unroll
     for (int k = 0; k < L::NFKT; k += 4)
-      dmma884(acc[0][0], acc[0][1], ldg(LF + (size_t)arow * L::NFKT + k + acol), bp[k]);
+      dmma884(acc[0][0], acc[0][1], ldg(LF + ((rt * (L::NFKT / 4) + (k >> 2)) << 5) + lane), bp[k]);
   } else {
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
@@ -283,7 +283,7 @@ __global__ void __launch_bounds__(DMma<N, T>::NTH)
 #pragma unroll
       for (int ks = 0; ks < L::kf(f) / 4; ++ks) {
         const int k = L::koff(f) + ks * 4;
-        dmma884(tu[0], tu[1], ldg(LF + (size_t)arow * L::NFKT + k + acol), bu[k]);
+        dmma884(tu[0], tu[1], ldg(LF + ((rt * (L::NFKT / 4) + (k >> 2)) << 5) + lane), bu[k]);
       }
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
@@ -322,17 +322,17 @@ __global__ void __launch_bounds__(DMma<N, T>::NTH)
   // ---- publish the traces of the new state: TR = E q_out
   if (E.mode != MODE_RHS && M.tr_out[T] != nullptr) {
     __syncthreads();
-    const R* Ep = (const R*)TY.op[7];   // [RTF*8][NPK]
+    const R* Ep = (const R*)TY.op[7];   // [RTF][NPK/4][32] trace-operator fragments
     R* tro = (R*)M.tr_out[T];
     // columns: (element, field) pairs, col = e*4 + c; 4 column tiles for
     // E = 8.  One row tile per warp pass, each A fragment feeds 4 MMAs.
     const int er = lane >> 2;
     for (int rf = warp; rf < L::RTF; rf += L::W) {
       R y[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
-      const R* arow_p = Ep + (size_t)(rf * 8 + er) * NPK + acol;
+      const R* arow_p = Ep + ((rf * (NPK / 4)) << 5) + lane;
 #pragma unroll 5
       for (int ks = 0; ks < NPK / 4; ++ks) {
-        const R a = ldg(arow_p + ks * 4);
+        const R a = ldg(arow_p + (ks << 5));
 #pragma unroll
         for (int cf = 0; cf < 4; ++cf) {
           const int col = cf * 8 + er;

@@ -58,7 +58,10 @@ struct TetMma {
                        SST = SV + E * RA, SRES = SST, SG = SST + E * RB,
                        SMAT = SG + E * GEO_TET, TOTAL = SMAT + E * 4;
   static constexpr size_t BYTES = sizeof(double) * TOTAL + sizeof(int) * (E + E * NFP + NFP);
-  static constexpr int MINB = (W <= 4) ? 6 : ((W <= 8) ? 3 : 1);
+#ifndef HW_TET_MINB
+#define HW_TET_MINB 6
+#endif
+  static constexpr int MINB = (W <= 4) ? HW_TET_MINB : ((W <= 8) ? 3 : 1);
 };
 
 template <int N>
@@ -159,18 +162,18 @@ __global__ void __launch_bounds__(TetMma<N>::NTH, TetMma<N>::MINB)
 
   // ---- P2: volume GEMMs on DMMA
   const int rt = warp / L::CT, ct = warp - rt * L::CT;
-  const int arow = rt * 8 + (lane >> 2), acol = lane & 3;
+
   const int bk = lane & 3, bcol = ct * 8 + (lane >> 2);
   R dp[3][2] = {{0, 0}, {0, 0}, {0, 0}}, dv[2] = {0, 0};
   {
-    const R* Dg = (const R*)TY.op[2];   // [3][RT8][NPK], zero padded
+    const R* Dg = (const R*)TY.op[2];   // [3][RT][NPK/4][32] A fragments, zero padded
     const R* bq = sq + bcol * EQ + bk;
     const R* bv = sv + bcol * EV + bk;
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
 #pragma unroll
       for (int ks = 0; ks < NPK / 4; ++ks) {
-        const R a = ldg(Dg + ((size_t)c * L::RT8 + arow) * NPK + ks * 4 + acol);
+        const R a = ldg(Dg + (((c * L::RT + rt) * (NPK / 4) + ks) << 5) + lane);
         dmma884(dp[c][0], dp[c][1], a, bq[ks * 4]);
         dmma884(dv[0], dv[1], a, bv[c * NPK + ks * 4]);
       }
@@ -242,7 +245,7 @@ __global__ void __launch_bounds__(TetMma<N>::NTH, TetMma<N>::MINB)
       accu[x][i] = -(G[x] * dp[0][i] + G[3 + x] * dp[1][i] + G[6 + x] * dp[2][i]);
   }
   {
-    const R* Lg = (const R*)TY.op[3];   // [4][RT8][NFK], zero padded
+    const R* Lg = (const R*)TY.op[3];   // [4][RT][NFK/4][32] A fragments
     const R* bp = sfp + bcol * EF + bk;
     const R* bu = sfu + bcol * EF + bk;
 #pragma unroll
@@ -250,7 +253,7 @@ __global__ void __launch_bounds__(TetMma<N>::NTH, TetMma<N>::MINB)
       R tu[2] = {0, 0};
 #pragma unroll
       for (int ks = 0; ks < NFK / 4; ++ks) {
-        const R a = ldg(Lg + ((size_t)f * L::RT8 + arow) * NFK + ks * 4 + acol);
+        const R a = ldg(Lg + (((f * L::RT + rt) * (NFK / 4) + ks) << 5) + lane);
         dmma884(accp[0], accp[1], a, bp[f * NFK + ks * 4]);
         dmma884(tu[0], tu[1], a, bu[f * NFK + ks * 4]);
       }

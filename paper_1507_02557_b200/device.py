@@ -173,6 +173,17 @@ def pack_mesh(disc):
     return pack
 
 
+def mma_fragments(A):
+    """(..., 8*RT, 4*KS) row-major padded matrix -> (..., RT, KS, 32): the
+    mma.m8n8k4 A fragment of row tile rt and k-step ks in lane order
+    (lane = 4*row + k), so a warp reads each fragment as 256 contiguous
+    bytes instead of 8 rows of 32 bytes."""
+    *lead, r8, k4 = A.shape
+    B = A.reshape(*lead, r8 // 8, 8, k4 // 4, 4)
+    B = np.moveaxis(B, -3, -2)                     # (..., RT, KS, 8, 4)
+    return np.ascontiguousarray(B.reshape(*lead, r8 // 8, k4 // 4, 32))
+
+
 def _pack_ops(t, d):
     if t == "hex":
         return {0: d["D1"], 1: d["Vend"], 2: d["w1"], 4: _hex_nodes(d)}
@@ -186,9 +197,9 @@ def _pack_ops(t, d):
         Lpad = np.zeros((4, rt8, nfk))
         for f in range(4):
             Lpad[f, :Np, :nfn] = d["LIFT"][:, f * nfn:(f + 1) * nfn]
-        # 0, 1: scalar kernel (transposed); 2, 3: DMMA kernel (row-major, padded)
+        # 0, 1: scalar kernel (transposed); 2, 3: DMMA kernel (padded, fragment order)
         return {0: np.stack([d["Dr"].T, d["Ds"].T, d["Dt"].T]), 1: d["LIFT"].T,
-                2: Dpad, 3: Lpad}
+                2: mma_fragments(Dpad), 3: mma_fragments(Lpad)}
     if t in ("wedge", "pyramid"):
         A = d["S"] if t == "wedge" else np.stack([d["Dr"], d["Ds"], d["Dt"]])
         # scalar kernel: op[0][c][m][n] = A_c[n][m], op[1][c][m][n] = A_c[m][n]
@@ -199,9 +210,10 @@ def _pack_ops(t, d):
 
 
 def _mma_ops(t, d, A):
-    """Zero-padded row-major operands of the DMMA kernels (hw_dense_mma.cuh):
-    op[2] A_c, op[3] A_c^T (3, RT8, NPK); op[4] LIFT with each face's K block
-    padded to a multiple of 4 (RT8, NFKT); op[7] E (RTF8, NPK)."""
+    """Zero-padded operands of the DMMA kernels (hw_dense_mma.cuh), stored in
+    A-fragment order (mma_fragments): op[2] A_c, op[3] A_c^T (3, RT8, NPK);
+    op[4] LIFT with each face's K block padded to a multiple of 4
+    (RT8, NFKT); op[7] E (RTF8, NPK)."""
     Np = d["Np"]
     rt8, npk = -(-Np // 8) * 8, -(-Np // 4) * 4
     Ap = np.zeros((3, rt8, npk))
@@ -220,7 +232,8 @@ def _mma_ops(t, d, A):
     nfp = int(offs[-1])
     Ep = np.zeros((-(-nfp // 8) * 8, npk))
     Ep[:nfp, :Np] = d["E"]
-    return {2: Ap, 3: ATp, 4: L, 7: Ep}
+    return {2: mma_fragments(Ap), 3: mma_fragments(ATp), 4: mma_fragments(L),
+            7: mma_fragments(Ep)}
 
 
 def tet_gather_index(mesh, dops, perm_tri, face_offsets):
