@@ -75,6 +75,9 @@ __host__ __device__ constexpr int n_dofs(int t) {
 
 template <typename R>
 __device__ __forceinline__ R ldg(const R* p) { return __ldg(p); }
+__device__ __forceinline__ double2 ldg2(const double* p) {   // 16-byte aligned pair
+  return __ldg(reinterpret_cast<const double2*>(p));
+}
 
 // Upwind flux of the acoustic system at one face point, own side (-) and
 // neighbour side (+), with my outward normal n (hybridwave/dg.py:337-350).

@@ -33,6 +33,15 @@ struct DMma {
     return s;
   }
   static constexpr int NFKT = koff(NF);                 // padded, face-concatenated K of the lift
+  // operand fragments are stored in k-step pairs (16-byte loads)
+  static constexpr int KSP = NPK / 4, KPP = (KSP + 1) / 2;         // volume / trace GEMMs
+  static constexpr int KSL = NFKT / 4, KPL = (KSL + 1) / 2;        // lift
+  __host__ __device__ static constexpr int kface(int j) {          // face of lift k-step j
+    int f = 0;
+    for (int g = 1; g < NF; ++g)
+      if (4 * j >= koff(g)) f = g;
+    return f;
+  }
   static constexpr int RTF = (NFP + 7) / 8;             // row tiles of the trace GEMM
   static constexpr int GEOS = GEO | 1;   // odd smem stride: per-element record reads spread over banks
   // q / res field stride = 4 or 12 (mod 16) doubles: the trace GEMM's B
@@ -199,19 +208,26 @@ __global__ void __launch_bounds__(DMma<N, T>::NTH)
       const R* bq = sq + bcol * EQ + bk;
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        const R* ac = A + (((c * L::RT + rt) * (NPK / 4)) << 5) + lane;
-#pragma unroll 10
-        for (int ks = 0; ks < NPK / 4; ++ks) dmma884(dp[c][0], dp[c][1], ldg(ac + (ks << 5)), bq[ks * 4]);
+        const R* ac = A + (((c * L::RT + rt) * L::KPP) << 6) + 2 * lane;
+        double2 pr;
+#pragma unroll
+        for (int ks = 0; ks < L::KSP; ++ks) {
+          if (!(ks & 1)) pr = ldg2(ac + ((ks >> 1) << 6));
+          dmma884(dp[c][0], dp[c][1], (ks & 1) ? pr.y : pr.x, bq[ks * 4]);
+        }
       }
     } else {
       const R* bv = sv + bcol * EV + bk;
       const R* AV = skew ? AT : A;
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        const R* ac = AV + (((c * L::RT + rt) * (NPK / 4)) << 5) + lane;
-#pragma unroll 10
-        for (int ks = 0; ks < NPK / 4; ++ks)
-          dmma884(dv[0], dv[1], ldg(ac + (ks << 5)), bv[c * NPK + ks * 4]);
+        const R* ac = AV + (((c * L::RT + rt) * L::KPP) << 6) + 2 * lane;
+        double2 pr;
+#pragma unroll
+        for (int ks = 0; ks < L::KSP; ++ks) {
+          if (!(ks & 1)) pr = ldg2(ac + ((ks >> 1) << 6));
+          dmma884(dv[0], dv[1], (ks & 1) ? pr.y : pr.x, bv[c * NPK + ks * 4]);
+        }
       }
     }
   }
@@ -265,9 +281,13 @@ __global__ void __launch_bounds__(DMma<N, T>::NTH)
     acc[0][0] = skew ? dv[0] : -dv[0];
     acc[0][1] = skew ? dv[1] : -dv[1];
     const R* bp = sfp + bcol * EF + bk;
+    const R* lf = LF + ((rt * L::KPL) << 6) + 2 * lane;
+    double2 pr;
 #pragma unroll
-    for (int k = 0; k < L::NFKT; k += 4)
-      dmma884(acc[0][0], acc[0][1], ldg(LF + ((rt * (L::NFKT / 4) + (k >> 2)) << 5) + lane), bp[k]);
+    for (int j = 0; j < L::KSL; ++j) {
+      if (!(j & 1)) pr = ldg2(lf + ((j >> 1) << 6));
+      dmma884(acc[0][0], acc[0][1], (j & 1) ? pr.y : pr.x, bp[4 * j]);
+    }
   } else {
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
@@ -277,20 +297,23 @@ __global__ void __launch_bounds__(DMma<N, T>::NTH)
         acc[x][i] = -(G[x] * dp[0][i] + G[3 + x] * dp[1][i] + G[6 + x] * dp[2][i]);
     }
     const R* bu = sfu + bcol * EF + bk;
+    const R* lf = LF + ((rt * L::KPL) << 6) + 2 * lane;
+    double2 pr;
+    R tu[2] = {0, 0};
 #pragma unroll
-    for (int f = 0; f < NF; ++f) {
-      R tu[2] = {0, 0};
+    for (int j = 0; j < L::KSL; ++j) {      // k-steps of all faces; fold per face
+      if (!(j & 1)) pr = ldg2(lf + ((j >> 1) << 6));
+      dmma884(tu[0], tu[1], (j & 1) ? pr.y : pr.x, bu[4 * j]);
+      const int f = L::kface(j);
+      if (j + 1 == L::KSL || L::kface(j + 1) != f) {
 #pragma unroll
-      for (int ks = 0; ks < L::kf(f) / 4; ++ks) {
-        const int k = L::koff(f) + ks * 4;
-        dmma884(tu[0], tu[1], ldg(LF + ((rt * (L::NFKT / 4) + (k >> 2)) << 5) + lane), bu[k]);
-      }
-#pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const R* g = sg + (col0 + i) * L::GEOS + GF + FS * f;
-        acc[0][i] += g[0] * tu[i];
-        acc[1][i] += g[1] * tu[i];
-        acc[2][i] += g[2] * tu[i];
+        for (int i = 0; i < 2; ++i) {
+          const R* g = sg + (col0 + i) * L::GEOS + GF + FS * f;
+          acc[0][i] += g[0] * tu[i];
+          acc[1][i] += g[1] * tu[i];
+          acc[2][i] += g[2] * tu[i];
+          tu[i] = R(0);
+        }
       }
     }
   }
@@ -329,10 +352,12 @@ __global__ void __launch_bounds__(DMma<N, T>::NTH)
     const int er = lane >> 2;
     for (int rf = warp; rf < L::RTF; rf += L::W) {
       R y[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
-      const R* arow_p = Ep + ((rf * (NPK / 4)) << 5) + lane;
-#pragma unroll 5
-      for (int ks = 0; ks < NPK / 4; ++ks) {
-        const R a = ldg(arow_p + (ks << 5));
+      const R* arow_p = Ep + ((rf * L::KPP) << 6) + 2 * lane;
+      double2 pr;
+#pragma unroll
+      for (int ks = 0; ks < L::KSP; ++ks) {
+        if (!(ks & 1)) pr = ldg2(arow_p + ((ks >> 1) << 6));
+        const R a = (ks & 1) ? pr.y : pr.x;
 #pragma unroll
         for (int cf = 0; cf < 4; ++cf) {
           const int col = cf * 8 + er;

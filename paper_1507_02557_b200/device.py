@@ -184,6 +184,19 @@ def mma_fragments(A):
     return np.ascontiguousarray(B.reshape(*lead, r8 // 8, k4 // 4, 32))
 
 
+def mma_fragment_pairs(A):
+    """mma_fragments with consecutive k-steps paired per lane,
+    (..., RT, ceil(KS/2), 32, 2) (odd KS zero padded): one 16-byte load
+    feeds two MMAs."""
+    F = mma_fragments(A)
+    *lead, rt, ks, _ = F.shape
+    if ks % 2:
+        F = np.concatenate([F, np.zeros((*lead, rt, 1, 32))], axis=-2)
+        ks += 1
+    F = F.reshape(*lead, rt, ks // 2, 2, 32)
+    return np.ascontiguousarray(np.swapaxes(F, -1, -2))
+
+
 def _pack_ops(t, d):
     if t == "hex":
         return {0: d["D1"], 1: d["Vend"], 2: d["w1"], 4: _hex_nodes(d)}
@@ -232,8 +245,8 @@ def _mma_ops(t, d, A):
     nfp = int(offs[-1])
     Ep = np.zeros((-(-nfp // 8) * 8, npk))
     Ep[:nfp, :Np] = d["E"]
-    return {2: mma_fragments(Ap), 3: mma_fragments(ATp), 4: mma_fragments(L),
-            7: mma_fragments(Ep)}
+    return {2: mma_fragment_pairs(Ap), 3: mma_fragment_pairs(ATp), 4: mma_fragment_pairs(L),
+            7: mma_fragment_pairs(Ep)}
 
 
 def tet_gather_index(mesh, dops, perm_tri, face_offsets):
