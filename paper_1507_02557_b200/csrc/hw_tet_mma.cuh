@@ -53,7 +53,12 @@ struct TetMma {
   static constexpr int ESG = 16 * NFN + 1;                  // staged neighbour values
   // buffers live in disjoint phases share storage: v_c (volume) with fp/fu
   // (flux, lift); the neighbour staging (flux) with the residual (epilogue)
-  static constexpr int RA = cmax(EV, 2 * EF), RB = stride4mod16(cmax(16 * NFN, EQ));
+#ifndef HW_TET_REGSTAGE
+#define HW_TET_REGSTAGE 1
+#endif
+  // neighbour values: registers (REGSTAGE) or smem staging
+  static constexpr int RA = cmax(EV, 2 * EF),
+                       RB = stride4mod16(HW_TET_REGSTAGE ? EQ : cmax(16 * NFN, EQ));
   static constexpr int SQ = 0, SV = SQ + E * EQ, SFP = SV, SFU = SFP + E * EF,
                        SST = SV + E * RA, SRES = SST, SG = SST + E * RB,
                        SMAT = SG + E * GEO_TET, TOTAL = SMAT + E * 4;
@@ -120,15 +125,46 @@ __global__ void __launch_bounds__(TetMma<N>::NTH, TetMma<N>::MINB)
   }
   copy_rows<GEO_TET, GEO_TET, NTH, EB>(sg, (const R*)TY.geo, sk, ne);
   copy_rows<4, 4, NTH, EB>(smat, (const R*)TY.mat, sk, ne);
+#if HW_TET_REGSTAGE
+  // gather index straight into registers: thread-item u is (e, j) =
+  // (tid + u * NTH) / NFP, % NFP, the same mapping the flux loop uses
+  constexpr int IT = (EB * NFP + NTH - 1) / NTH;
+  int gv[IT];
+#pragma unroll
+  for (int u = 0; u < IT; ++u) {
+    const int i = tid + u * NTH;
+    gv[u] = -1;
+    if (i < ne * NFP) gv[u] = __ldg(TY.iop[1] + (size_t)sk[i / NFP] * NFP + i % NFP);
+  }
+#else
   if (NFP % 4 == 0)   // gather ints
     copy_rows16<NFP, NFP, NTH, EB>(sgi, TY.iop[1], sk, ne);
   else
     copy_rows<NFP, NFP, NTH, EB>(sgi, TY.iop[1], sk, ne);
+#endif
   cp_async_commit();
   asm volatile("cp.async.wait_group 0;\n" ::: "memory");
   __syncthreads();
 
-  // ---- P1: neighbour face-node values via the gather index (fire and forget)
+  // ---- P1: neighbour face-node values via the gather index
+#if HW_TET_REGSTAGE
+  R nb[IT][4];   // consumed by the flux after the volume GEMMs
+#pragma unroll
+  for (int u = 0; u < IT; ++u) {
+    const int g = gv[u];
+    if (g >= 0) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) nb[u][c] = ldg(q + (size_t)g + c * NP);
+    } else if (g != -1) {   // pyramid / wedge neighbour: its published face trace
+      const unsigned v = (unsigned)(-3 - g);
+      const int t2 = (v & 1u) ? HW_WEDGE : HW_PYRAMID;
+      const int nfp2 = (v & 1u) ? Dims<N>::NFP_WEDGE : Dims<N>::NFP_PYR;
+      const R* src = (const R*)M.tr_in[t2] + (size_t)(v >> 1);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) nb[u][c] = ldg(src + c * nfp2);
+    }
+  }
+#else
   for (int i = tid; i < ne * NFP; i += NTH) {
     const int e = i / NFP, j = i - e * NFP;
     const int g = sgi[i];
@@ -147,6 +183,7 @@ __global__ void __launch_bounds__(TetMma<N>::NTH, TetMma<N>::MINB)
     }
   }
   cp_async_commit();
+#endif
 
   // v_c = sum_x G[c][x] u_x
   for (int i = tid; i < ne * NP; i += NTH) {
@@ -191,7 +228,14 @@ __global__ void __launch_bounds__(TetMma<N>::NTH, TetMma<N>::MINB)
       (fld < 4 ? sfp : sfu)[e * EF + (fld & 3) * NFK + n] = R(0);
     }
   const R pen = R(M.penalty_scale);
+#if HW_TET_REGSTAGE
+#pragma unroll
+  for (int u = 0; u < IT; ++u) {
+    const int i = tid + u * NTH;
+    if (i >= ne * NFP) break;
+#else
   for (int i = tid; i < ne * NFP; i += NTH) {
+#endif
     const int e = i / NFP, j = i - e * NFP;
     const int f = j / NFN, jj = j - f * NFN;
     const int node = sfn[j];
@@ -200,12 +244,17 @@ __global__ void __launch_bounds__(TetMma<N>::NTH, TetMma<N>::MINB)
     const R um[3] = {qe[NPK], qe[2 * NPK], qe[3 * NPK]};
     const R* g = sg + e * GEO_TET + 9 + FS * f;
     const R nrm[3] = {g[0], g[1], g[2]};
-    const int gi = sgi[i];
     R pp, up[3];
-    if (gi != -1) {
+#if HW_TET_REGSTAGE
+    if (gv[u] != -1) {
+      pp = nb[u][0]; up[0] = nb[u][1]; up[1] = nb[u][2]; up[2] = nb[u][3];
+    } else {
+#else
+    if (sgi[i] != -1) {
       const R* s = sst + e * L::RB + j;
       pp = s[0]; up[0] = s[NFP]; up[1] = s[2 * NFP]; up[2] = s[3 * NFP];
     } else {
+#endif
       pp = -pm; up[0] = um[0]; up[1] = um[1]; up[2] = um[2];
     }
     R tp, tu, fp, fu;
