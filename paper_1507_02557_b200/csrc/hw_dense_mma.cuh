@@ -56,7 +56,11 @@ struct DMma {
   static constexpr int ESG = ETR;
   // storage shared by phase-disjoint buffers: v_c (volume) with fp/fu
   // (flux, lift); own + neighbour traces (flux) with the residual (epilogue)
-  static constexpr int RA = cmax(EV, 2 * EF), RB = cmax(ETR + ESG, EQ);
+#ifndef HW_DENSE_REGSTAGE
+#define HW_DENSE_REGSTAGE 1
+#endif
+  // neighbour values in registers (REGSTAGE) or staged in smem
+  static constexpr int RA = cmax(EV, 2 * EF), RB = cmax(ETR + (HW_DENSE_REGSTAGE ? 0 : ESG), EQ);
   static constexpr int SQ = 0, SV = SQ + E * EQ, SFP = SV, SFU = SFP + E * EF,
                        STR = SV + E * RA, SST = STR + E * ETR, SRES = STR,
                        SG = STR + E * RB, SMAT = SG + E * GEOS, TOTAL = SMAT + E * 4;
@@ -141,12 +145,15 @@ __global__ void __launch_bounds__(DMma<N, T>::NTH)
   for (int i = tid; i < ne * NF; i += NTH)
     snc[i] = __ldg(TY.nbr_code + (size_t)sk[i / NF] * NF + i % NF);
   cp_async_commit();
+  // thread-item u = face point (e, j) = (tid + u * NTH) / NFP, % NFP (the
+  // flux loop uses the same mapping)
+  constexpr int IT = (EB * NFP + NTH - 1) / NTH;
+  int gv[IT];
+  R nb[IT][4];
   {
     // neighbour values at my face points through the host gather index
-    // (already in my point order): index loads batched, then cp.async
+    // (already in my point order): index loads batched, then the values
     const bool sem = M.formulation == HW_SEM;
-    constexpr int IT = (EB * NFP + NTH - 1) / NTH;
-    int gv[IT];
 #pragma unroll
     for (int u = 0; u < IT; ++u) {
       const int i = tid + u * NTH;
@@ -175,9 +182,14 @@ __global__ void __launch_bounds__(DMma<N, T>::NTH)
         stride = Dims<N>::NP_HEX;
       }
       src += gv[u];
+#if HW_DENSE_REGSTAGE
+#pragma unroll
+      for (int c = 0; c < 4; ++c) nb[u][c] = ldg(src + c * stride);
+#else
       R* dst = sst + e * ESG + j;
 #pragma unroll
       for (int c = 0; c < 4; ++c) cp_async(dst + c * NFP, src + c * stride);
+#endif
     }
     cp_async_commit();
   }
@@ -243,7 +255,10 @@ __global__ void __launch_bounds__(DMma<N, T>::NTH)
   }
   __syncthreads();
   const R pen = R(M.penalty_scale);
-  for (int i = tid; i < ne * NFP; i += NTH) {
+#pragma unroll
+  for (int u = 0; u < IT; ++u) {
+    const int i = tid + u * NTH;
+    if (i >= ne * NFP) break;
     const int e = i / NFP, j = i - e * NFP;
     int jj;
     const int f = face_of_point<N, T>(j, jj);
@@ -257,8 +272,12 @@ __global__ void __launch_bounds__(DMma<N, T>::NTH)
     if (code & HW_NBR_BOUNDARY) {
       pp = -own[0]; up[0] = um[0]; up[1] = um[1]; up[2] = um[2];
     } else {
+#if HW_DENSE_REGSTAGE
+      pp = nb[u][0]; up[0] = nb[u][1]; up[1] = nb[u][2]; up[2] = nb[u][3];
+#else
       const R* se = sst + e * ESG + j;
       pp = se[0]; up[0] = se[NFP]; up[1] = se[2 * NFP]; up[2] = se[3 * NFP];
+#endif
     }
     R tp, tu, fp, fu;
     penalties(g[4], g[5], pen, tp, tu);
