@@ -35,10 +35,13 @@ template <int N>
 struct TetMma {
   using D = Dims<N>;
   static constexpr int NP = D::NP_TET, NFN = D::NFN, NFP = 4 * D::NFN;
-#ifndef HW_TET_E3
-#define HW_TET_E3 8
+#ifndef HW_TET_E2
+#define HW_TET_E2 16
 #endif
-  static constexpr int E = (N == 1) ? 32 : (N == 3 ? HW_TET_E3 : (N <= 4 ? 16 : 8));
+#ifndef HW_TET_E4
+#define HW_TET_E4 8
+#endif
+  static constexpr int E = (N == 1) ? 32 : (N == 2 ? HW_TET_E2 : (N == 4 ? HW_TET_E4 : 8));
   static constexpr int CT = E / 8;
   static constexpr int RT = (NP + 7) / 8;
   static constexpr int RT8 = RT * 8;

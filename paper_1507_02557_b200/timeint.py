@@ -58,7 +58,13 @@ def _is_host(state):
     return not isinstance(next(iter(state.values())), torch.Tensor)
 
 
-def _export(disc, q, host):
+def _export(disc, q, host, out=None):
+    """Device state -> the caller's side: new host arrays, or (out given)
+    written into the caller's host arrays (pinned ones copy at DMA speed)."""
+    if host and out is not None:
+        for t in disc.types:
+            torch.from_numpy(out[t]).copy_(q[t])
+        return out
     if host:
         return {t: q[t].cpu().numpy() for t in disc.types}
     return {t: q[t].clone() for t in disc.types}
@@ -122,9 +128,10 @@ class Stepper:
         self.n_steps += 1
 
 
-def single_rate_run(disc, state, dt, T_final, callback=None):
+def single_rate_run(disc, state, dt, T_final, callback=None, out=None):
     """AB3 to T_final; the last step lands through the fractional
-    coefficients (hybridwave/timeint.py:57-72)."""
+    coefficients (hybridwave/timeint.py:57-72).  out: optional host arrays
+    the final state is written into."""
     _no_forcing(disc)
     host = _is_host(state)
     S = Stepper(disc, state, "ab")
@@ -135,7 +142,7 @@ def single_rate_run(disc, state, dt, T_final, callback=None):
         time += h
         if callback is not None:
             callback(time, _export(disc, S.q, host))
-    return _export(disc, S.q, host)
+    return _export(disc, S.q, host, out)
 
 
 def lsrk_step(disc, q, res, dt, q_tmp=None):
@@ -157,7 +164,7 @@ def lsrk_step(disc, q, res, dt, q_tmp=None):
     return q
 
 
-def lsrk_run(disc, state, dt, T_final, callback=None):
+def lsrk_run(disc, state, dt, T_final, callback=None, out=None):
     """Low-storage RK(4,5) to T_final with the single_rate_run signature;
     the last step is shortened to land on T_final."""
     _no_forcing(disc)
@@ -170,7 +177,7 @@ def lsrk_run(disc, state, dt, T_final, callback=None):
         time += h
         if callback is not None:
             callback(time, _export(disc, S.q, host))
-    return _export(disc, S.q, host)
+    return _export(disc, S.q, host, out)
 
 
 class MRABDriver:

@@ -13,7 +13,9 @@ WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
         "smsp__inst_executed.sum", "lts__t_bytes.sum",
         "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
-        "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum"]
+        "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum",
+        "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed",
+        "l1tex__throughput.avg.pct_of_peak_sustained_active"]
 
 
 def main(path):
