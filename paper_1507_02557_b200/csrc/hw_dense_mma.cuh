@@ -33,6 +33,14 @@ struct DMma {
     return s;
   }
   static constexpr int NFKT = koff(NF);                 // padded, face-concatenated K of the lift
+  // koff for a runtime face index: select chain (the constexpr loop would
+  // become a runtime loop)
+  __device__ __forceinline__ static int koff_rt(int f) {
+    int o = 0;
+#pragma unroll
+    for (int g = 0; g < NF - 1; ++g) o += (g < f) ? kf(g) : 0;
+    return o;
+  }
   // operand fragments are stored in k-step pairs (16-byte loads)
   static constexpr int KSP = NPK / 4, KPP = (KSP + 1) / 2;         // volume / trace GEMMs
   static constexpr int KSL = NFKT / 4, KPL = (KSL + 1) / 2;        // lift
@@ -282,8 +290,9 @@ __global__ void __launch_bounds__(DMma<N, T>::NTH)
     R tp, tu, fp, fu;
     penalties(g[4], g[5], pen, tp, tu);
     upwind_flux(own[0], um, pp, up, nrm, tp, tu, skew, fp, fu);
-    sfp[e * EF + L::koff(f) + jj] = fp * g[3];
-    sfu[e * EF + L::koff(f) + jj] = fu * g[3];
+    const int ko = L::koff_rt(f);
+    sfp[e * EF + ko + jj] = fp * g[3];
+    sfu[e * EF + ko + jj] = fu * g[3];
   }
   __syncthreads();
   // residual rows into the (now free) trace storage, behind the lift GEMM

@@ -69,7 +69,7 @@ struct TT<N, HW_HEX> {
 template <int N, int T>
 __host__ __device__ constexpr int stage_off(int f) {
   int s = 0;
-  for (int g = 0; g < f; ++g) s += TT<N, T>::stage(g);
+  for (int g = 0; g < TT<N, T>::NF; ++g) s += (g < f) ? TT<N, T>::stage(g) : 0;
   return s;
 }
 
