@@ -12,9 +12,11 @@ graph of one step.
   python bench.py [--gpus N --steps K --warmup W] [--impl reference]
                   [--mesh hybrid:38 --order 3 --form GL --dtype f64]
 
-Multi-GPU (torchrun): every rank advances its own copy of the workload
-(weak scaling, no data-path collective yet: the partitioned halo path is
-listed as next work in DESIGN.md); timing is the max over ranks.
+Multi-GPU (torchrun, N > 1): the mesh is extended along x to N slabs and
+element-partitioned (one slab per rank, the single-GPU workload each: weak
+scaling); every LSRK stage exchanges the partition-boundary element states
+with NCCL batched P2P while the interior elements compute
+(paper_1507_02557_b200/parallel.py); timing is the max over ranks.
 """
 
 import argparse
