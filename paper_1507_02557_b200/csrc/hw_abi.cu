@@ -221,10 +221,10 @@ static int launch_rhs_all(const hw_mesh_t& M, const hw_fields_t& Q, const Epi& E
     cudaStream_t st = ss ? ss->s[a] : st0;
     switch (t) {
       case HW_HEX: {
-        using L = Smem<N, HW_HEX, R>;
+        using L = Smem<N, HW_HEX, R, HW_HEX_NT>;
         if ((rc = set_smem(hex_kernel<N, R>, L::BYTES))) return rc;
-        hex_kernel<N, R><<<(unsigned)((n + L::EPB - 1) / L::EPB), NT, L::BYTES, st>>>(M, Q, E,
-                                                                                   list, n);
+        hex_kernel<N, R><<<(unsigned)((n + L::EPB - 1) / L::EPB), HW_HEX_NT, L::BYTES, st>>>(
+            M, Q, E, list, n);
         rc = check_launch("hex_kernel");
         break;
       }

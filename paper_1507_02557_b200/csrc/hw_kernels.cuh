@@ -252,12 +252,12 @@ __device__ __forceinline__ void publish_traces(const hw_mesh_t& M, const R* sq, 
 
 // ------------------------------------------------------------------ smem layout
 
-template <int N, int T, typename R>
+template <int N, int T, typename R, int NTH = NT>
 struct Smem {
   using X = TT<N, T>;
   static constexpr int NP = X::NP, NF = X::NF, NFP = X::NFP;
-  static constexpr int EPB = (NT / NP) > 0 ? (NT / NP) : 1;
-  static constexpr int S = (EPB * NP + NT - 1) / NT;
+  static constexpr int EPB = (NTH / NP) > 0 ? (NTH / NP) : 1;
+  static constexpr int S = (EPB * NP + NTH - 1) / NTH;
   static constexpr int FLUXW = (T == HW_HEX) ? 4 : 2;       // flux words per face point
   static constexpr int STG = stage_off<N, T>(NF);           // staged values per element
   // rows copied with 16-byte cp.async first (even sizes keep them aligned)
@@ -575,11 +575,15 @@ __device__ __forceinline__ R hex_metric(const R* X, R r, R s, R t, R G[9]) {
   return J;
 }
 
+#ifndef HW_HEX_NT
+#define HW_HEX_NT 128
+#endif
 template <int N, typename R>
-__global__ void __launch_bounds__(NT) hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi E,
+__global__ void __launch_bounds__(HW_HEX_NT) hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi E,
                                                  const int32_t* __restrict__ list,
                                                  int64_t nwork) {
-  using L = Smem<N, HW_HEX, R>;
+  using L = Smem<N, HW_HEX, R, HW_HEX_NT>;
+  constexpr int NT = HW_HEX_NT;   // threads per block of this kernel
   using D = Dims<N>;
   constexpr int N1 = D::N1, NP = L::NP, NFQ = D::NFQ, NFP = L::NFP, EPB = L::EPB, S = L::S;
   extern __shared__ __align__(16) unsigned char smem_raw[];
