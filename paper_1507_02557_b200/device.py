@@ -387,9 +387,10 @@ class DeviceMesh:
             self.struct.tr_in[i] = a.data_ptr() if a is not None else None
             self.struct.tr_out[i] = b.data_ptr() if b is not None else None
 
-    def compute_traces(self, q_fields, buf, stream):
-        """hw_traces: face traces of q (HWFields) into trace set `buf`."""
-        nat.check(nat.lib().hw_traces(self.struct, q_fields, nat.fields(self.traces[buf]), None,
+    def compute_traces(self, q_fields, buf, stream, subset=None):
+        """hw_traces: face traces of q (HWFields) into trace set `buf`
+        (optionally only for the elements of an HWSubset)."""
+        nat.check(nat.lib().hw_traces(self.struct, q_fields, nat.fields(self.traces[buf]), subset,
                                       stream))
 
     def _put(self, arr, dtype=None):

@@ -202,6 +202,50 @@ class MRABDriver:
             for t in disc.types:
                 idx = np.flatnonzero(self.levels[t] == lev).astype(np.int32)
                 self._lists[(lev, t)] = torch.as_tensor(idx, device=dev) if len(idx) else None
+        self._tick_subsets()
+
+    def _tick_subsets(self):
+        """Per tick of the macro step: the elements whose effective state and
+        face traces the stepping elements read (themselves and their face
+        neighbours), so the dense-output pass and the trace pass touch only
+        those instead of the whole mesh."""
+        disc, L = self.disc, self.n_levels
+        mesh = disc.mesh
+        names = ("hex", "wedge", "pyramid", "tet")
+        need = {lev: {t: self.levels[t] == lev for t in disc.types} for lev in range(1, L + 1)}
+        for lev in range(1, L + 1):
+            own = {t: need[lev][t].copy() for t in disc.types}
+            for t in disc.types:
+                nb = mesh.nbr[t][own[t]]                       # (n, nf, 3)
+                for tid2, t2 in enumerate(names):
+                    if t2 not in need[lev]:
+                        continue
+                    sel = nb[:, :, 0] == tid2
+                    need[lev][t2][nb[:, :, 1][sel]] = True
+        dev = disc.device
+        empty = torch.zeros(0, dtype=torch.int32, device=dev)
+        self._tick_keep, self._eff_subs, self._trace_subs = [], {}, {}
+        for tick in range(2 ** (L - 1)):
+            stepping = [lev for lev in range(1, L + 1) if tick % (2 ** (L - lev)) == 0]
+            needed = {t: np.any([need[lev][t] for lev in stepping], axis=0) for t in disc.types}
+            tl = [None] * 4
+            for t in disc.types:
+                idx = np.flatnonzero(needed[t]).astype(np.int32)
+                tl[TYPE_ID[t]] = torch.as_tensor(idx, device=dev) if len(idx) else empty
+            self._tick_keep.append(tl)
+            self._trace_subs[tick] = nat.subset(tl)
+            for lev in range(1, L + 1):
+                el = [None] * 4
+                any_ = False
+                for t in disc.types:
+                    idx = np.flatnonzero(needed[t] & (self.levels[t] == lev)).astype(np.int32)
+                    el[TYPE_ID[t]] = torch.as_tensor(idx, device=dev) if len(idx) else empty
+                    any_ |= len(idx) > 0
+                for t in range(4):
+                    if el[t] is None:
+                        el[t] = empty
+                self._tick_keep.append(el)
+                self._eff_subs[(tick, lev)] = nat.subset(el) if any_ else None
 
     def _subset(self, levs):
         lists = [None] * 4
@@ -226,19 +270,22 @@ class MRABDriver:
                 period = 2 ** (L - lev)
                 frac = tick % period
                 nh = n_hist[lev]
+                sub = self._eff_subs[(tick, lev)]        # read by this tick's stepping elements
+                if sub is None:
+                    continue
                 if frac == 0 or nh == 0:
                     nat.check(lib.hw_axpy3(dm.struct, F(q), F(eff), F(ring[0]), None, None,
-                                           1, 0.0, 0.0, 0.0, 0.0, subs[lev], st))
+                                           1, 0.0, 0.0, 0.0, 0.0, sub, st))
                     continue
                 c = ab_coefficients(nh, frac / period) - ab_coefficients(nh, 1.0)
                 c = list(c) + [0.0] * (3 - nh)
                 s0 = steps[lev] % 3
                 h = [ring[s0], ring[(s0 - 1) % 3], ring[(s0 - 2) % 3]]
                 nat.check(lib.hw_axpy3(dm.struct, F(q), F(eff), F(h[0]), F(h[1]), F(h[2]),
-                                       nh, c[0], c[1], c[2], dt_min * period, subs[lev], st))
+                                       nh, c[0], c[1], c[2], dt_min * period, sub, st))
             # traces of the effective state, then the fused RHS + AB update
             # of each stepping level (no trace publishing)
-            dm.compute_traces(F(eff), 0, st)
+            dm.compute_traces(F(eff), 0, st, subset=self._trace_subs[tick])
             dm.set_traces(0, None)
             for lev in stepping:
                 n_hist[lev] = min(n_hist[lev] + 1, 3)
