@@ -22,9 +22,14 @@ struct DMma {
   static constexpr int RT = (NP + 7) / 8;
   static constexpr int RT8 = RT * 8;
   static constexpr int NPK = ((NP + 3) / 4) * 4;
-  // two warp groups of RT warps: group 0 grad p + the u lift (u rows),
-  // group 1 div v + the p lift (p rows)
-  static constexpr int W = 2 * RT;
+  // small RT: two warp groups of RT warps, group 0 grad p + the u lift
+  // (u rows), group 1 div v + the p lift (p rows); large RT (N >= 4): one
+  // warp per row tile does both (keeps the block at <= RT warps)
+#ifndef HW_DENSE_SPLIT_MAX_RT
+#define HW_DENSE_SPLIT_MAX_RT 6
+#endif
+  static constexpr bool SPLIT = RT <= HW_DENSE_SPLIT_MAX_RT;
+  static constexpr int W = SPLIT ? 2 * RT : RT;
   static constexpr int NTH = 32 * W;
   __host__ __device__ static constexpr int kf(int f) { return ((X::cnt(f) + 3) / 4) * 4; }
   __host__ __device__ static constexpr int koff(int f) {
@@ -217,14 +222,15 @@ __global__ void __launch_bounds__(DMma<N, T>::NTH)
   __syncthreads();
 
   // ---- volume GEMMs
-  const int grp = warp / L::RT, rt = warp - grp * L::RT;   // grp is warp-uniform
+  const int grp = L::SPLIT ? warp / L::RT : 0, rt = warp - grp * L::RT;   // warp-uniform
+  const bool do_u = !L::SPLIT || grp == 0, do_p = !L::SPLIT || grp == 1;
 
   const int bk = lane & 3, bcol = lane >> 2;
   R dp[3][2] = {{0, 0}, {0, 0}, {0, 0}}, dv[2] = {0, 0};
   {
     const R* A = (const R*)TY.op[2];    // [3][RT][NPK/4][32] A_c fragments
     const R* AT = (const R*)TY.op[3];   // A_c^T fragments
-    if (grp == 0) {
+    if (do_u) {
       const R* bq = sq + bcol * EQ + bk;
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
@@ -236,7 +242,8 @@ __global__ void __launch_bounds__(DMma<N, T>::NTH)
           dmma884(dp[c][0], dp[c][1], (ks & 1) ? pr.y : pr.x, bq[ks * 4]);
         }
       }
-    } else {
+    }
+    if (do_p) {
       const R* bv = sv + bcol * EV + bk;
       const R* AV = skew ? AT : A;
 #pragma unroll
@@ -304,19 +311,20 @@ __global__ void __launch_bounds__(DMma<N, T>::NTH)
   // ---- lift GEMMs, combine, epilogue (group 1: p rows, group 0: u rows)
   const int col0 = (lane & 3) * 2;
   const R* LF = (const R*)TY.op[4];     // [RT][NFKT/4][32] lift fragments
-  R acc[3][2];
-  if (grp == 1) {
-    acc[0][0] = skew ? dv[0] : -dv[0];
-    acc[0][1] = skew ? dv[1] : -dv[1];
+  R acc[3][2], accp[2];
+  if (do_p) {
+    accp[0] = skew ? dv[0] : -dv[0];
+    accp[1] = skew ? dv[1] : -dv[1];
     const R* bp = sfp + bcol * EF + bk;
     const R* lf = LF + ((rt * L::KPL) << 6) + 2 * lane;
     double2 pr;
 #pragma unroll
     for (int j = 0; j < L::KSL; ++j) {
       if (!(j & 1)) pr = ldg2(lf + ((j >> 1) << 6));
-      dmma884(acc[0][0], acc[0][1], (j & 1) ? pr.y : pr.x, bp[4 * j]);
+      dmma884(accp[0], accp[1], (j & 1) ? pr.y : pr.x, bp[4 * j]);
     }
-  } else {
+  }
+  if (do_u) {
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
       const R* G = sg + (col0 + i) * L::GEOS;
@@ -358,9 +366,8 @@ __global__ void __launch_bounds__(DMma<N, T>::NTH)
       const size_t base = (size_t)sk[e] * 4 * NP + n;
       R* qe = sq + e * EQ + n;
       const R* re = sres + e * EQ + n;
-      if (grp == 1) {
-        qe[0] = epilogue_q<R>(E, T, base, acc[0][i] * smat[e * 4 + 0], qe[0], re[0]);
-      } else {
+      if (do_p) qe[0] = epilogue_q<R>(E, T, base, accp[i] * smat[e * 4 + 0], qe[0], re[0]);
+      if (do_u) {
         const R irho = smat[e * 4 + 1];
 #pragma unroll
         for (int x = 0; x < 3; ++x)
