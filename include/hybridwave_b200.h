@@ -136,8 +136,10 @@ int hw_hist_push(const hw_mesh_t* mesh, hw_fields_t* h0, hw_fields_t* h1,
 int hw_halo_pack(const hw_mesh_t* mesh, int elem_type, const void* q,
                  const int32_t* idx, int64_t n, void* sendbuf, void* stream);
 
-/* Sum of U^T M U with material weights per type (discrete_energy,
- * hybridwave/dg.py:655-674); writes one double per type slot to out[4]. */
+/* Discrete energy U^T M U with material weights (p^2 / kappa + rho |u|^2)
+ * per element type (discrete_energy, hybridwave/dg.py:655-674).  out is a
+ * DEVICE pointer to HW_NTYPES doubles: zeroed on `stream`, then one sum
+ * per type slot (asynchronous, graph-capturable). */
 int hw_energy(const hw_mesh_t* mesh, const hw_fields_t* q, double* out,
               void* stream);
 

@@ -382,6 +382,46 @@ static unsigned grid_for(int64_t total) {
 
 using namespace hw;
 
+// discrete energy per type (hw_energy)
+template <int N, typename R>
+static int launch_energy(const hw_mesh_t& M, const hw_fields_t& Q, double* out,
+                         cudaStream_t st) {
+  for (int t = 0; t < HW_NTYPES; ++t) {
+    const int64_t K = M.t[t].K;
+    if (K <= 0) continue;
+    const int64_t items = K * np_of(t, N);
+    const unsigned g = grid_for(items);
+    switch (t) {
+      case HW_HEX: energy_kernel<N, HW_HEX, R><<<g, 256, 0, st>>>(M, Q, out, K); break;
+      case HW_WEDGE: energy_kernel<N, HW_WEDGE, R><<<g, 256, 0, st>>>(M, Q, out, K); break;
+      case HW_PYRAMID: energy_kernel<N, HW_PYRAMID, R><<<g, 256, 0, st>>>(M, Q, out, K); break;
+      default: energy_kernel<N, HW_TET, R><<<g, 256, 0, st>>>(M, Q, out, K); break;
+    }
+    int rc = check_launch("energy_kernel");
+    if (rc) return rc;
+  }
+  return 0;
+}
+
+template <typename R>
+static int dispatch_energy(const hw_mesh_t& M, const hw_fields_t& Q, double* out,
+                           cudaStream_t st) {
+  switch (M.N) {
+    case 1: return launch_energy<1, R>(M, Q, out, st);
+    case 2: return launch_energy<2, R>(M, Q, out, st);
+    case 3: return launch_energy<3, R>(M, Q, out, st);
+    case 4: return launch_energy<4, R>(M, Q, out, st);
+    case 5: return launch_energy<5, R>(M, Q, out, st);
+#if HW_MAX_ORDER >= 6
+    case 6: return launch_energy<6, R>(M, Q, out, st);
+#endif
+#if HW_MAX_ORDER >= 7
+    case 7: return launch_energy<7, R>(M, Q, out, st);
+#endif
+    default: return fail("polynomial order not compiled into this library");
+  }
+}
+
 extern "C" {
 
 int hw_version(void) { return 1; }
@@ -528,8 +568,13 @@ int hw_halo_pack(const hw_mesh_t* mesh, int elem_type, const void* q, const int3
   return check_launch("pack_kernel");
 }
 
-int hw_energy(const hw_mesh_t*, const hw_fields_t*, double*, void*) {
-  return fail("hw_energy: not built yet");
+int hw_energy(const hw_mesh_t* mesh, const hw_fields_t* q, double* out, void* stream) {
+  if (!out) return fail("hw_energy: out is null");
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = cudaMemsetAsync(out, 0, HW_NTYPES * sizeof(double), st);
+  if (e != cudaSuccess) return fail(cudaGetErrorString(e));
+  return mesh->dtype == HW_F64 ? dispatch_energy<double>(*mesh, *q, out, st)
+                               : dispatch_energy<float>(*mesh, *q, out, st);
 }
 
 }  // extern "C"

@@ -827,6 +827,74 @@ __global__ void __launch_bounds__(HW_HEX_NT) hex_kernel(hw_mesh_t M, hw_fields_t
   }
 }
 
+// Discrete energy U^T M U with material weights (hybridwave/dg.py:655-674):
+// p / kappa + rho |u|^2, mass: hex w3 J (per node), tet J M_ref, pyramid J,
+// wedge identity (LSC basis).  One thread per (element, node); block sums
+// accumulate into out[T] with a double atomicAdd.
+template <int N, int T, typename R>
+__global__ void __launch_bounds__(256) energy_kernel(hw_mesh_t M, hw_fields_t Q, double* out,
+                                                     int64_t K) {
+  using X = TT<N, T>;
+  using D = Dims<N>;
+  constexpr int NP = X::NP;
+  const hw_type_t& TY = M.t[T];
+  const R* q = (const R*)Q.p[T];
+  const R* geo = (const R*)TY.geo;
+  const R* mat = (const R*)TY.mat;
+  double acc = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < K * NP;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = i / NP;
+    const int n = (int)(i - e * NP);
+    const R* qe = q + e * 4 * NP;
+    const double wp = 1.0 / (double)mat[e * 4 + 0], wu = 1.0 / (double)mat[e * 4 + 1];
+    double w = 1.0;
+    if (T == HW_HEX) {
+      const R* g = geo + e * GEO_HEX;
+      const R* w1 = (const R*)TY.op[2];
+      const int a = n / (D::N1 * D::N1), b = (n / D::N1) % D::N1, c = n % D::N1;
+      double J;
+      if (g[HX_AFF] != R(0)) {
+        J = (double)g[HX_J];
+      } else {
+        const R* x1 = (const R*)TY.op[4];
+        R G[9];
+        J = (double)hex_metric<R>(g, x1[a], x1[b], x1[c], G);
+      }
+      w = (double)w1[a] * (double)w1[b] * (double)w1[c] * J;
+    } else if (T != HW_WEDGE) {
+      const R* G = geo + e * X::GEO;
+      const double det = (double)G[0] * ((double)G[4] * G[8] - (double)G[5] * G[7]) -
+                         (double)G[1] * ((double)G[3] * G[8] - (double)G[5] * G[6]) +
+                         (double)G[2] * ((double)G[3] * G[7] - (double)G[4] * G[6]);
+      w = 1.0 / det;   // G = dr/dx: det G = 1/J
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const double v = (double)qe[c * NP + n];
+      double mv = v;
+      if (T == HW_TET) {   // (M_ref u)_n
+        const R* Mr = (const R*)TY.op[4] + n * NP;
+        mv = 0.0;
+        for (int j = 0; j < NP; ++j) mv += (double)Mr[j] * (double)qe[c * NP + j];
+      }
+      s += (c == 0 ? wp : wu) * v * mv;
+    }
+    acc += w * s;
+  }
+  // block reduction
+  __shared__ double red[32];
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    acc = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+    if (threadIdx.x == 0) atomicAdd(out + T, acc);
+  }
+}
+
 // Face traces of q for a publishing type (hw_traces): EPB elements per block.
 template <int N, int T, typename R>
 __global__ void __launch_bounds__(NT) trace_kernel(hw_mesh_t M, hw_fields_t Q, hw_fields_t TR,

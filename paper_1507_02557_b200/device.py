@@ -162,7 +162,8 @@ def pack_mesh(disc):
             "geo": geometry_records(t, verts, face_impedance_avg(mesh, t)),
             "mat": material_records(np.asarray(mesh.materials[t], dtype=float)),
             "nbr_elem": elem, "nbr_code": code,
-            "op": _pack_ops(t, dops),
+            "op": {**_pack_ops(t, dops),
+                   **({4: disc.ops[t].M_ref} if t == "tet" else {})},   # tet: energy mass
             "iop": _pack_iops(t, dops, disc.N, mesh, perm_tri, face_offsets, dops_all,
                               perm_quad, disc.formulation.kind == "SEM"),
             "nfp": int(dops["face_offsets"][-1]),

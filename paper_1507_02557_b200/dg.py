@@ -154,6 +154,14 @@ class Discretization:
     def stream_ptr(self):
         return torch.cuda.current_stream(self.device).cuda_stream
 
+    def energy_device(self, q):
+        """Discrete energy of a device state (hw_energy): a 0-d fp64 CUDA
+        tensor (no host sync).  Same value as discrete_energy(state, disc)."""
+        out = torch.empty(4, dtype=torch.float64, device=self.device)
+        nat.check(nat.lib().hw_energy(self.device_mesh.struct, nat.fields(self.slots(q)),
+                                      out.data_ptr(), self.stream_ptr()))
+        return out.sum()
+
     def rhs_device(self, q, out=None, subset=None):
         """Device RHS: q, out dicts of CUDA tensors (no host copies)."""
         dm = self.device_mesh

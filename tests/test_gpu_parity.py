@@ -130,6 +130,28 @@ def test_mrab_matches_reference(native_lib):
     assert _l2rel(s, ref) < 1e-10
 
 
+@pytest.mark.parametrize("spec,N,form", [("hybrid:2", 3, "GL"), ("hybrid:2", 2, "SEM"),
+                                          ("hex:2", 3, "GL"), ("tet:2", 4, "GL")])
+def test_energy_matches_host(native_lib, spec, N, form):
+    """hw_energy (device, per type, atomics) = discrete_energy (host)."""
+    from paper_1507_02557_b200.dg import discrete_energy
+    d, st = _cavity(spec, N, form)
+    rng = np.random.default_rng(3)
+    st = {t: v + 0.1 * rng.standard_normal(v.shape) for t, v in st.items()}
+    ref = discrete_energy(st, d)
+    got = float(d.energy_device(d.to_device(st)))
+    assert abs(got - ref) <= 1e-12 * abs(ref)
+
+
+def test_energy_nonaffine_hex(native_lib):
+    from paper_1507_02557_b200.dg import Discretization, discrete_energy
+    d = Discretization(_perturbed("hex:3", 0.04, 7), 3, "GL")
+    rng = np.random.default_rng(4)
+    st = {t: rng.standard_normal((d.n_elems[t], 4, d.ops[t].Np)) for t in d.types}
+    ref = discrete_energy(st, d)
+    assert abs(float(d.energy_device(d.to_device(st))) - ref) <= 1e-12 * abs(ref)
+
+
 def test_mrab_graph_replay_matches_eager(native_lib):
     """The CUDA-graph replay of the 3-macro-step launch period reproduces the
     eager launches bit for bit (same kernels, same arguments), counters too."""
