@@ -66,10 +66,19 @@ struct TetMma {
                        SST = SV + E * RA, SRES = SST, SG = SST + E * RB,
                        SMAT = SG + E * GEO_TET, TOTAL = SMAT + E * 4;
   static constexpr size_t BYTES = sizeof(double) * TOTAL + sizeof(int) * (E + E * NFP + NFP);
+#ifndef HW_TET_PERSIST
+#define HW_TET_PERSIST 0
+#endif
+  // persistent blocks with register-resident operator fragments where they
+  // fit (N <= 3: 27 doubles per thread)
+  static constexpr bool PERSIST = HW_TET_PERSIST && (3 * (NPK / 4) + 4 * (NFK / 4)) <= 32;
 #ifndef HW_TET_MINB
 #define HW_TET_MINB 6
 #endif
-  static constexpr int MINB = (W <= 4) ? HW_TET_MINB : ((W <= 8) ? 3 : 1);
+#ifndef HW_TET_PMINB
+#define HW_TET_PMINB 4
+#endif
+  static constexpr int MINB = (W <= 4) ? (PERSIST ? HW_TET_PMINB : HW_TET_MINB) : ((W <= 8) ? 3 : 1);
 };
 
 template <int N>
@@ -97,12 +106,32 @@ __global__ void __launch_bounds__(TetMma<N>::NTH, TetMma<N>::MINB)
 
   const hw_type_t& TY = M.t[HW_TET];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t w0 = (int64_t)blockIdx.x * EB;
-  const int ne = (int)((nwork - w0) < EB ? (nwork - w0) : EB);
   const bool lsrk = E.mode == MODE_LSRK;
+  for (int i = tid; i < NFP; i += NTH) sfn[i] = __ldg(TY.iop[0] + i);
+  // persistent blocks: this warp's operator fragments (its row tile of D_c
+  // and LIFT_f) stay in registers for every batch of elements it processes
+  R Av[3][NPK / 4], Al[4][NFK / 4];
+  if (L::PERSIST) {
+    const int rt0 = warp / L::CT;
+    const R* Dg = (const R*)TY.op[2];
+    const R* Lg = (const R*)TY.op[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+      for (int ks = 0; ks < NPK / 4; ++ks)
+        Av[c][ks] = ldg(Dg + (((c * L::RT + rt0) * (NPK / 4) + ks) << 5) + lane);
+#pragma unroll
+    for (int f = 0; f < 4; ++f)
+#pragma unroll
+      for (int ks = 0; ks < NFK / 4; ++ks)
+        Al[f][ks] = ldg(Lg + (((f * L::RT + rt0) * (NFK / 4) + ks) << 5) + lane);
+  }
+  const int64_t nbatch = (nwork + EB - 1) / EB;
+  for (int64_t bidx = blockIdx.x; bidx < nbatch; bidx += (L::PERSIST ? gridDim.x : nbatch)) {
+  const int64_t w0 = bidx * EB;
+  const int ne = (int)((nwork - w0) < EB ? (nwork - w0) : EB);
 
   if (tid < EB) sk[tid] = tid < ne ? (list ? list[w0 + tid] : (int)(w0 + tid)) : 0;
-  for (int i = tid; i < NFP; i += NTH) sfn[i] = __ldg(TY.iop[0] + i);
   // K padding must be zero for the DMMA (rows are never written by copies)
   constexpr int PADN = (NPK > NP) ? NPK - NP : 1, PADF = (NFK > NFN) ? NFK - NFN : 1;
   if (NPK > NP)
@@ -213,7 +242,8 @@ __global__ void __launch_bounds__(TetMma<N>::NTH, TetMma<N>::MINB)
     for (int c = 0; c < 3; ++c) {
 #pragma unroll
       for (int ks = 0; ks < NPK / 4; ++ks) {
-        const R a = ldg(Dg + (((c * L::RT + rt) * (NPK / 4) + ks) << 5) + lane);
+        const R a = L::PERSIST ? Av[c][ks]
+                               : ldg(Dg + (((c * L::RT + rt) * (NPK / 4) + ks) << 5) + lane);
         dmma884(dp[c][0], dp[c][1], a, bq[ks * 4]);
         dmma884(dv[0], dv[1], a, bv[c * NPK + ks * 4]);
       }
@@ -305,7 +335,8 @@ __global__ void __launch_bounds__(TetMma<N>::NTH, TetMma<N>::MINB)
       R tu[2] = {0, 0};
 #pragma unroll
       for (int ks = 0; ks < NFK / 4; ++ks) {
-        const R a = ldg(Lg + (((f * L::RT + rt) * (NFK / 4) + ks) << 5) + lane);
+        const R a = L::PERSIST ? Al[f][ks]
+                               : ldg(Lg + (((f * L::RT + rt) * (NFK / 4) + ks) << 5) + lane);
         dmma884(accp[0], accp[1], a, bp[f * NFK + ks * 4]);
         dmma884(tu[0], tu[1], a, bu[f * NFK + ks * 4]);
       }
@@ -338,6 +369,8 @@ __global__ void __launch_bounds__(TetMma<N>::NTH, TetMma<N>::MINB)
         epilogue_s<R>(E, HW_TET, base + (1 + x) * NP, accu[x][i] * irho, qe[(1 + x) * NPK],
                       re[(1 + x) * NPK]);
     }
+  }
+  if (L::PERSIST) __syncthreads();   // the next batch reuses shared memory
   }
 }
 
