@@ -4,7 +4,6 @@
 #include <cstring>
 #include <mutex>
 #include <string>
-#include <unordered_map>
 #include <unordered_set>
 
 #include "hw_kernels.cuh"
@@ -128,25 +127,6 @@ static SideStreams* side_streams() {
   return per_dev[dev];
 }
 
-// blocks of `kernel` resident on the whole device (SMs x occupancy), cached
-template <typename KernelT>
-static int64_t resident_blocks(KernelT kernel, int threads, size_t smem) {
-  static std::mutex mu;
-  static std::unordered_map<const void*, int64_t> cache;
-  std::lock_guard<std::mutex> lock(mu);
-  const void* key = (const void*)kernel;
-  auto it = cache.find(key);
-  if (it != cache.end()) return it->second;
-  int dev = 0, sms = 0, per = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess ||
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, threads, smem) != cudaSuccess)
-    return 0;
-  const int64_t v = (int64_t)sms * per;
-  cache[key] = v;
-  return v;
-}
-
 // shared-memory floor per CTA (bytes, env HW_SMEM_FLOOR; tuning experiments:
 // fewer resident CTAs leave more of the SM's L1 for the operator matrices)
 static size_t smem_floor() {
@@ -261,12 +241,8 @@ static int launch_rhs_all(const hw_mesh_t& M, const hw_fields_t& Q, const Epi& E
         if (sizeof(R) == 8 && !tet_scalar()) {
           using L = TetMma<N>;
           if ((rc = set_smem(tet_mma_kernel<N>, L::BYTES))) return rc;
-          int64_t nb = (n + L::E - 1) / L::E;
-          if (L::PERSIST) {   // persistent: at most one wave of resident blocks
-            const int64_t cap = resident_blocks(tet_mma_kernel<N>, L::NTH, L::BYTES);
-            if (cap > 0 && nb > cap) nb = cap;
-          }
-          tet_mma_kernel<N><<<(unsigned)nb, L::NTH, L::BYTES, st>>>(M, Q, E, list, n);
+          tet_mma_kernel<N><<<(unsigned)((n + L::E - 1) / L::E), L::NTH, L::BYTES, st>>>(
+              M, Q, E, list, n);
           rc = check_launch("tet_mma_kernel");
         } else {
           rc = launch_dense<N, HW_TET, R>(M, Q, E, list, n, st);
