@@ -63,19 +63,14 @@ struct DMma {
   static constexpr int EQ = stride4mod16(4 * QF);
   static constexpr int EV = stride4mod16(3 * NPK);
   static constexpr int EF = stride4mod16(NFKT);
-  // own traces and neighbour values, both [4][NFP] in my face-point order
-  // (even stride: 16-byte copies)
+  // own traces [4][NFP] in my face-point order (even stride: 16-byte
+  // copies); neighbour values are gathered into registers
   static constexpr int ETR = 4 * NFP + 2;
-  static constexpr int ESG = ETR;
   // storage shared by phase-disjoint buffers: v_c (volume) with fp/fu
-  // (flux, lift); own + neighbour traces (flux) with the residual (epilogue)
-#ifndef HW_DENSE_REGSTAGE
-#define HW_DENSE_REGSTAGE 1
-#endif
-  // neighbour values in registers (REGSTAGE) or staged in smem
-  static constexpr int RA = cmax(EV, 2 * EF), RB = cmax(ETR + (HW_DENSE_REGSTAGE ? 0 : ESG), EQ);
+  // (flux, lift); own traces (flux) with the residual (epilogue)
+  static constexpr int RA = cmax(EV, 2 * EF), RB = cmax(ETR, EQ);
   static constexpr int SQ = 0, SV = SQ + E * EQ, SFP = SV, SFU = SFP + E * EF,
-                       STR = SV + E * RA, SST = STR + E * ETR, SRES = STR,
+                       STR = SV + E * RA, SRES = STR,
                        SG = STR + E * RB, SMAT = SG + E * GEOS, TOTAL = SMAT + E * 4;
   static constexpr size_t BYTES = sizeof(double) * TOTAL + sizeof(int) * (E + E * NF);
   static constexpr bool VEC = (NP % 2 == 0) && (NPK == NP);
@@ -111,7 +106,7 @@ __global__ void __launch_bounds__(DMma<N, T>::NTH)
   using X = TT<N, T>;
   using R = double;
   constexpr int NP = L::NP, NF = L::NF, NFP = L::NFP, EB = L::E, NPK = L::NPK, NTH = L::NTH,
-                EQ = L::EQ, EV = L::EV, EF = L::EF, ESG = L::ESG, ETR = L::ETR, GEO = L::GEO,
+                EQ = L::EQ, EV = L::EV, EF = L::EF, ETR = L::ETR, GEO = L::GEO,
                 GF = L::GF;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   R* sm = reinterpret_cast<R*>(smem_raw);
@@ -123,7 +118,6 @@ __global__ void __launch_bounds__(DMma<N, T>::NTH)
   R* sfp = sm + L::SFP;
   R* sfu = sm + L::SFU;
   R* str = sm + L::STR;
-  R* sst = sm + L::SST;
   R* sg = sm + L::SG;
   R* smat = sm + L::SMAT;
 
@@ -195,14 +189,8 @@ __global__ void __launch_bounds__(DMma<N, T>::NTH)
         stride = Dims<N>::NP_HEX;
       }
       src += gv[u];
-#if HW_DENSE_REGSTAGE
 #pragma unroll
       for (int c = 0; c < 4; ++c) nb[u][c] = ldg(src + c * stride);
-#else
-      R* dst = sst + e * ESG + j;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) cp_async(dst + c * NFP, src + c * stride);
-#endif
     }
     cp_async_commit();
   }
@@ -294,12 +282,7 @@ __global__ void __launch_bounds__(DMma<N, T>::NTH)
     if (code & HW_NBR_BOUNDARY) {
       pp = -own[0]; up[0] = um[0]; up[1] = um[1]; up[2] = um[2];
     } else {
-#if HW_DENSE_REGSTAGE
       pp = nb[u][0]; up[0] = nb[u][1]; up[1] = nb[u][2]; up[2] = nb[u][3];
-#else
-      const R* se = sst + e * ESG + j;
-      pp = se[0]; up[0] = se[NFP]; up[1] = se[2 * NFP]; up[2] = se[3 * NFP];
-#endif
     }
     R tp, tu, fp, fu;
     penalties(g[4], g[5], pen, tp, tu);
