@@ -269,11 +269,11 @@ struct Smem {
   static constexpr int STR = SST + EPB * STG;               // own traces (publishing types)
   static constexpr int SG = STR + ((T == HW_TET) ? 0 : EPB * 4 * NFP);
   static constexpr int SMAT = SG + EPB * X::GEO;
-  static constexpr int SOPS = SMAT + EPB * 4;   // hex: D1, x, w, Vend, 1/(w_i w_j w_k)
-  static constexpr int TOTAL = SOPS + ((T == HW_HEX) ? (N + 1) * (N + 1) + 4 * (N + 1) + NP : 0);
+  static constexpr int SOPS = SMAT + EPB * 4;   // hex: D1, x, w, Vend, 1/w
+  static constexpr int TOTAL = SOPS + ((T == HW_HEX) ? (N + 1) * (N + 1) + 5 * (N + 1) : 0);
   // ints: element ids, links (x2); hex: node -> face point table (6 x NP)
   static constexpr size_t BYTES =
-      sizeof(R) * TOTAL + sizeof(int) * (2 * EPB * NF + EPB + ((T == HW_HEX) ? 6 * NP : 0));
+      sizeof(R) * TOTAL + sizeof(int) * (2 * EPB * NF + EPB + ((T == HW_HEX) ? 24 : 0));
 };
 
 template <int N, int T, typename R>
@@ -590,7 +590,7 @@ __global__ void __launch_bounds__(HW_HEX_NT) hex_kernel(hw_mesh_t M, hw_fields_t
   R* sm = reinterpret_cast<R*>(smem_raw);
   int* sk = reinterpret_cast<int*>(sm + L::TOTAL);
   int* snc = sk + EPB;
-  int* spt = snc + 2 * EPB * 6;  // node -> face point (6 x NP)
+  int* spc = snc + 2 * EPB * 6;  // node -> face point: per face pt = c . (i, j, k, 1)
   R* sq = sm + L::SQ;
   R* sf = sm + L::SF;
   R* sg = sm + L::SG;
@@ -599,7 +599,7 @@ __global__ void __launch_bounds__(HW_HEX_NT) hex_kernel(hw_mesh_t M, hw_fields_t
   R* sx = sD + N1 * N1;          // 1-D nodes
   R* sw1 = sx + N1;              // 1-D weights
   R* sve = sw1 + N1;             // endpoint rows (2 x N1)
-  R* siw3 = sve + 2 * N1;        // 1 / (w_i w_j w_k) per node
+  R* siw1 = sve + 2 * N1;        // 1 / w (1-D)
 
   const hw_type_t& TY = M.t[HW_HEX];
   const bool sem = M.formulation == HW_SEM;
@@ -610,13 +610,10 @@ __global__ void __launch_bounds__(HW_HEX_NT) hex_kernel(hw_mesh_t M, hw_fields_t
   if (tid < 2 * N1) sve[tid] = ldg((const R*)TY.op[1] + tid);
   if (tid < N1) {
     sw1[tid] = ldg((const R*)TY.op[2] + tid);
+    siw1[tid] = R(1) / sw1[tid];
     sx[tid] = ldg((const R*)TY.op[4] + tid);
   }
-  for (int i = tid; i < NP; i += NT) {
-    const R* w = (const R*)TY.op[2];
-    siw3[i] = R(1) / (ldg(w + i / (N1 * N1)) * ldg(w + (i / N1) % N1) * ldg(w + i % N1));
-  }
-  for (int i = tid; i < 6 * NP; i += NT) spt[i] = __ldg(TY.iop[1] + i);
+  if (tid < 24) spc[tid] = __ldg(TY.iop[3] + tid);
   if (tid < ne) sk[tid] = list ? list[w0 + tid] : (int)(w0 + tid);
   __syncthreads();
   // group 1 (volume inputs): state rows, records, links
@@ -705,7 +702,7 @@ __global__ void __launch_bounds__(HW_HEX_NT) hex_kernel(hw_mesh_t M, hw_fields_t
         div += G[x] * d[1 + x][0] + G[3 + x] * d[1 + x][1] + G[6 + x] * d[1 + x][2];
       }
       acc[s][0] = -div;
-      minv[s] = siw3[n] * iJ;
+      minv[s] = siw1[ii] * siw1[jj] * siw1[kk] * iJ;
     }
   }
 
@@ -802,7 +799,8 @@ __global__ void __launch_bounds__(HW_HEX_NT) hex_kernel(hw_mesh_t M, hw_fields_t
       } else {
         w = sve[end * N1 + l];
       }
-      const int pt = spt[f * NP + n];
+      const int* cf = spc + 4 * f;
+      const int pt = cf[0] * idx[0] + cf[1] * idx[1] + cf[2] * idx[2] + cf[3];
       const R* o = fl + f * NFQ + pt;
 #pragma unroll
       for (int c = 0; c < 4; ++c) lift[c] += w * o[c * NFP];

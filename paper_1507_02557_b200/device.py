@@ -134,6 +134,23 @@ def hex_node_face_points(dops, N):
     return out
 
 
+def hex_face_point_coefficients(dops, N):
+    """(6, 4) int32: node (i, j, k) -> its face point on face f is
+    c[f] . (i, j, k, 1) (the face rules enumerate points on the tensor grid,
+    so the map is affine; checked exactly against hex_node_face_points)."""
+    tab = hex_node_face_points(dops, N)
+    n1 = N + 1
+    n = np.arange(n1 ** 3)
+    I = np.stack([n // (n1 * n1), (n // n1) % n1, n % n1, np.ones_like(n)], axis=1)
+    out = np.zeros((6, 4), dtype=np.int32)
+    for f in range(6):
+        c = np.rint(np.linalg.lstsq(I.astype(float), tab[f].astype(float), rcond=None)[0])
+        if not np.array_equal(I @ c.astype(np.int64), tab[f]):
+            raise ValueError("hex face-point map is not affine in the node indices")
+        out[f] = c
+    return out
+
+
 def pack_mesh(disc):
     """Host (numpy) image of everything the kernels read: per type
     {geo, mat, nbr_elem, nbr_code, op{slot}, iop{slot}, form, K} plus the
@@ -330,6 +347,7 @@ def _pack_iops(t, d, N, mesh=None, perm_tri=None, face_offsets=None, dops_all=No
                perm_quad=None, sem=False):
     if t == "hex":
         return {0: d["face_tab"], 1: hex_node_face_points(d, N),
+                3: hex_face_point_coefficients(d, N),
                 2: face_gather_index(mesh, t, dops_all, perm_tri, perm_quad, face_offsets, N, sem)}
     if t == "tet":
         return {0: d["face_nodes"], 1: tet_gather_index(mesh, d, perm_tri, face_offsets)}
