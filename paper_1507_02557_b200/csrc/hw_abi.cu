@@ -137,18 +137,18 @@ static size_t smem_floor() {
   return v;
 }
 
-template <int N, int T>
+template <int N, int T, typename R>
 static int launch_dense_mma(const hw_mesh_t& M, const hw_fields_t& Q, const Epi& E,
                             const int32_t* list, int64_t n, cudaStream_t st) {
-  using L = DMma<N, T>;
+  using L = DMma<N, T, R>;
   // high orders (N >= 6): the DMMA kernel exceeds the CTA's thread / smem limits
   if constexpr (L::BYTES > 220 * 1024 || L::NTH > 1024) {
-    return launch_dense<N, T, double>(M, Q, E, list, n, st);
+    return launch_dense<N, T, R>(M, Q, E, list, n, st);
   } else {
   int rc;
   const size_t bytes = L::BYTES > smem_floor() ? L::BYTES : smem_floor();
-  if ((rc = set_smem(dense_mma_kernel<N, T>, bytes))) return rc;
-  dense_mma_kernel<N, T><<<(unsigned)((n + L::E - 1) / L::E), L::NTH, bytes, st>>>(M, Q, E,
+  if ((rc = set_smem(dense_mma_kernel<N, T, R>, bytes))) return rc;
+  dense_mma_kernel<N, T, R><<<(unsigned)((n + L::E - 1) / L::E), L::NTH, bytes, st>>>(M, Q, E,
                                                                                  list, n);
   return check_launch("dense_mma_kernel");
   }
@@ -228,20 +228,19 @@ static int launch_rhs_all(const hw_mesh_t& M, const hw_fields_t& Q, const Epi& E
         rc = check_launch("hex_kernel");
         break;
       }
-      case HW_WEDGE:
-        rc = (sizeof(R) == 8 && !tet_scalar()) ? launch_dense_mma<N, HW_WEDGE>(M, Q, E, list, n, st)
-                                               : launch_dense<N, HW_WEDGE, R>(M, Q, E, list, n, st);
+      case HW_WEDGE:   // fp64 DMMA for both storage precisions
+        rc = !tet_scalar() ? launch_dense_mma<N, HW_WEDGE, R>(M, Q, E, list, n, st)
+                           : launch_dense<N, HW_WEDGE, R>(M, Q, E, list, n, st);
         break;
       case HW_PYRAMID:
-        rc = (sizeof(R) == 8 && !tet_scalar())
-                 ? launch_dense_mma<N, HW_PYRAMID>(M, Q, E, list, n, st)
-                 : launch_dense<N, HW_PYRAMID, R>(M, Q, E, list, n, st);
+        rc = !tet_scalar() ? launch_dense_mma<N, HW_PYRAMID, R>(M, Q, E, list, n, st)
+                           : launch_dense<N, HW_PYRAMID, R>(M, Q, E, list, n, st);
         break;
       case HW_TET:
-        if (sizeof(R) == 8 && !tet_scalar()) {
-          using L = TetMma<N>;
-          if ((rc = set_smem(tet_mma_kernel<N>, L::BYTES))) return rc;
-          tet_mma_kernel<N><<<(unsigned)((n + L::E - 1) / L::E), L::NTH, L::BYTES, st>>>(
+        if (!tet_scalar()) {   // fp64 DMMA for both storage precisions
+          using L = TetMma<N, R>;
+          if ((rc = set_smem(tet_mma_kernel<N, R>, L::BYTES))) return rc;
+          tet_mma_kernel<N, R><<<(unsigned)((n + L::E - 1) / L::E), L::NTH, L::BYTES, st>>>(
               M, Q, E, list, n);
           rc = check_launch("tet_mma_kernel");
         } else {

@@ -1,5 +1,5 @@
 // Wedge / pyramid RHS + update with the dense contractions on the fp64
-// tensor cores (mma.sync.m8n8k4.f64), fp64 only.  Same organisation as
+// tensor cores (mma.sync.m8n8k4.f64); storage fp64 or fp32, arithmetic fp64.  Same organisation as
 // tet_mma_kernel; in addition these types publish the face traces of their
 // new state (trace buffer, see hw_kernels.cuh) with a third GEMM
 //   TR = E q_out    (face points x (element, field)),
@@ -13,7 +13,8 @@
 
 namespace hw {
 
-template <int N, int T>
+// S: storage type (double or float); arithmetic fp64 (DMMA) throughout
+template <int N, int T, typename S = double>
 struct DMma {
   using X = TT<N, T>;
   using D = Dims<N>;
@@ -57,38 +58,44 @@ struct DMma {
   }
   static constexpr int RTF = (NFP + 7) / 8;             // row tiles of the trace GEMM
   static constexpr int GEOS = GEO | 1;   // odd smem stride: per-element record reads spread over banks
-  // q / res field stride = 4 or 12 (mod 16) doubles: the trace GEMM's B
-  // fragments (8 columns = 2 elements x 4 fields) then hit every bank twice
-  static constexpr int QF = NPK + ((NPK % 16 <= 4) ? 4 - NPK % 16 : (NPK % 16 <= 12 ? 12 - NPK % 16 : 20 - NPK % 16));
-  static constexpr int EQ = stride4mod16(4 * QF);
-  static constexpr int EV = stride4mod16(3 * NPK);
-  static constexpr int EF = stride4mod16(NFKT);
-  // own traces [4][NFP] in my face-point order (even stride: 16-byte
-  // copies); neighbour values are gathered into registers
-  static constexpr int ETR = 4 * NFP + 2;
+  // q / res field stride: the trace GEMM's B fragments (8 columns = 2
+  // elements x 4 fields) conflict-free: fp64 4 or 12 (mod 16) doubles,
+  // fp32 8 or 24 (mod 32) floats
+  __host__ __device__ static constexpr int qf_stride(int n) {
+    if (sizeof(S) == 8)
+      return n + ((n % 16 <= 4) ? 4 - n % 16 : (n % 16 <= 12 ? 12 - n % 16 : 20 - n % 16));
+    return n + ((n % 32 <= 8) ? 8 - n % 32 : (n % 32 <= 24 ? 24 - n % 32 : 40 - n % 32));
+  }
+  static constexpr int QF = qf_stride(NPK);
+  static constexpr int EQ = frag_stride<S>(4 * QF);
+  static constexpr int EV = frag_stride<S>(3 * NPK);
+  static constexpr int EF = frag_stride<S>(NFKT);
+  // own traces [4][NFP] in my face-point order (stride padded by 16 bytes:
+  // 16-byte copies); neighbour values are gathered into registers
+  static constexpr int V16 = 16 / sizeof(S);
+  static constexpr int ETR = 4 * NFP + V16;
   // storage shared by phase-disjoint buffers: v_c (volume) with fp/fu
   // (flux, lift); own traces (flux) with the residual (epilogue)
   static constexpr int RA = cmax(EV, 2 * EF), RB = cmax(ETR, EQ);
   static constexpr int SQ = 0, SV = SQ + E * EQ, SFP = SV, SFU = SFP + E * EF,
                        STR = SV + E * RA, SRES = STR,
                        SG = STR + E * RB, SMAT = SG + E * GEOS, TOTAL = SMAT + E * 4;
-  static constexpr size_t BYTES = sizeof(double) * TOTAL + sizeof(int) * (E + E * NF);
-  static constexpr bool VEC = (NP % 2 == 0) && (NPK == NP);
+  static constexpr size_t BYTES = sizeof(S) * TOTAL + sizeof(int) * (E + E * NF);
 };
 
 // element rows (K, 4, NP) -> smem [e][field (stride QF)][node]
-template <typename L>
-__device__ __forceinline__ void copy_q_rows(double* dst, const double* src, const int* sk, int ne) {
-  constexpr int NP = L::NP;
-  if (NP % 2 == 0) {
-    constexpr int CF = NP / 2, CH = 4 * CF, TOT = L::E * CH;   // 16-byte chunks
+template <typename L, typename S>
+__device__ __forceinline__ void copy_q_rows(S* dst, const S* src, const int* sk, int ne) {
+  constexpr int NP = L::NP, V = L::V16;
+  if (NP % V == 0) {
+    constexpr int CF = NP / V, CH = 4 * CF, TOT = L::E * CH;   // 16-byte chunks
 #pragma unroll
     for (int u = 0; u < (TOT + L::NTH - 1) / L::NTH; ++u) {
       const int i = (int)threadIdx.x + u * L::NTH;
       if ((TOT % L::NTH) && i >= TOT) break;
       const int e = i / CH, r = i - e * CH, fld = r / CF, c = r - fld * CF;
       if (e >= ne) break;
-      cp_async16(dst + e * L::EQ + fld * L::QF + 2 * c, src + (size_t)sk[e] * 4 * NP + fld * NP + 2 * c);
+      cp_async16(dst + e * L::EQ + fld * L::QF + V * c, src + (size_t)sk[e] * 4 * NP + fld * NP + V * c);
     }
   } else {
     for (int i = threadIdx.x; i < ne * 4 * NP; i += L::NTH) {
@@ -98,28 +105,28 @@ __device__ __forceinline__ void copy_q_rows(double* dst, const double* src, cons
   }
 }
 
-template <int N, int T>
-__global__ void __launch_bounds__(DMma<N, T>::NTH)
+template <int N, int T, typename S>
+__global__ void __launch_bounds__(DMma<N, T, S>::NTH)
     dense_mma_kernel(hw_mesh_t M, hw_fields_t Q, Epi E, const int32_t* __restrict__ list,
                      int64_t nwork) {
-  using L = DMma<N, T>;
+  using L = DMma<N, T, S>;
   using X = TT<N, T>;
   using R = double;
   constexpr int NP = L::NP, NF = L::NF, NFP = L::NFP, EB = L::E, NPK = L::NPK, NTH = L::NTH,
                 EQ = L::EQ, EV = L::EV, EF = L::EF, ETR = L::ETR, GEO = L::GEO,
                 GF = L::GF;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  R* sm = reinterpret_cast<R*>(smem_raw);
+  S* sm = reinterpret_cast<S*>(smem_raw);
   int* sk = reinterpret_cast<int*>(sm + L::TOTAL);
   int* snc = sk + EB;
-  R* sq = sm + L::SQ;
-  R* sres = sm + L::SRES;
-  R* sv = sm + L::SV;
-  R* sfp = sm + L::SFP;
-  R* sfu = sm + L::SFU;
-  R* str = sm + L::STR;
-  R* sg = sm + L::SG;
-  R* smat = sm + L::SMAT;
+  S* sq = sm + L::SQ;
+  S* sres = sm + L::SRES;
+  S* sv = sm + L::SV;
+  S* sfp = sm + L::SFP;
+  S* sfu = sm + L::SFU;
+  S* str = sm + L::STR;
+  S* sg = sm + L::SG;
+  S* smat = sm + L::SMAT;
 
   const hw_type_t& TY = M.t[T];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -135,20 +142,20 @@ __global__ void __launch_bounds__(DMma<N, T>::NTH)
     for (int i = tid; i < EB * 11 * PADN; i += NTH) {
       const int e = i / (11 * PADN), r = i - e * 11 * PADN;
       const int fld = r / PADN, n = NP + r - fld * PADN;
-      if (fld < 4) sq[e * EQ + fld * L::QF + n] = R(0);
-      else if (fld >= 8) sv[e * EV + (fld - 8) * NPK + n] = R(0);
+      if (fld < 4) sq[e * EQ + fld * L::QF + n] = S(0);
+      else if (fld >= 8) sv[e * EV + (fld - 8) * NPK + n] = S(0);
     }
   __syncthreads();
 
   // ---- P0: rows, records, links (all async), then neighbour staging
-  const R* q = (const R*)Q.p[T];
-  const R* resg = (const R*)E.res[T];
+  const S* q = (const S*)Q.p[T];
+  const S* resg = (const S*)E.res[T];
   copy_q_rows<L>(sq, q, sk, ne);
   {   // own traces of the input state (published by the previous stage)
-    copy_rows16<4 * NFP, ETR, NTH, EB>(str, (const R*)M.tr_in[T], sk, ne);
+    copy_rows16<4 * NFP, ETR, NTH, EB>(str, (const S*)M.tr_in[T], sk, ne);
   }
-  copy_rows<GEO, L::GEOS, NTH, EB>(sg, (const R*)TY.geo, sk, ne);
-  copy_rows<4, 4, NTH, EB>(smat, (const R*)TY.mat, sk, ne);
+  copy_rows<GEO, L::GEOS, NTH, EB>(sg, (const S*)TY.geo, sk, ne);
+  copy_rows<4, 4, NTH, EB>(smat, (const S*)TY.mat, sk, ne);
   for (int i = tid; i < ne * NF; i += NTH)
     snc[i] = __ldg(TY.nbr_code + (size_t)sk[i / NF] * NF + i % NF);
   cp_async_commit();
@@ -176,21 +183,21 @@ __global__ void __launch_bounds__(DMma<N, T>::NTH)
       int jj;
       const int f = face_of_point<N, T>(j, jj);
       const int t2 = HW_NBR_TYPE(snc[e * NF + f]);
-      const R* src;
+      const S* src;
       int stride;
       if (publishes(t2, sem)) {
-        src = (const R*)M.tr_in[t2];
+        src = (const S*)M.tr_in[t2];
         stride = nfp_of<N>(t2);
       } else if (t2 == HW_TET) {
-        src = (const R*)Q.p[HW_TET];
+        src = (const S*)Q.p[HW_TET];
         stride = Dims<N>::NP_TET;
       } else {
-        src = (const R*)Q.p[HW_HEX];
+        src = (const S*)Q.p[HW_HEX];
         stride = Dims<N>::NP_HEX;
       }
       src += gv[u];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) nb[u][c] = ldg(src + c * stride);
+      for (int c = 0; c < 4; ++c) nb[u][c] = R(ldg(src + c * stride));
     }
     cp_async_commit();
   }
@@ -200,12 +207,12 @@ __global__ void __launch_bounds__(DMma<N, T>::NTH)
   // v_c = sum_x G[c][x] u_x
   for (int i = tid; i < ne * NP; i += NTH) {
     const int e = i / NP, n = i - e * NP;
-    const R* G = sg + e * L::GEOS;
-    const R* u = sq + e * EQ + n;
+    const S* G = sg + e * L::GEOS;
+    const S* u = sq + e * EQ + n;
     const R u0 = u[L::QF], u1 = u[2 * L::QF], u2 = u[3 * L::QF];
 #pragma unroll
     for (int c = 0; c < 3; ++c)
-      sv[e * EV + c * NPK + n] = G[c * 3] * u0 + G[c * 3 + 1] * u1 + G[c * 3 + 2] * u2;
+      sv[e * EV + c * NPK + n] = S(R(G[c * 3]) * u0 + R(G[c * 3 + 1]) * u1 + R(G[c * 3 + 2]) * u2);
   }
   __syncthreads();
 
@@ -218,7 +225,7 @@ __global__ void __launch_bounds__(DMma<N, T>::NTH)
     const R* A = (const R*)TY.op[2];    // [3][RT][NPK/4][32] A_c fragments
     const R* AT = (const R*)TY.op[3];   // A_c^T fragments
     auto vol_u = [&]() {
-      const R* bq = sq + bcol * EQ + bk;
+      const S* bq = sq + bcol * EQ + bk;
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
         const R* ac = A + (((c * L::RT + rt) * L::KPP) << 6) + 2 * lane;
@@ -231,7 +238,7 @@ __global__ void __launch_bounds__(DMma<N, T>::NTH)
       }
     };
     auto vol_p = [&]() {
-      const R* bv = sv + bcol * EV + bk;
+      const S* bv = sv + bcol * EV + bk;
       const R* AV = skew ? AT : A;
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
@@ -260,8 +267,8 @@ __global__ void __launch_bounds__(DMma<N, T>::NTH)
   // ---- flux at the face points (face point fastest across threads)
   for (int i = tid; i < EB * L::NFKT; i += NTH) {   // lift K padding (storage held v_c)
     const int e = i / L::NFKT, k = i - e * L::NFKT;
-    sfp[e * EF + k] = R(0);
-    sfu[e * EF + k] = R(0);
+    sfp[e * EF + k] = S(0);
+    sfu[e * EF + k] = S(0);
   }
   __syncthreads();
   const R pen = R(M.penalty_scale);
@@ -272,10 +279,10 @@ __global__ void __launch_bounds__(DMma<N, T>::NTH)
     const int e = i / NFP, j = i - e * NFP;
     int jj;
     const int f = face_of_point<N, T>(j, jj);
-    const R* te = str + e * ETR + j;
+    const S* te = str + e * ETR + j;
     const R own[4] = {te[0], te[NFP], te[2 * NFP], te[3 * NFP]};
     const R um[3] = {own[1], own[2], own[3]};
-    const R* g = sg + e * L::GEOS + GF + FS * f;
+    const S* g = sg + e * L::GEOS + GF + FS * f;
     const R nrm[3] = {g[0], g[1], g[2]};
     const int code = snc[e * NF + f];
     R pp, up[3];
@@ -285,11 +292,11 @@ __global__ void __launch_bounds__(DMma<N, T>::NTH)
       pp = nb[u][0]; up[0] = nb[u][1]; up[1] = nb[u][2]; up[2] = nb[u][3];
     }
     R tp, tu, fp, fu;
-    penalties(g[4], g[5], pen, tp, tu);
+    penalties(R(g[4]), R(g[5]), pen, tp, tu);
     upwind_flux(own[0], um, pp, up, nrm, tp, tu, skew, fp, fu);
     const int ko = L::koff_rt(f);
-    sfp[e * EF + ko + jj] = fp * g[3];
-    sfu[e * EF + ko + jj] = fu * g[3];
+    sfp[e * EF + ko + jj] = S(fp * R(g[3]));
+    sfu[e * EF + ko + jj] = S(fu * R(g[3]));
   }
   __syncthreads();
   // residual rows into the (now free) trace storage, behind the lift GEMM
@@ -305,7 +312,7 @@ __global__ void __launch_bounds__(DMma<N, T>::NTH)
   auto lift_p = [&]() {
     accp[0] = skew ? dv[0] : -dv[0];
     accp[1] = skew ? dv[1] : -dv[1];
-    const R* bp = sfp + bcol * EF + bk;
+    const S* bp = sfp + bcol * EF + bk;
     const R* lf = LF + ((rt * L::KPL) << 6) + 2 * lane;
     double2 pr;
 #pragma unroll
@@ -317,12 +324,12 @@ __global__ void __launch_bounds__(DMma<N, T>::NTH)
   auto lift_u = [&]() {
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
-      const R* G = sg + (col0 + i) * L::GEOS;
+      const S* G = sg + (col0 + i) * L::GEOS;
 #pragma unroll
       for (int x = 0; x < 3; ++x)
-        acc[x][i] = -(G[x] * dp[0][i] + G[3 + x] * dp[1][i] + G[6 + x] * dp[2][i]);
+        acc[x][i] = -(R(G[x]) * dp[0][i] + R(G[3 + x]) * dp[1][i] + R(G[6 + x]) * dp[2][i]);
     }
-    const R* bu = sfu + bcol * EF + bk;
+    const S* bu = sfu + bcol * EF + bk;
     const R* lf = LF + ((rt * L::KPL) << 6) + 2 * lane;
     double2 pr;
     R tu[2] = {0, 0};
@@ -334,10 +341,10 @@ __global__ void __launch_bounds__(DMma<N, T>::NTH)
       if (j + 1 == L::KSL || L::kface(j + 1) != f) {
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
-          const R* g = sg + (col0 + i) * L::GEOS + GF + FS * f;
-          acc[0][i] += g[0] * tu[i];
-          acc[1][i] += g[1] * tu[i];
-          acc[2][i] += g[2] * tu[i];
+          const S* g = sg + (col0 + i) * L::GEOS + GF + FS * f;
+          acc[0][i] += R(g[0]) * tu[i];
+          acc[1][i] += R(g[1]) * tu[i];
+          acc[2][i] += R(g[2]) * tu[i];
           tu[i] = R(0);
         }
       }
@@ -360,16 +367,16 @@ __global__ void __launch_bounds__(DMma<N, T>::NTH)
       const int e = col0 + i;
       if (e >= ne) continue;
       const size_t base = (size_t)sk[e] * 4 * NP + n;
-      R* qe = sq + e * EQ + n;
-      const R* re = sres + e * EQ + n;
+      S* qe = sq + e * EQ + n;
+      const S* re = sres + e * EQ + n;
       auto out_p = [&]() {
-        qe[0] = epilogue_q<R>(E, T, base, accp[i] * smat[e * 4 + 0], qe[0], re[0]);
+        qe[0] = epilogue_q<S>(E, T, base, S(accp[i] * R(smat[e * 4 + 0])), qe[0], re[0]);
       };
       auto out_u = [&]() {
-        const R irho = smat[e * 4 + 1];
+        const R irho = R(smat[e * 4 + 1]);
 #pragma unroll
         for (int x = 0; x < 3; ++x)
-          qe[(1 + x) * L::QF] = epilogue_q<R>(E, T, base + (1 + x) * NP, acc[x][i] * irho,
+          qe[(1 + x) * L::QF] = epilogue_q<S>(E, T, base + (1 + x) * NP, S(acc[x][i] * irho),
                                               qe[(1 + x) * L::QF], re[(1 + x) * L::QF]);
       };
       if (L::SPLIT) {
@@ -385,7 +392,7 @@ __global__ void __launch_bounds__(DMma<N, T>::NTH)
   if (E.mode != MODE_RHS && M.tr_out[T] != nullptr) {
     __syncthreads();
     const R* Ep = (const R*)TY.op[7];   // [RTF][NPK/4][32] trace-operator fragments
-    R* tro = (R*)M.tr_out[T];
+    S* tro = (S*)M.tr_out[T];
     // columns: (element, field) pairs, col = e*4 + c; 4 column tiles for
     // E = 8.  One row tile per warp pass, each A fragment feeds 4 MMAs.
     const int er = lane >> 2;
@@ -411,10 +418,10 @@ __global__ void __launch_bounds__(DMma<N, T>::NTH)
           const int e = c0 >> 2;
           if (e >= ne) continue;
           R s = R(1);
-          if (T == HW_WEDGE) s = sg[e * L::GEOS + 9];
-          R* o = tro + (size_t)sk[e] * 4 * NFP + j;
-          o[(c0 & 3) * NFP] = y[cf][0] * s;
-          o[((c0 & 3) + 1) * NFP] = y[cf][1] * s;
+          if (T == HW_WEDGE) s = R(sg[e * L::GEOS + 9]);
+          S* o = tro + (size_t)sk[e] * 4 * NFP + j;
+          o[(c0 & 3) * NFP] = S(y[cf][0] * s);
+          o[((c0 & 3) + 1) * NFP] = S(y[cf][1] * s);
         }
       }
     }

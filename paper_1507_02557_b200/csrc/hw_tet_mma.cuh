@@ -1,5 +1,6 @@
 // Tet RHS + update with the dense contractions on the fp64 tensor cores
-// (mma.sync.m8n8k4.f64, SASS DMMA), fp64 only.
+// (mma.sync.m8n8k4.f64, SASS DMMA); state storage fp64 or fp32, arithmetic
+// fp64 (fp32 storage rounds once, at the store).
 //
 // A block owns E tets; warp w owns one 8x8 output tile (row tile = 8 nodes,
 // column tile = 8 elements).  All per-element smem arrays are element-major
@@ -33,6 +34,14 @@ __host__ __device__ constexpr int stride4mod16(int n) {   // smallest s >= n, s 
   return n + ((4 - n % 16) + 16) % 16;
 }
 
+// element stride (in storage scalars) that makes a B-fragment load (4
+// consecutive k x 8 elements) conflict-free: fp64 4 (mod 16) doubles, fp32
+// 4 (mod 8) floats (one 128-byte wavefront); both keep 16-byte row alignment
+template <typename S>
+__host__ __device__ constexpr int frag_stride(int n) {
+  return sizeof(S) == 8 ? stride4mod16(n) : n + ((4 - n % 8) + 8) % 8;
+}
+
 // elements per block (tuning: HW_TET_E2 / HW_TET_E4 for N = 2 / 4)
 #ifndef HW_TET_E2
 #define HW_TET_E2 16
@@ -44,7 +53,9 @@ __host__ __device__ constexpr int stride4mod16(int n) {   // smallest s >= n, s 
 #define HW_TET_MINB 6
 #endif
 
-template <int N>
+// S: storage type of the state, records and smem (double or float); the
+// arithmetic is fp64 throughout (DMMA), fp32 storage rounds at the store
+template <int N, typename S = double>
 struct TetMma {
   using D = Dims<N>;
   static constexpr int NP = D::NP_TET, NFN = D::NFN, NFP = 4 * D::NFN;
@@ -55,25 +66,25 @@ struct TetMma {
   static constexpr int NFK = ((NFN + 3) / 4) * 4;
   static constexpr int W = RT * CT;
   static constexpr int NTH = 32 * W;
-  static constexpr bool VEC = (NP % 2 == 0) && (NPK == NP);  // 16-byte row copies
-  static constexpr int EQ = stride4mod16(4 * NPK);          // q / res element stride
-  static constexpr int EV = stride4mod16(3 * NPK);          // v_c
-  static constexpr int EF = stride4mod16(4 * NFK);          // fp / fu
+  static constexpr bool VEC = (NPK == NP) && ((4 * NP * sizeof(S)) % 16 == 0);  // 16-byte rows
+  static constexpr int EQ = frag_stride<S>(4 * NPK);        // q / res element stride
+  static constexpr int EV = frag_stride<S>(3 * NPK);        // v_c
+  static constexpr int EF = frag_stride<S>(4 * NFK);        // fp / fu
   // buffers live in disjoint phases share storage: v_c (volume) with fp/fu
   // (flux, lift)
   static constexpr int RA = cmax(EV, 2 * EF);
   static constexpr int SQ = 0, SV = SQ + E * EQ, SFP = SV, SFU = SFP + E * EF,
                        SRES = SV + E * RA, SG = SRES + E * EQ,
                        SMAT = SG + E * GEO_TET, TOTAL = SMAT + E * 4;
-  static constexpr size_t BYTES = sizeof(double) * TOTAL + sizeof(int) * (E + NFP);
+  static constexpr size_t BYTES = sizeof(S) * TOTAL + sizeof(int) * (E + NFP);
   static constexpr int MINB = (W <= 4) ? HW_TET_MINB : ((W <= 8) ? 3 : 1);
   // flux items (element, face point) per thread
   static constexpr int IT = (E * NFP + NTH - 1) / NTH;
 };
 
 // element rows (K, 4, NP) -> smem [e][field (stride NPK)][node]
-template <typename L>
-__device__ __forceinline__ void tet_rows(double* dst, const double* src, const int* sk, int ne) {
+template <typename L, typename S>
+__device__ __forceinline__ void tet_rows(S* dst, const S* src, const int* sk, int ne) {
   constexpr int NP = L::NP, NPK = L::NPK;
   if (L::VEC) {
     copy_rows16<4 * NP, L::EQ, L::NTH, L::E>(dst, src, sk, ne);
@@ -86,25 +97,25 @@ __device__ __forceinline__ void tet_rows(double* dst, const double* src, const i
   }
 }
 
-template <int N>
-__global__ void __launch_bounds__(TetMma<N>::NTH, TetMma<N>::MINB)
+template <int N, typename S>
+__global__ void __launch_bounds__(TetMma<N, S>::NTH, TetMma<N, S>::MINB)
     tet_mma_kernel(hw_mesh_t M, hw_fields_t Q, Epi E, const int32_t* __restrict__ list,
                    int64_t nwork) {
-  using L = TetMma<N>;
-  using R = double;
+  using L = TetMma<N, S>;
+  using R = double;   // arithmetic
   constexpr int NP = L::NP, NFN = L::NFN, NFP = L::NFP, EB = L::E, NPK = L::NPK,
                 NFK = L::NFK, NTH = L::NTH, EQ = L::EQ, EV = L::EV, EF = L::EF, IT = L::IT;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  R* sm = reinterpret_cast<R*>(smem_raw);
+  S* sm = reinterpret_cast<S*>(smem_raw);
   int* sk = reinterpret_cast<int*>(sm + L::TOTAL);
   int* sfn = sk + EB;               // own face node table
-  R* sq = sm + L::SQ;
-  R* sres = sm + L::SRES;
-  R* sv = sm + L::SV;
-  R* sfp = sm + L::SFP;
-  R* sfu = sm + L::SFU;
-  R* sg = sm + L::SG;
-  R* smat = sm + L::SMAT;
+  S* sq = sm + L::SQ;
+  S* sres = sm + L::SRES;
+  S* sv = sm + L::SV;
+  S* sfp = sm + L::SFP;
+  S* sfu = sm + L::SFU;
+  S* sg = sm + L::SG;
+  S* smat = sm + L::SMAT;
 
   const hw_type_t& TY = M.t[HW_TET];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -120,18 +131,18 @@ __global__ void __launch_bounds__(TetMma<N>::NTH, TetMma<N>::MINB)
     for (int i = tid; i < EB * 11 * PADN; i += NTH) {
       const int e = i / (11 * PADN), r = i - e * 11 * PADN;
       const int fld = r / PADN, n = NP + r - fld * PADN;
-      if (fld < 4) sq[e * EQ + fld * NPK + n] = R(0);
-      else if (fld >= 8) sv[e * EV + (fld - 8) * NPK + n] = R(0);
+      if (fld < 4) sq[e * EQ + fld * NPK + n] = S(0);
+      else if (fld >= 8) sv[e * EV + (fld - 8) * NPK + n] = S(0);
     }
   __syncthreads();
 
   // ---- P0: element rows, records; the gather index straight into
   // registers (thread-item u is (e, j) = (tid + u * NTH) / NFP, % NFP, the
   // mapping the flux loop uses)
-  const R* q = (const R*)Q.p[HW_TET];
+  const S* q = (const S*)Q.p[HW_TET];
   tet_rows<L>(sq, q, sk, ne);
-  copy_rows<GEO_TET, GEO_TET, NTH, EB>(sg, (const R*)TY.geo, sk, ne);
-  copy_rows<4, 4, NTH, EB>(smat, (const R*)TY.mat, sk, ne);
+  copy_rows<GEO_TET, GEO_TET, NTH, EB>(sg, (const S*)TY.geo, sk, ne);
+  copy_rows<4, 4, NTH, EB>(smat, (const S*)TY.mat, sk, ne);
   int gv[IT];
 #pragma unroll
   for (int u = 0; u < IT; ++u) {
@@ -150,26 +161,26 @@ __global__ void __launch_bounds__(TetMma<N>::NTH, TetMma<N>::MINB)
     const int g = gv[u];
     if (g >= 0) {
 #pragma unroll
-      for (int c = 0; c < 4; ++c) nb[u][c] = ldg(q + (size_t)g + c * NP);
+      for (int c = 0; c < 4; ++c) nb[u][c] = R(ldg(q + (size_t)g + c * NP));
     } else if (g != -1) {   // pyramid / wedge neighbour: its published face trace
       const unsigned v = (unsigned)(-3 - g);
       const int t2 = (v & 1u) ? HW_WEDGE : HW_PYRAMID;
       const int nfp2 = (v & 1u) ? Dims<N>::NFP_WEDGE : Dims<N>::NFP_PYR;
-      const R* src = (const R*)M.tr_in[t2] + (size_t)(v >> 1);
+      const S* src = (const S*)M.tr_in[t2] + (size_t)(v >> 1);
 #pragma unroll
-      for (int c = 0; c < 4; ++c) nb[u][c] = ldg(src + c * nfp2);
+      for (int c = 0; c < 4; ++c) nb[u][c] = R(ldg(src + c * nfp2));
     }
   }
 
   // v_c = sum_x G[c][x] u_x
   for (int i = tid; i < ne * NP; i += NTH) {
     const int e = i / NP, n = i - e * NP;
-    const R* G = sg + e * GEO_TET;
-    const R* u = sq + e * EQ + n;
+    const S* G = sg + e * GEO_TET;
+    const S* u = sq + e * EQ + n;
     const R u0 = u[NPK], u1 = u[2 * NPK], u2 = u[3 * NPK];
 #pragma unroll
     for (int c = 0; c < 3; ++c)
-      sv[e * EV + c * NPK + n] = G[c * 3] * u0 + G[c * 3 + 1] * u1 + G[c * 3 + 2] * u2;
+      sv[e * EV + c * NPK + n] = S(R(G[c * 3]) * u0 + R(G[c * 3 + 1]) * u1 + R(G[c * 3 + 2]) * u2);
   }
   __syncthreads();
 
@@ -179,8 +190,8 @@ __global__ void __launch_bounds__(TetMma<N>::NTH, TetMma<N>::MINB)
   R dp[3][2] = {{0, 0}, {0, 0}, {0, 0}}, dv[2] = {0, 0};
   {
     const R* Dg = (const R*)TY.op[2];   // [3][RT][NPK/4][32] A fragments, zero padded
-    const R* bq = sq + bcol * EQ + bk;
-    const R* bv = sv + bcol * EV + bk;
+    const S* bq = sq + bcol * EQ + bk;
+    const S* bv = sv + bcol * EV + bk;
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
 #pragma unroll
@@ -198,7 +209,7 @@ __global__ void __launch_bounds__(TetMma<N>::NTH, TetMma<N>::MINB)
     for (int i = tid; i < EB * 8 * PADF; i += NTH) {
       const int e = i / (8 * PADF), r = i - e * 8 * PADF;
       const int fld = r / PADF, n = NFN + r - fld * PADF;
-      (fld < 4 ? sfp : sfu)[e * EF + (fld & 3) * NFK + n] = R(0);
+      (fld < 4 ? sfp : sfu)[e * EF + (fld & 3) * NFK + n] = S(0);
     }
   const R pen = R(M.penalty_scale);
 #pragma unroll
@@ -208,10 +219,10 @@ __global__ void __launch_bounds__(TetMma<N>::NTH, TetMma<N>::MINB)
     const int e = i / NFP, j = i - e * NFP;
     const int f = j / NFN, jj = j - f * NFN;
     const int node = sfn[j];
-    const R* qe = sq + e * EQ + node;
+    const S* qe = sq + e * EQ + node;
     const R pm = qe[0];
     const R um[3] = {qe[NPK], qe[2 * NPK], qe[3 * NPK]};
-    const R* g = sg + e * GEO_TET + 9 + FS * f;
+    const S* g = sg + e * GEO_TET + 9 + FS * f;
     const R nrm[3] = {g[0], g[1], g[2]};
     R pp, up[3];
     if (gv[u] != -1) {
@@ -220,15 +231,15 @@ __global__ void __launch_bounds__(TetMma<N>::NTH, TetMma<N>::MINB)
       pp = -pm; up[0] = um[0]; up[1] = um[1]; up[2] = um[2];
     }
     R tp, tu, fp, fu;
-    penalties(g[4], g[5], pen, tp, tu);
+    penalties(R(g[4]), R(g[5]), pen, tp, tu);
     upwind_flux(pm, um, pp, up, nrm, tp, tu, false, fp, fu);
-    sfp[e * EF + f * NFK + jj] = fp * g[3];
-    sfu[e * EF + f * NFK + jj] = fu * g[3];
+    sfp[e * EF + f * NFK + jj] = S(fp * R(g[3]));
+    sfu[e * EF + f * NFK + jj] = S(fu * R(g[3]));
   }
   __syncthreads();
   // LSRK residual rows, fetched behind the lift GEMM
   if (lsrk) {
-    tet_rows<L>(sres, (const R*)E.res[HW_TET], sk, ne);
+    tet_rows<L>(sres, (const S*)E.res[HW_TET], sk, ne);
     cp_async_commit();
   }
 
@@ -238,15 +249,15 @@ __global__ void __launch_bounds__(TetMma<N>::NTH, TetMma<N>::MINB)
   R accu[3][2];
 #pragma unroll
   for (int i = 0; i < 2; ++i) {
-    const R* G = sg + (col0 + i) * GEO_TET;
+    const S* G = sg + (col0 + i) * GEO_TET;
 #pragma unroll
     for (int x = 0; x < 3; ++x)
-      accu[x][i] = -(G[x] * dp[0][i] + G[3 + x] * dp[1][i] + G[6 + x] * dp[2][i]);
+      accu[x][i] = -(R(G[x]) * dp[0][i] + R(G[3 + x]) * dp[1][i] + R(G[6 + x]) * dp[2][i]);
   }
   {
     const R* Lg = (const R*)TY.op[3];   // [4][RT][NFK/4][32] A fragments
-    const R* bp = sfp + bcol * EF + bk;
-    const R* bu = sfu + bcol * EF + bk;
+    const S* bp = sfp + bcol * EF + bk;
+    const S* bu = sfu + bcol * EF + bk;
 #pragma unroll
     for (int f = 0; f < 4; ++f) {
       R tu[2] = {0, 0};
@@ -258,10 +269,10 @@ __global__ void __launch_bounds__(TetMma<N>::NTH, TetMma<N>::MINB)
       }
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
-        const R* g = sg + (col0 + i) * GEO_TET + 9 + FS * f;
-        accu[0][i] += g[0] * tu[i];
-        accu[1][i] += g[1] * tu[i];
-        accu[2][i] += g[2] * tu[i];
+        const S* g = sg + (col0 + i) * GEO_TET + 9 + FS * f;
+        accu[0][i] += R(g[0]) * tu[i];
+        accu[1][i] += R(g[1]) * tu[i];
+        accu[2][i] += R(g[2]) * tu[i];
       }
     }
   }
@@ -277,12 +288,12 @@ __global__ void __launch_bounds__(TetMma<N>::NTH, TetMma<N>::MINB)
       if (e >= ne) continue;
       const R kap = smat[e * 4 + 0], irho = smat[e * 4 + 1];
       const size_t base = (size_t)sk[e] * 4 * NP + n;
-      const R* qe = sq + e * EQ + n;
-      const R* re = sres + e * EQ + n;
-      epilogue_s<R>(E, HW_TET, base, accp[i] * kap, qe[0], re[0]);
+      const S* qe = sq + e * EQ + n;
+      const S* re = sres + e * EQ + n;
+      epilogue_s<S>(E, HW_TET, base, S(accp[i] * kap), qe[0], re[0]);
 #pragma unroll
       for (int x = 0; x < 3; ++x)
-        epilogue_s<R>(E, HW_TET, base + (1 + x) * NP, accu[x][i] * irho, qe[(1 + x) * NPK],
+        epilogue_s<S>(E, HW_TET, base + (1 + x) * NP, S(accu[x][i] * irho), qe[(1 + x) * NPK],
                       re[(1 + x) * NPK]);
     }
   }

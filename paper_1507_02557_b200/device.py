@@ -191,6 +191,10 @@ def pack_mesh(disc):
     return pack
 
 
+# operator slots read as fp64 DMMA fragments by the tensor-core kernels
+MMA_SLOTS = {"hex": (), "tet": (2, 3), "wedge": (2, 3, 4, 7), "pyramid": (2, 3, 4, 7)}
+
+
 def mma_fragments(A):
     """(..., 8*RT, 4*KS) row-major padded matrix -> (..., RT, KS, 32): the
     mma.m8n8k4 A fragment of row tile rt and k-step ks in lane order
@@ -380,7 +384,8 @@ class DeviceMesh:
             T.nbr_elem = self._put(P["nbr_elem"], torch.int32)
             T.nbr_code = self._put(P["nbr_code"], torch.int32)
             for slot, arr in P["op"].items():
-                T.op[slot] = self._put(arr)
+                # DMMA operand fragments are fp64 for both storage precisions
+                T.op[slot] = self._put(arr, torch.float64 if slot in MMA_SLOTS[t] else None)
             for slot, arr in P["iop"].items():
                 T.iop[slot] = self._put(arr, torch.int32)
         S.perm_tri = self._put(pack["perm_tri"], torch.int32)
