@@ -81,6 +81,13 @@ struct DMma {
                        STR = SV + E * RA, SRES = STR,
                        SG = STR + E * RB, SMAT = SG + E * GEOS, TOTAL = SMAT + E * 4;
   static constexpr size_t BYTES = sizeof(S) * TOTAL + sizeof(int) * (E + E * NF);
+#ifndef HW_DENSE_MINB
+#define HW_DENSE_MINB 1
+#endif
+#ifndef HW_DENSE_MINB32
+#define HW_DENSE_MINB32 1
+#endif
+  static constexpr int MINB = sizeof(S) == 8 ? HW_DENSE_MINB : HW_DENSE_MINB32;
 };
 
 // element rows (K, 4, NP) -> smem [e][field (stride QF)][node]
@@ -106,7 +113,7 @@ __device__ __forceinline__ void copy_q_rows(S* dst, const S* src, const int* sk,
 }
 
 template <int N, int T, typename S>
-__global__ void __launch_bounds__(DMma<N, T, S>::NTH)
+__global__ void __launch_bounds__(DMma<N, T, S>::NTH, DMma<N, T, S>::MINB)
     dense_mma_kernel(hw_mesh_t M, hw_fields_t Q, Epi E, const int32_t* __restrict__ list,
                      int64_t nwork) {
   using L = DMma<N, T, S>;

@@ -52,6 +52,9 @@ __host__ __device__ constexpr int frag_stride(int n) {
 #ifndef HW_TET_MINB
 #define HW_TET_MINB 6
 #endif
+#ifndef HW_TET_MINB32
+#define HW_TET_MINB32 12
+#endif
 
 // S: storage type of the state, records and smem (double or float); the
 // arithmetic is fp64 throughout (DMMA), fp32 storage rounds at the store
@@ -77,7 +80,8 @@ struct TetMma {
                        SRES = SV + E * RA, SG = SRES + E * EQ,
                        SMAT = SG + E * GEO_TET, TOTAL = SMAT + E * 4;
   static constexpr size_t BYTES = sizeof(S) * TOTAL + sizeof(int) * (E + NFP);
-  static constexpr int MINB = (W <= 4) ? HW_TET_MINB : ((W <= 8) ? 3 : 1);
+  static constexpr int MINB = (W <= 4) ? (sizeof(S) == 8 ? HW_TET_MINB : HW_TET_MINB32)
+                                       : ((W <= 8) ? 3 : 1);
   // flux items (element, face point) per thread
   static constexpr int IT = (E * NFP + NTH - 1) / NTH;
 };
