@@ -147,9 +147,14 @@ static int launch_dense_mma(const hw_mesh_t& M, const hw_fields_t& Q, const Epi&
   } else {
   int rc;
   const size_t bytes = L::BYTES > smem_floor() ? L::BYTES : smem_floor();
-  if ((rc = set_smem(dense_mma_kernel<N, T, R>, bytes))) return rc;
-  dense_mma_kernel<N, T, R><<<(unsigned)((n + L::E - 1) / L::E), L::NTH, bytes, st>>>(M, Q, E,
-                                                                                 list, n);
+  const unsigned grid = (unsigned)((n + L::E - 1) / L::E);
+  if (L::SPLIT) {
+    if ((rc = set_smem(dense_mma_kernel<N, T, R>, bytes))) return rc;
+    dense_mma_kernel<N, T, R><<<grid, L::NTH, bytes, st>>>(M, Q, E, list, n);
+  } else {
+    if ((rc = set_smem(dense_mma_kernel_big<N, T, R>, bytes))) return rc;
+    dense_mma_kernel_big<N, T, R><<<grid, L::NTH, bytes, st>>>(M, Q, E, list, n);
+  }
   return check_launch("dense_mma_kernel");
   }
 }

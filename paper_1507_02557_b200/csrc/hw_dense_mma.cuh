@@ -81,11 +81,14 @@ struct DMma {
                        STR = SV + E * RA, SRES = STR,
                        SG = STR + E * RB, SMAT = SG + E * GEOS, TOTAL = SMAT + E * 4;
   static constexpr size_t BYTES = sizeof(S) * TOTAL + sizeof(int) * (E + E * NF);
+  // blocks per SM the register allocation targets (split layouts; the
+  // large-RT layouts use the compiler's default heuristic, see
+  // dense_mma_kernel_big: an explicit 1 would let it take 150+ registers)
 #ifndef HW_DENSE_MINB
-#define HW_DENSE_MINB 1
+#define HW_DENSE_MINB 3
 #endif
 #ifndef HW_DENSE_MINB32
-#define HW_DENSE_MINB32 1
+#define HW_DENSE_MINB32 4
 #endif
   static constexpr int MINB = sizeof(S) == 8 ? HW_DENSE_MINB : HW_DENSE_MINB32;
 };
@@ -113,9 +116,9 @@ __device__ __forceinline__ void copy_q_rows(S* dst, const S* src, const int* sk,
 }
 
 template <int N, int T, typename S>
-__global__ void __launch_bounds__(DMma<N, T, S>::NTH, DMma<N, T, S>::MINB)
-    dense_mma_kernel(hw_mesh_t M, hw_fields_t Q, Epi E, const int32_t* __restrict__ list,
-                     int64_t nwork) {
+__device__ __forceinline__ void dense_mma_body(const hw_mesh_t& M, const hw_fields_t& Q,
+                                               const Epi& E, const int32_t* __restrict__ list,
+                                               int64_t nwork) {
   using L = DMma<N, T, S>;
   using X = TT<N, T>;
   using R = double;
@@ -433,6 +436,22 @@ __global__ void __launch_bounds__(DMma<N, T, S>::NTH, DMma<N, T, S>::MINB)
       }
     }
   }
+}
+
+// split layouts (RT <= HW_DENSE_SPLIT_MAX_RT): register target from MINB
+template <int N, int T, typename S>
+__global__ void __launch_bounds__(DMma<N, T, S>::NTH, DMma<N, T, S>::MINB)
+    dense_mma_kernel(hw_mesh_t M, hw_fields_t Q, Epi E, const int32_t* __restrict__ list,
+                     int64_t nwork) {
+  dense_mma_body<N, T, S>(M, Q, E, list, nwork);
+}
+
+// large-RT layouts: compiler's default register heuristic
+template <int N, int T, typename S>
+__global__ void __launch_bounds__(DMma<N, T, S>::NTH)
+    dense_mma_kernel_big(hw_mesh_t M, hw_fields_t Q, Epi E, const int32_t* __restrict__ list,
+                         int64_t nwork) {
+  dense_mma_body<N, T, S>(M, Q, E, list, nwork);
 }
 
 }  // namespace hw
