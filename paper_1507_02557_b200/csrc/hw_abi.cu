@@ -168,6 +168,24 @@ static int launch_traces_t(const hw_mesh_t& M, const hw_fields_t& Q, const hw_fi
   return check_launch("trace_kernel");
 }
 
+// wedge / pyramid traces on DMMA (scalar kernel where the DMMA layout
+// does not fit a block)
+template <int N, int T, typename R>
+static int launch_traces_mma(const hw_mesh_t& M, const hw_fields_t& Q, const hw_fields_t& TR,
+                             const int32_t* list, int64_t n, cudaStream_t st) {
+  using L = DMma<N, T, R>;
+  if constexpr (L::NTH > 1024) {
+    return launch_traces_t<N, T, R>(M, Q, TR, list, n, st);
+  } else {
+    constexpr size_t bytes = sizeof(R) * (L::E * (L::EQ + L::GEOS) + 2) + sizeof(int) * L::E;
+    int rc;
+    if ((rc = set_smem(trace_mma_kernel<N, T, R>, bytes))) return rc;
+    trace_mma_kernel<N, T, R><<<(unsigned)((n + L::E - 1) / L::E), L::NTH, bytes, st>>>(
+        M, Q, TR, list, n);
+    return check_launch("trace_mma_kernel");
+  }
+}
+
 // face traces of every publishing type (wedge, pyramid, GL hex) of q -> TR
 template <int N, typename R>
 static int launch_traces_all(const hw_mesh_t& M, const hw_fields_t& Q, const hw_fields_t& TR,
@@ -184,8 +202,8 @@ static int launch_traces_all(const hw_mesh_t& M, const hw_fields_t& Q, const hw_
     subset_of(sub, t, K, &list, &n);
     if (n <= 0) continue;
     if (t == HW_HEX) rc = launch_traces_t<N, HW_HEX, R>(M, Q, TR, list, n, st);
-    else if (t == HW_WEDGE) rc = launch_traces_t<N, HW_WEDGE, R>(M, Q, TR, list, n, st);
-    else rc = launch_traces_t<N, HW_PYRAMID, R>(M, Q, TR, list, n, st);
+    else if (t == HW_WEDGE) rc = launch_traces_mma<N, HW_WEDGE, R>(M, Q, TR, list, n, st);
+    else rc = launch_traces_mma<N, HW_PYRAMID, R>(M, Q, TR, list, n, st);
     if (rc) return rc;
   }
   return 0;

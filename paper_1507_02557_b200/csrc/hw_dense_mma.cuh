@@ -115,6 +115,49 @@ __device__ __forceinline__ void copy_q_rows(S* dst, const S* src, const int* sk,
   }
 }
 
+// TR = E q for the block's elements, q in smem ([e][field (stride QF)]
+// [node], K padding zero): DMMA with the element-field pairs as columns (4
+// column tiles for E = 8), one row tile of face points per warp pass, each
+// A fragment feeding 4 MMAs.  Wedges scale by 1/sqrt(J) (record word 9).
+template <typename L, int T, typename S>
+__device__ __forceinline__ void publish_mma(const hw_type_t& TY, const S* sq, const S* sg,
+                                            const int* sk, int ne, S* tro) {
+  using R = double;
+  constexpr int NFP = L::NFP;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int er = lane >> 2, bk = lane & 3;
+  const R* Ep = (const R*)TY.op[7];   // [RTF][NPK/4][32] trace-operator fragments
+  for (int rf = warp; rf < L::RTF; rf += L::W) {
+    R y[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
+    const R* arow_p = Ep + ((rf * L::KPP) << 6) + 2 * lane;
+    double2 pr;
+#pragma unroll
+    for (int ks = 0; ks < L::KSP; ++ks) {
+      if (!(ks & 1)) pr = ldg2(arow_p + ((ks >> 1) << 6));
+      const R a = (ks & 1) ? pr.y : pr.x;
+#pragma unroll
+      for (int cf = 0; cf < 4; ++cf) {
+        const int col = cf * 8 + er;
+        dmma884(y[cf][0], y[cf][1], a, sq[(col >> 2) * L::EQ + (col & 3) * L::QF + bk + ks * 4]);
+      }
+    }
+    const int j = rf * 8 + er;
+    if (j < NFP) {
+#pragma unroll
+      for (int cf = 0; cf < 4; ++cf) {
+        const int c0 = cf * 8 + (lane & 3) * 2;      // output columns c0, c0+1
+        const int e = c0 >> 2;
+        if (e >= ne) continue;
+        R s = R(1);
+        if (T == HW_WEDGE) s = R(sg[e * L::GEOS + 9]);
+        S* o = tro + (size_t)sk[e] * 4 * NFP + j;
+        o[(c0 & 3) * NFP] = S(y[cf][0] * s);
+        o[((c0 & 3) + 1) * NFP] = S(y[cf][1] * s);
+      }
+    }
+  }
+}
+
 template <int N, int T, typename S>
 __device__ __forceinline__ void dense_mma_body(const hw_mesh_t& M, const hw_fields_t& Q,
                                                const Epi& E, const int32_t* __restrict__ list,
@@ -401,40 +444,7 @@ __device__ __forceinline__ void dense_mma_body(const hw_mesh_t& M, const hw_fiel
   // ---- publish the traces of the new state: TR = E q_out
   if (E.mode != MODE_RHS && M.tr_out[T] != nullptr) {
     __syncthreads();
-    const R* Ep = (const R*)TY.op[7];   // [RTF][NPK/4][32] trace-operator fragments
-    S* tro = (S*)M.tr_out[T];
-    // columns: (element, field) pairs, col = e*4 + c; 4 column tiles for
-    // E = 8.  One row tile per warp pass, each A fragment feeds 4 MMAs.
-    const int er = lane >> 2;
-    for (int rf = warp; rf < L::RTF; rf += L::W) {
-      R y[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
-      const R* arow_p = Ep + ((rf * L::KPP) << 6) + 2 * lane;
-      double2 pr;
-#pragma unroll
-      for (int ks = 0; ks < L::KSP; ++ks) {
-        if (!(ks & 1)) pr = ldg2(arow_p + ((ks >> 1) << 6));
-        const R a = (ks & 1) ? pr.y : pr.x;
-#pragma unroll
-        for (int cf = 0; cf < 4; ++cf) {
-          const int col = cf * 8 + er;
-          dmma884(y[cf][0], y[cf][1], a, sq[(col >> 2) * EQ + (col & 3) * L::QF + bk + ks * 4]);
-        }
-      }
-      const int j = rf * 8 + er;
-      if (j < NFP) {
-#pragma unroll
-        for (int cf = 0; cf < 4; ++cf) {
-          const int c0 = cf * 8 + (lane & 3) * 2;      // output columns c0, c0+1
-          const int e = c0 >> 2;
-          if (e >= ne) continue;
-          R s = R(1);
-          if (T == HW_WEDGE) s = R(sg[e * L::GEOS + 9]);
-          S* o = tro + (size_t)sk[e] * 4 * NFP + j;
-          o[(c0 & 3) * NFP] = S(y[cf][0] * s);
-          o[((c0 & 3) + 1) * NFP] = S(y[cf][1] * s);
-        }
-      }
-    }
+    publish_mma<L, T, S>(TY, sq, sg, sk, ne, (S*)M.tr_out[T]);
   }
 }
 
@@ -452,6 +462,38 @@ __global__ void __launch_bounds__(DMma<N, T, S>::NTH)
     dense_mma_kernel_big(hw_mesh_t M, hw_fields_t Q, Epi E, const int32_t* __restrict__ list,
                          int64_t nwork) {
   dense_mma_body<N, T, S>(M, Q, E, list, nwork);
+}
+
+// Face traces of q (hw_traces) for wedges / pyramids on DMMA: the
+// epilogue's trace GEMM on the input rows.
+template <int N, int T, typename S>
+__global__ void __launch_bounds__(DMma<N, T, S>::NTH)
+    trace_mma_kernel(hw_mesh_t M, hw_fields_t Q, hw_fields_t TR, const int32_t* __restrict__ list,
+                     int64_t nwork) {
+  using L = DMma<N, T, S>;
+  constexpr int NP = L::NP, NPK = L::NPK, EB = L::E;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  S* sq = reinterpret_cast<S*>(smem_raw);
+  S* sg = sq + EB * L::EQ;
+  int* sk = reinterpret_cast<int*>(sg + EB * L::GEOS + 2);
+  const hw_type_t& TY = M.t[T];
+  const int tid = threadIdx.x;
+  const int64_t w0 = (int64_t)blockIdx.x * EB;
+  const int ne = (int)((nwork - w0) < EB ? (nwork - w0) : EB);
+  if (tid < EB) sk[tid] = tid < ne ? (list ? list[w0 + tid] : (int)(w0 + tid)) : 0;
+  constexpr int PADN = (NPK > NP) ? NPK - NP : 1;
+  if (NPK > NP)
+    for (int i = tid; i < EB * 4 * PADN; i += L::NTH) {
+      const int e = i / (4 * PADN), r = i - e * 4 * PADN;
+      sq[e * L::EQ + (r / PADN) * L::QF + NP + r % PADN] = S(0);
+    }
+  __syncthreads();
+  copy_q_rows<L>(sq, (const S*)Q.p[T], sk, ne);
+  if (T == HW_WEDGE) copy_rows<L::GEO, L::GEOS, L::NTH, EB>(sg, (const S*)TY.geo, sk, ne);
+  cp_async_commit();
+  cp_async_wait_all();
+  __syncthreads();
+  publish_mma<L, T, S>(TY, sq, sg, sk, ne, (S*)TR.p[T]);
 }
 
 }  // namespace hw
