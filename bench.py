@@ -474,12 +474,37 @@ def partitioned(args, world, rank, local, dev, dtype, s_bytes):
         e1.record(stream)
         torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
-    tt = torch.tensor([ms, float(ps.n_dof_owned)], device=dev, dtype=torch.float64)
+    # end to end: this rank's state from pinned host memory into HBM, the
+    # steps, the owned state back to pinned host memory (max over ranks)
+    h_in = {t_: torch.empty(ps.S.q[t_].shape, dtype=ps.S.q[t_].dtype, pin_memory=True)
+            for t_ in dl.types}
+    for t_ in dl.types:
+        h_in[t_].copy_(ps.S.q[t_])
+    h_out = {t_: torch.empty(ps.owned_state()[t_].shape, dtype=ps.S.q[t_].dtype,
+                             pin_memory=True) for t_ in dl.types}
+    torch.cuda.synchronize()
+    dist.barrier()
+    x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2e_steps = max(2, min(args.steps, 20))
+    x0.record(stream)
+    for t_ in dl.types:
+        ps.S.q[t_].copy_(h_in[t_], non_blocking=True)
+    for _ in range(e2e_steps):
+        ps.lsrk_step(dt)
+    own = ps.owned_state()
+    for t_ in dl.types:
+        h_out[t_].copy_(own[t_], non_blocking=True)
+    x1.record(stream)
+    torch.cuda.synchronize()
+    ms_e2e = x0.elapsed_time(x1)
+    tt = torch.tensor([ms, float(ps.n_dof_owned), ms_e2e], device=dev, dtype=torch.float64)
     mx = tt.clone()
     dist.all_reduce(mx, op=dist.ReduceOp.MAX)
     sm_ = tt.clone()
     dist.all_reduce(sm_, op=dist.ReduceOp.SUM)
-    ms, total_dof = float(mx[0]), float(sm_[1])
+    ms, total_dof, ms_e2e = float(mx[0]), float(sm_[1]), float(mx[2])
+    h2d = sum(v.numel() * v.element_size() for v in h_in.values())
+    d2h = sum(v.numel() * v.element_size() for v in h_out.values())
     assert all(torch.isfinite(ps.S.q[t_]).all() for t_ in dl.types), "state diverged"
     value = total_dof * 5 * args.steps / (ms * 1e-3) / 1e9
     halo = sum(int(b - a) * 4 * dl.ops[t_].Np * s_bytes
@@ -499,8 +524,14 @@ def partitioned(args, world, rank, local, dev, dtype, s_bytes):
                            "parallelism": f"element partition x{world}, NCCL halo",
                            "cuda_graph": False,
                            "l2_policy": "inputs larger than L2"},
-                "gpu_launches": None, "clocks": clk.summary(), "roofline": None,
-                "e2e": None, "cpu_baseline": None}
+                "gpu_launches": ps.launches_per_stage() * 5 * args.steps,
+                "clocks": clk.summary(), "roofline": None,
+                "e2e": {"value": total_dof * 5 * e2e_steps / (ms_e2e * 1e-3) / 1e9, "unit": UNIT,
+                        "h2d_bytes_per_step": h2d / e2e_steps,
+                        "d2h_bytes_per_step": d2h / e2e_steps, "steps": e2e_steps,
+                        "api": "PartStepper.lsrk_step per rank, rank state H2D / owned "
+                               "state D2H (pinned) inside the timed region, max over ranks"},
+                "cpu_baseline": None}
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
     return 0

@@ -107,6 +107,19 @@ class PartStepper:
             transport.steppers[part.rank] = self
         self.n_dof_owned = sum(part.n_owned[t] * 4 * d.ops[t].Np for t in d.types)
 
+    def launches_per_stage(self):
+        """Kernel launches one stage issues (bench gpu_launches): halo packs,
+        interior and boundary stage kernels per present type, ghost traces
+        per publishing type with ghosts."""
+        d, p = self.disc, self.part
+        n = sum(len(per_t) for per_t in self.send_idx.values())
+        n += sum(1 for t in d.types if p.n_interior[t] > 0)
+        n += sum(1 for t in d.types if p.n_owned[t] > p.n_interior[t])
+        sem = d.formulation.kind == "SEM"
+        pub = ("wedge", "pyramid") if sem else ("hex", "wedge", "pyramid")
+        n += sum(1 for t in d.types if t in pub and d.n_elems[t] > p.n_owned[t])
+        return n
+
     def _pack(self, q):
         L, st = nat.lib(), self.disc.stream_ptr()
         dm = self.disc.device_mesh
