@@ -331,7 +331,7 @@ def hex_dominant_mesh(n, layers=(110, 4, 1, 5)):
     return layered_hybrid_mesh(n, ["hex"] * h + ["wedge"] * w + ["pyrtop"] * p + ["tet"] * t)
 
 
-def graded_hybrid_mesh(n, layers=None, ratio=0.5):
+def graded_hybrid_mesh(n, layers=None, ratio=0.5, nx=None):
     """BASELINE config 5 (not in the reference): the reference's band
     layout with geometrically graded z-spacing, finest in the pyramid/tet
     refinement zone, so local timesteps span several MRAB levels."""
@@ -345,7 +345,7 @@ def graded_hybrid_mesh(n, layers=None, ratio=0.5):
     s = s ** (np.log(1 / ratio) / np.log(2.0))
     zs = np.concatenate([[0.0], np.cumsum(s)]) / s.sum()
     return layered_hybrid_mesh(n, ["hex"] * h + ["wedge"] * w + ["pyrtop"] * p + ["tet"] * t,
-                               zs=zs)
+                               zs=zs, nx=nx)
 
 
 # ---------------------------------------------------------------- GMSH

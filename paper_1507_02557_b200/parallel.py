@@ -23,7 +23,7 @@ from .operators import TYPE_ID
 from .partition import build_local_parts, partition_elements
 from .timeint import LSRK_A, LSRK_B, Stepper
 
-__all__ = ["PartStepper", "NCCLTransport", "LoopbackTransport", "make_parts"]
+__all__ = ["PartStepper", "PartMRAB", "NCCLTransport", "LoopbackTransport", "make_parts"]
 
 
 def make_parts(mesh, nparts, method="xslab", N=3, ranks=None):
@@ -64,9 +64,10 @@ class LoopbackTransport:
     def start(self, ps, q):
         for peer, per_t in ps.part.recv.items():
             other = self.steppers[peer]
+            src = other.halo_source()
             for t, (a, b) in per_t.items():
                 src_idx = other.send_idx[ps.part.rank][t]
-                q[t][a:b].copy_(other.S.q[t][src_idx.long()])
+                q[t][a:b].copy_(src[t][src_idx.long()])
         return None
 
     def wait(self, handle):
@@ -106,6 +107,10 @@ class PartStepper:
         if isinstance(transport, LoopbackTransport):
             transport.steppers[part.rank] = self
         self.n_dof_owned = sum(part.n_owned[t] * 4 * d.ops[t].Np for t in d.types)
+
+    def halo_source(self):
+        """The state whose partition-boundary rows the peers receive."""
+        return self.S.q
 
     def launches_per_stage(self):
         """Kernel launches one stage issues (bench gpu_launches): halo packs,
@@ -164,3 +169,174 @@ class PartStepper:
 
     def owned_state(self):
         return {t: self.S.q[t][:self.part.n_owned[t]] for t in self.disc.types}
+
+
+class PartMRAB:
+    """Multi-rate AB3 (timeint.MRABDriver's tick pattern) on one rank's local
+    part.  Each tick: dense-output (effective) state of the owned elements
+    the tick reads plus the partition-boundary elements the peers read,
+    exchange of the boundary elements' effective state into the peers'
+    ghost rows, traces of the elements read, fused RHS + AB3 update of the
+    owned stepping elements.  Ghost elements never step; their history lives
+    on the owning rank, so every value a rank consumes equals the single-GPU
+    run's (tests/test_gpu_parity.py::test_partitioned_mrab_loopback)."""
+
+    def __init__(self, part, N, formulation, state_local, levels_local, n_levels, transport,
+                 dtype=torch.float64, device=None):
+        from .timeint import ab_coefficients   # noqa: F401 (used in tick)
+        self.part = part
+        self.transport = transport
+        self.disc = d = Discretization(part.mesh, N, formulation, dtype=dtype, device=device)
+        dev = d.device
+        self.L = L = int(n_levels)
+        self.levels = {t: np.asarray(levels_local[t]) for t in d.types}
+        self.q = d.to_device(state_local)
+        self.eff = d.empty_state()
+        self.ring = [d.zeros_state() for _ in range(3)]
+        self.n_hist = np.zeros(L + 1, dtype=int)
+        self.steps = np.zeros(L + 1, dtype=int)
+        self.send_idx = {peer: {t: torch.as_tensor(idx, dtype=torch.int32, device=dev)
+                                for t, idx in per_t.items()}
+                         for peer, per_t in part.send.items()}
+        self.sendbuf = {peer: {t: torch.empty((len(idx), 4, d.ops[t].Np), dtype=dtype, device=dev)
+                               for t, idx in per_t.items()}
+                        for peer, per_t in part.send.items()}
+        if isinstance(transport, LoopbackTransport):
+            transport.steppers[part.rank] = self
+        self._build_subsets()
+
+    def halo_source(self):
+        return self.eff
+
+    def _build_subsets(self):
+        d, part, L = self.disc, self.part, self.L
+        mesh = d.mesh
+        dev = d.device
+        names = ("hex", "wedge", "pyramid", "tet")
+        owned = {t: np.arange(d.n_elems[t]) < part.n_owned[t] for t in d.types}
+        sent = {t: np.zeros(d.n_elems[t], dtype=bool) for t in d.types}
+        for per_t in part.send.values():
+            for t, idx in per_t.items():
+                sent[t][idx] = True
+        # read set of level lev: its owned elements and their face neighbours
+        need = {}
+        for lev in range(1, L + 1):
+            own = {t: owned[t] & (self.levels[t] == lev) for t in d.types}
+            nd = {t: own[t].copy() for t in d.types}
+            for t in d.types:
+                nb = mesh.nbr[t][own[t]]
+                for tid2, t2 in enumerate(names):
+                    if t2 not in nd:
+                        continue
+                    sel = nb[:, :, 0] == tid2
+                    nd[t2][nb[:, :, 1][sel]] = True
+            need[lev] = nd
+        empty = torch.zeros(0, dtype=torch.int32, device=dev)
+
+        def sub(masks):
+            lists = [empty] * 4
+            for t in d.types:
+                idx = np.flatnonzero(masks[t]).astype(np.int32)
+                lists[TYPE_ID[t]] = torch.as_tensor(idx, device=dev) if len(idx) else empty
+            self._keep.append(lists)
+            self._ntypes[id(lists)] = sum(1 for x in lists if x.numel())
+            return nat.subset(lists), sum(int(x.numel()) for x in lists)
+
+        self._keep, self._ntypes, eff_types = [], {}, {}
+        self.eff_sub, self.trace_sub, self.step_sub = {}, {}, {}
+        for tick in range(2 ** (L - 1)):
+            stepping = [lev for lev in range(1, L + 1) if tick % (2 ** (L - lev)) == 0]
+            needed = {t: np.any([need[lev][t] for lev in stepping], axis=0) for t in d.types}
+            self.trace_sub[tick] = sub(needed)[0]
+            for lev in range(1, L + 1):
+                m = {t: (owned[t] & (needed[t] | sent[t])) & (self.levels[t] == lev)
+                     for t in d.types}
+                st, n = sub(m)
+                self.eff_sub[(tick, lev)] = st if n else None
+                eff_types[(tick, lev)] = self._ntypes[id(self._keep[-1])]
+        step_types = {}
+        for lev in range(1, L + 1):
+            st, n = sub({t: owned[t] & (self.levels[t] == lev) for t in d.types})
+            self.step_sub[lev] = st if n else None
+            step_types[lev] = self._ntypes[id(self._keep[-1])]
+        # kernel launches per macro step (bench gpu_launches): dense output,
+        # halo packs, traces (publishing types), stage kernels
+        sem = d.formulation.kind == "SEM"
+        pub = [t for t in d.types if t in (("wedge", "pyramid") if sem else ("hex", "wedge", "pyramid"))]
+        npack = sum(len(per_t) for per_t in part.send.values())
+        n = 0
+        for tick in range(2 ** (L - 1)):
+            stepping = [lev for lev in range(1, L + 1) if tick % (2 ** (L - lev)) == 0]
+            n += npack + len(pub) + sum(step_types[lev] for lev in stepping)
+            n += sum(eff_types[(tick, lev)] for lev in range(1, L + 1))
+        self.launches_per_macro = n
+
+    def _pack(self):
+        L_, st, dm = nat.lib(), self.disc.stream_ptr(), self.disc.device_mesh
+        for peer, per_t in self.send_idx.items():
+            for t, idx in per_t.items():
+                nat.check(L_.hw_halo_pack(dm.struct, TYPE_ID[t], self.eff[t].data_ptr(),
+                                          idx.data_ptr(), idx.numel(),
+                                          self.sendbuf[peer][t].data_ptr(), st))
+
+    def tick_effective(self, tick, dt_min):
+        """Dense output of this tick's owned read / sent elements, packed for
+        the peers."""
+        from .timeint import ab_coefficients
+        d, L = self.disc, self.L
+        lib, dm, st = nat.lib(), d.device_mesh, d.stream_ptr()
+        F = lambda s_: nat.fields(d.slots(s_))
+        for lev in range(1, L + 1):
+            sub = self.eff_sub[(tick, lev)]
+            if sub is None:
+                continue
+            period = 2 ** (L - lev)
+            frac = tick % period
+            nh = self.n_hist[lev]
+            if frac == 0 or nh == 0:
+                nat.check(lib.hw_axpy3(dm.struct, F(self.q), F(self.eff), F(self.ring[0]), None,
+                                       None, 1, 0.0, 0.0, 0.0, 0.0, sub, st))
+                continue
+            c = ab_coefficients(nh, frac / period) - ab_coefficients(nh, 1.0)
+            c = list(c) + [0.0] * (3 - nh)
+            s0 = self.steps[lev] % 3
+            h = [self.ring[s0], self.ring[(s0 - 1) % 3], self.ring[(s0 - 2) % 3]]
+            nat.check(lib.hw_axpy3(dm.struct, F(self.q), F(self.eff), F(h[0]), F(h[1]), F(h[2]),
+                                   nh, c[0], c[1], c[2], dt_min * period, sub, st))
+        self._pack()
+
+    def tick_exchange(self):
+        """Start the exchange of the packed boundary rows into the peers'
+        ghost rows (returns the transport handle)."""
+        return self.transport.start(self, self.eff)
+
+    def tick_step(self, tick, dt_min, handle):
+        """Wait for the ghosts' effective state, traces of the read set, and
+        the fused RHS + AB3 update of the owned stepping elements."""
+        from .timeint import ab_coefficients
+        d, L = self.disc, self.L
+        lib, dm, st = nat.lib(), d.device_mesh, d.stream_ptr()
+        F = lambda s_: nat.fields(d.slots(s_))
+        self.transport.wait(handle)
+        dm.compute_traces(F(self.eff), 0, st, subset=self.trace_sub[tick])
+        dm.set_traces(0, None)
+        for lev in [lev for lev in range(1, L + 1) if tick % (2 ** (L - lev)) == 0]:
+            self.n_hist[lev] = min(self.n_hist[lev] + 1, 3)
+            self.steps[lev] += 1
+            sub = self.step_sub[lev]
+            if sub is None:
+                continue
+            s0 = self.steps[lev] % 3
+            h0, h1, h2 = self.ring[s0], self.ring[(s0 - 1) % 3], self.ring[(s0 - 2) % 3]
+            nh = self.n_hist[lev]
+            c = list(ab_coefficients(nh)) + [0.0] * (3 - nh)
+            nat.check(lib.hw_ab_step(dm.struct, F(self.eff), F(self.q), F(h0), F(h1), F(h2), nh,
+                                     c[0], c[1], c[2], dt_min * 2 ** (L - lev), sub, st))
+
+    def macro_step(self, dt_min):
+        for tick in range(2 ** (self.L - 1)):
+            self.tick_effective(tick, dt_min)
+            self.tick_step(tick, dt_min, self.tick_exchange())
+
+    def owned_state(self):
+        return {t: self.q[t][:self.part.n_owned[t]] for t in self.disc.types}
