@@ -76,6 +76,57 @@ def _no_forcing(disc):
                                   "callback; use compute_rhs + ab3_step")
 
 
+def _forced_rhs(disc, q, time):
+    """Device RHS plus the forcing residual (host callback at the cubature
+    points, hybridwave/dg.py:497-515), device dict."""
+    out = disc.rhs_device(q)
+    disc._add_forcing(out, time)
+    return out
+
+
+def _single_rate_forced(disc, state, dt, T_final, callback, out):
+    """single_rate_run with a forcing callback: unfused RHS (hw_rhs) + host
+    forcing + the AB3 update, in the reference's operation order."""
+    host = _is_host(state)
+    q = disc.to_device(state)
+    hist = []
+    time = 0.0
+    while time < T_final - 1e-14:
+        h = min(dt, T_final - time)
+        hist.insert(0, _forced_rhs(disc, q, time))
+        del hist[3:]
+        c = ab_coefficients(len(hist), h / dt)
+        new = {}
+        for t in disc.types:
+            acc = q[t].clone()
+            for ci, f in zip(c, hist):
+                acc += dt * float(ci) * f[t]
+            new[t] = acc
+        q = new
+        time += h
+        if callback is not None:
+            callback(time, _export(disc, q, host))
+    return _export(disc, q, host, out)
+
+
+def _lsrk_forced(disc, state, dt, T_final, callback, out):
+    host = _is_host(state)
+    q = disc.to_device(state)
+    res = disc.zeros_state()
+    time = 0.0
+    while time < T_final - 1e-14:
+        h = min(dt, T_final - time)
+        for a, b, c in zip(LSRK_A, LSRK_B, LSRK_C):
+            k = _forced_rhs(disc, q, time + c * h)
+            for t in disc.types:
+                res[t] = a * res[t] + h * k[t]
+                q[t] = q[t] + b * res[t]
+        time += h
+        if callback is not None:
+            callback(time, _export(disc, q, host))
+    return _export(disc, q, host, out)
+
+
 class Stepper:
     """Device buffers and launch sequence for one integrator, reusable by
     the benchmark (and CUDA-graph capturable: no host syncs, fixed
@@ -131,8 +182,10 @@ class Stepper:
 def single_rate_run(disc, state, dt, T_final, callback=None, out=None):
     """AB3 to T_final; the last step lands through the fractional
     coefficients (hybridwave/timeint.py:57-72).  out: optional host arrays
-    the final state is written into."""
-    _no_forcing(disc)
+    the final state is written into.  With a forcing callback the step is
+    the unfused RHS + host forcing + update (slow path)."""
+    if disc.forcing is not None:
+        return _single_rate_forced(disc, state, dt, T_final, callback, out)
     host = _is_host(state)
     S = Stepper(disc, state, "ab")
     time = 0.0
@@ -166,8 +219,10 @@ def lsrk_step(disc, q, res, dt, q_tmp=None):
 
 def lsrk_run(disc, state, dt, T_final, callback=None, out=None):
     """Low-storage RK(4,5) to T_final with the single_rate_run signature;
-    the last step is shortened to land on T_final."""
-    _no_forcing(disc)
+    the last step is shortened to land on T_final (forcing: slow path as in
+    single_rate_run)."""
+    if disc.forcing is not None:
+        return _lsrk_forced(disc, state, dt, T_final, callback, out)
     host = _is_host(state)
     S = Stepper(disc, state, "lsrk")
     time = 0.0

@@ -4,7 +4,7 @@ Run in the build container (the reference is not on the GPU box):
     PYTHONPATH=/root/reference/pkg/src PYTHONDONTWRITEBYTECODE=1 \
         python tests/golden/make_golden.py
 
-Writes tests/golden/*.npz.  States are regenerated in the tests from the
+Writes tests/golden/*.npz (`make_golden.py forcing`: only forcing.npz).  States are regenerated in the tests from the
 recorded seeds (np.random.default_rng(seed).standard_normal(shape)), so
 only reference outputs are stored.
 """
@@ -181,5 +181,35 @@ def main():
     print("golden fixtures written to", HERE)
 
 
+def forcing_fn(x, time):
+    """Smooth volume source f(x, t) for the forcing fixtures (K, nq, 3) -> (K, nq)."""
+    return (np.sin(np.pi * x[..., 0]) * np.cos(np.pi * x[..., 1]) * (1.0 + x[..., 2])
+            * np.cos(3.0 * time))
+
+
+def forcing_fixtures():
+    """compute_rhs with a forcing callback, and 10 AB3 / LSRK steps with it."""
+    fd = {}
+    for tag, spec, N, form in [("hyb2_gl", "hybrid:2", 2, "GL"), ("hyb2_sem", "hybrid:2", 2, "SEM"),
+                               ("tet2_gl", "tet:2", 3, "GL")]:
+        mesh = build_mesh(spec)
+        set_random_materials(mesh, 5)
+        d = Discretization(mesh, N, form, forcing=forcing_fn)
+        st = d.project(cavity_fields, 0.0)
+        rhs = d.compute_rhs(st, 0.37)
+        dt = 0.5 * min(float(v.min()) for v in local_timesteps(d, 0.5).values())
+        ab = single_rate_run(d, st, dt, 10 * dt)
+        lk = lsrk_run_ref(d, st, dt, 10 * dt)
+        for t in d.types:
+            fd[f"{tag}/rhs/{t}"] = rhs[t]
+            fd[f"{tag}/ab3/{t}"] = ab[t]
+            fd[f"{tag}/lsrk/{t}"] = lk[t]
+        fd[f"{tag}/dt"] = np.array(dt)
+    np.savez_compressed(os.path.join(HERE, "forcing.npz"), **fd)
+    print("forcing fixtures written")
+
+
 if __name__ == "__main__":
+    if sys.argv[1:] == ["forcing"]:
+        sys.exit(forcing_fixtures())
     sys.exit(main())
