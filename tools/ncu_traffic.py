@@ -7,8 +7,8 @@ import os
 import subprocess
 import sys
 
-KINDS = [("hex_kernel", "hex"), ("dense_mma_kernel<3, 1>", "wedge"),
-         ("dense_mma_kernel<3, 2>", "pyramid"), ("tet_mma_kernel", "tet")]
+KINDS = [("hex_kernel", "hex"), ("dense_mma_kernel<3, 1", "wedge"),
+         ("dense_mma_kernel<3, 2", "pyramid"), ("tet_mma_kernel", "tet")]
 
 
 def main(rep, note, prefix="hybrid:38/N3/GL/f64"):
