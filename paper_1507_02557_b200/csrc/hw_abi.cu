@@ -339,21 +339,33 @@ static int run_rhs(const hw_mesh_t* M, const hw_fields_t* Q, const Epi& E,
 
 // ---------------------------------------------------------------- elementwise
 
+// out = q + dt (c0 h0 + c1 h1 + c2 h2) on the listed element rows (MRAB
+// dense output); dt == 0 is a plain row copy (no history reads).  Element
+// rows (4 Np scalars) are even-length: two scalars per thread.
 template <typename R>
 __global__ void axpy3_kernel(const R* __restrict__ q, R* __restrict__ out, const R* __restrict__ h0,
                              const R* __restrict__ h1, const R* __restrict__ h2, int nh, R c0,
                              R c1, R c2, R dt, const int32_t* __restrict__ list, int64_t n,
                              int chunk) {
-  const int64_t total = n * chunk;
+  const int half = chunk >> 1;
+  const int64_t total = n * half;
+  const bool copy = dt == R(0);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t w = i / chunk;
-    const int r = (int)(i - w * chunk);
-    const size_t idx = (size_t)(list ? list[w] : w) * chunk + r;
-    R acc = c0 * h0[idx];
-    if (nh > 1) acc += c1 * h1[idx];
-    if (nh > 2) acc += c2 * h2[idx];
-    out[idx] = q[idx] + dt * acc;
+    const int64_t w = i / half;
+    const int r = (int)(i - w * half);
+    const size_t idx = (size_t)(list ? list[w] : w) * chunk + 2 * r;
+    const R q0 = q[idx], q1 = q[idx + 1];
+    if (copy) {
+      out[idx] = q0;
+      out[idx + 1] = q1;
+      continue;
+    }
+    R a0 = c0 * h0[idx], a1 = c0 * h0[idx + 1];
+    if (nh > 1) { a0 += c1 * h1[idx]; a1 += c1 * h1[idx + 1]; }
+    if (nh > 2) { a0 += c2 * h2[idx]; a1 += c2 * h2[idx + 1]; }
+    out[idx] = q0 + dt * a0;
+    out[idx + 1] = q1 + dt * a1;
   }
 }
 
@@ -533,7 +545,7 @@ int hw_axpy3(const hw_mesh_t* mesh, const hw_fields_t* q, hw_fields_t* out,
     subset_of(subset, t, K, &list, &n);
     if (n <= 0) continue;
     const int chunk = 4 * np_of(t, mesh->N);
-    const unsigned g = grid_for(n * chunk);
+    const unsigned g = grid_for(n * chunk / 2);
     if (mesh->dtype == HW_F64)
       axpy3_kernel<double><<<g, 256, 0, st>>>(
           (const double*)q->p[t], (double*)out->p[t], (const double*)h0->p[t],
