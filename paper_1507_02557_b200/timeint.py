@@ -360,11 +360,81 @@ class MRABDriver:
             for lev in range(1, L + 1):
                 self.rhs_evals[t][self.levels[t] == lev] += n_macro * 2 ** (lev - 1)
 
+    def _run_forced(self, state, T_final, callback):
+        """With a forcing callback: per tick the full-mesh RHS of the
+        effective state plus the forcing at the tick time (unfused, host
+        forcing), then the history push and AB3 update of the stepping
+        levels, in the reference's order (hybridwave/timeint.py:111-142)."""
+        disc, L = self.disc, self.n_levels
+        host = _is_host(state)
+        macro = 2 ** (L - 1) * self.plan.dt_min
+        n_macro = max(1, math.ceil(T_final / macro - 1e-12))
+        dt_min = T_final / (n_macro * 2 ** (L - 1))
+        q = disc.to_device(state)
+        hist = {t: torch.zeros((3,) + tuple(q[t].shape), dtype=q[t].dtype, device=q[t].device)
+                for t in disc.types}
+        n_hist = np.zeros(L + 1, dtype=int)
+        masks = {t: [torch.as_tensor(self.levels[t] == lev, device=q[t].device)
+                     for lev in range(1, L + 1)] for t in disc.types}
+        for m in range(n_macro):
+            t0 = m * dt_min * 2 ** (L - 1)
+            for tick in range(2 ** (L - 1)):
+                stepping = [lev for lev in range(1, L + 1) if tick % (2 ** (L - lev)) == 0]
+                eff = {}
+                for t in disc.types:
+                    e = q[t].clone()
+                    for lev in range(1, L + 1):
+                        period = 2 ** (L - lev)
+                        frac = tick % period
+                        nh = n_hist[lev]
+                        if frac == 0 or nh == 0:
+                            continue
+                        c = ab_coefficients(nh, frac / period) - ab_coefficients(nh, 1.0)
+                        sel = masks[t][lev - 1]
+                        upd = float(c[0]) * hist[t][0][sel]
+                        for i in range(1, nh):
+                            upd = upd + float(c[i]) * hist[t][i][sel]
+                        e[sel] += dt_min * period * upd
+                    eff[t] = e
+                rhs = disc.rhs_device(eff)
+                disc._add_forcing(rhs, t0 + tick * dt_min)
+                for t in disc.types:
+                    sel = torch.zeros_like(masks[t][0])
+                    for lev in stepping:
+                        sel |= masks[t][lev - 1]
+                    if not bool(sel.any()):
+                        continue
+                    self.rhs_evals[t][sel.cpu().numpy()] += 1
+                    hist[t][2][sel] = hist[t][1][sel]
+                    hist[t][1][sel] = hist[t][0][sel]
+                    hist[t][0][sel] = rhs[t][sel]
+                for lev in stepping:
+                    n_hist[lev] = min(n_hist[lev] + 1, 3)
+                    c = ab_coefficients(n_hist[lev])
+                    for t in disc.types:
+                        sel = masks[t][lev - 1]
+                        upd = float(c[0]) * hist[t][0][sel]
+                        for i in range(1, n_hist[lev]):
+                            upd = upd + float(c[i]) * hist[t][i][sel]
+                        q[t][sel] += dt_min * 2 ** (L - lev) * upd
+            self.macro_steps += 1
+            if callback is not None:
+                callback(t0 + dt_min * 2 ** (L - 1), _export(disc, q, host))
+        out = _export(disc, q, host)
+        for t in disc.types:
+            if host:
+                state[t][...] = out[t]
+            else:
+                state[t].copy_(out[t])
+        return state
+
     def run(self, state, T_final, callback=None, graph=True):
         """graph: once every level holds 3 history entries the launch
         pattern repeats every 3 macro steps (ring slots cycle mod 3); that
-        period is captured once as a CUDA graph and replayed (no callback)."""
-        _no_forcing(self.disc)
+        period is captured once as a CUDA graph and replayed (no callback).
+        A forcing callback takes the unfused path (_run_forced)."""
+        if self.disc.forcing is not None:
+            return self._run_forced(state, T_final, callback)
         disc = self.disc
         L = self.n_levels
         host = _is_host(state)

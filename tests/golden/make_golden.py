@@ -205,6 +205,18 @@ def forcing_fixtures():
             fd[f"{tag}/ab3/{t}"] = ab[t]
             fd[f"{tag}/lsrk/{t}"] = lk[t]
         fd[f"{tag}/dt"] = np.array(dt)
+    # multi-rate AB3 with forcing (hybrid:2, the trajectories.npz MRAB setup)
+    m = build_mesh("hybrid:2")
+    d = Discretization(m, 2, "GL", forcing=forcing_fn)
+    st0 = d.project(cavity_fields, 0.0)
+    plan = assign_mrab_levels(local_timesteps(d, 0.5), 3, m, cfl=0.5)
+    T = 6 * 4 * plan.dt_min
+    s, drv = mrab_run(d, plan, {t: v.copy() for t, v in st0.items()}, T)
+    for t in d.types:
+        fd[f"mrab/{t}"] = s[t]
+        fd[f"mrab/levels/{t}"] = plan.levels[t]
+    fd["mrab/dt_min"] = np.array(plan.dt_min)
+    fd["mrab/T"] = np.array(T)
     np.savez_compressed(os.path.join(HERE, "forcing.npz"), **fd)
     print("forcing fixtures written")
 
