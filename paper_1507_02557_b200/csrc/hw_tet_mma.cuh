@@ -80,8 +80,11 @@ struct TetMma {
                        SRES = SV + E * RA, SG = SRES + E * EQ,
                        SMAT = SG + E * GEO_TET, TOTAL = SMAT + E * 4;
   static constexpr size_t BYTES = sizeof(S) * TOTAL + sizeof(int) * (E + NFP);
+#ifndef HW_TET_MINB_MID
+#define HW_TET_MINB_MID 4
+#endif
   static constexpr int MINB = (W <= 4) ? (sizeof(S) == 8 ? HW_TET_MINB : HW_TET_MINB32)
-                                       : ((W <= 8) ? 3 : 1);
+                                       : ((W <= 8) ? HW_TET_MINB_MID : 1);
   // flux items (element, face point) per thread
   static constexpr int IT = (E * NFP + NTH - 1) / NTH;
 };
