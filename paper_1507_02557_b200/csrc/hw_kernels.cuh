@@ -578,8 +578,16 @@ __device__ __forceinline__ R hex_metric(const R* X, R r, R s, R t, R G[9]) {
 #ifndef HW_HEX_NT
 #define HW_HEX_NT 128
 #endif
+#ifndef HW_HEX_MINB
+#define HW_HEX_MINB 0
+#endif
+#if HW_HEX_MINB > 0
+#define HW_HEX_BOUNDS __launch_bounds__(HW_HEX_NT, HW_HEX_MINB)
+#else
+#define HW_HEX_BOUNDS __launch_bounds__(HW_HEX_NT)
+#endif
 template <int N, typename R>
-__global__ void __launch_bounds__(HW_HEX_NT) hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi E,
+__global__ void HW_HEX_BOUNDS hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi E,
                                                  const int32_t* __restrict__ list,
                                                  int64_t nwork) {
   using L = Smem<N, HW_HEX, R, HW_HEX_NT>;
