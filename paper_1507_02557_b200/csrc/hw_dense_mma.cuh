@@ -91,6 +91,7 @@ struct DMma {
 #define HW_DENSE_MINB32 4
 #endif
   static constexpr int MINB = sizeof(S) == 8 ? HW_DENSE_MINB : HW_DENSE_MINB32;
+  static constexpr int BIG_MINB = (65536 / (NTH * 64)) > 1 ? 65536 / (NTH * 64) : 1;
 };
 
 // element rows (K, 4, NP) -> smem [e][field (stride QF)][node]
@@ -456,9 +457,10 @@ __global__ void __launch_bounds__(DMma<N, T, S>::NTH, DMma<N, T, S>::MINB)
   dense_mma_body<N, T, S>(M, Q, E, list, nwork);
 }
 
-// large-RT layouts: compiler's default register heuristic
+// large-RT layouts: register target of <= 64 per thread (N=5 wedge 560 ->
+// 494 us, pyramid 113 -> 103 us; no change at N=4)
 template <int N, int T, typename S>
-__global__ void __launch_bounds__(DMma<N, T, S>::NTH)
+__global__ void __launch_bounds__(DMma<N, T, S>::NTH, DMma<N, T, S>::BIG_MINB)
     dense_mma_kernel_big(hw_mesh_t M, hw_fields_t Q, Epi E, const int32_t* __restrict__ list,
                          int64_t nwork) {
   dense_mma_body<N, T, S>(M, Q, E, list, nwork);
