@@ -10,5 +10,5 @@ run --mesh hybrid:38 --order 3 --form GL --dtype f32 --steps 20
 run --mesh tet:20 --order 3 --form GL --steps 20
 run --mesh tet:20 --order 3 --form GL --dtype f32 --steps 20
 run --mesh hex:4 --order 2 --form SEM --steps 100
-run --mesh graded:24 --order 3 --form GL --scheme mrab --levels 3 --steps 10 --warmup 3
+run --mesh graded:24 --order 3 --form GL --scheme mrab --levels 3 --steps 30 --warmup 5
 run --mesh hexdom:120 --order 4 --form GL --steps 5 --warmup 3
