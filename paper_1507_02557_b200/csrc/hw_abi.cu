@@ -245,9 +245,14 @@ static int launch_rhs_all(const hw_mesh_t& M, const hw_fields_t& Q, const Epi& E
     switch (t) {
       case HW_HEX: {
         using L = Smem<N, HW_HEX, R, HW_HEX_NT>;
-        if ((rc = set_smem(hex_kernel<N, R>, L::BYTES))) return rc;
-        hex_kernel<N, R><<<(unsigned)((n + L::EPB - 1) / L::EPB), HW_HEX_NT, L::BYTES, st>>>(
-            M, Q, E, list, n);
+        const unsigned grid = (unsigned)((n + L::EPB - 1) / L::EPB);
+        if (M.t[HW_HEX].form == HW_FORM_SKEW) {
+          if ((rc = set_smem(hex_kernel<N, R, true>, L::BYTES))) return rc;
+          hex_kernel<N, R, true><<<grid, HW_HEX_NT, L::BYTES, st>>>(M, Q, E, list, n);
+        } else {
+          if ((rc = set_smem(hex_kernel<N, R, false>, L::BYTES))) return rc;
+          hex_kernel<N, R, false><<<grid, HW_HEX_NT, L::BYTES, st>>>(M, Q, E, list, n);
+        }
         rc = check_launch("hex_kernel");
         break;
       }
@@ -260,11 +265,18 @@ static int launch_rhs_all(const hw_mesh_t& M, const hw_fields_t& Q, const Epi& E
                            : launch_dense<N, HW_PYRAMID, R>(M, Q, E, list, n, st);
         break;
       case HW_TET:
+        if (tet_scalar() && M.t[HW_TET].form == HW_FORM_SKEW)
+          return fail("the scalar tet kernel implements the strong form only");
         if (!tet_scalar()) {   // fp64 DMMA for both storage precisions
           using L = TetMma<N, R>;
-          if ((rc = set_smem(tet_mma_kernel<N, R>, L::BYTES))) return rc;
-          tet_mma_kernel<N, R><<<(unsigned)((n + L::E - 1) / L::E), L::NTH, L::BYTES, st>>>(
-              M, Q, E, list, n);
+          const unsigned grid = (unsigned)((n + L::E - 1) / L::E);
+          if (M.t[HW_TET].form == HW_FORM_SKEW) {
+            if ((rc = set_smem(tet_mma_kernel<N, R, true>, L::BYTES))) return rc;
+            tet_mma_kernel<N, R, true><<<grid, L::NTH, L::BYTES, st>>>(M, Q, E, list, n);
+          } else {
+            if ((rc = set_smem(tet_mma_kernel<N, R, false>, L::BYTES))) return rc;
+            tet_mma_kernel<N, R, false><<<grid, L::NTH, L::BYTES, st>>>(M, Q, E, list, n);
+          }
           rc = check_launch("tet_mma_kernel");
         } else {
           rc = launch_dense<N, HW_TET, R>(M, Q, E, list, n, st);

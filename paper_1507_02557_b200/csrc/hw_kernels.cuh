@@ -586,7 +586,7 @@ __device__ __forceinline__ R hex_metric(const R* X, R r, R s, R t, R G[9]) {
 #else
 #define HW_HEX_BOUNDS __launch_bounds__(HW_HEX_NT)
 #endif
-template <int N, typename R>
+template <int N, typename R, bool SK = false>   // SK: skew form (testing hook)
 __global__ void HW_HEX_BOUNDS hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi E,
                                                  const int32_t* __restrict__ list,
                                                  int64_t nwork) {
@@ -670,6 +670,34 @@ __global__ void HW_HEX_BOUNDS hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi E,
   asm volatile("cp.async.wait_group 1;\n" ::: "memory");
   __syncthreads();
 
+  // skew form (forms_override testing hook, hybridwave/dg.py:392-398): the
+  // pressure term is sum_c D^T (w3 J v_c), v_c = sum_x G[c][x] u_x, formed
+  // here in the flux storage (written only after the volume pass)
+  constexpr bool skew = SK;
+  R* spre = sf;   // [e][c][node]
+  if (skew) {
+    for (int i = tid; i < ne * NP; i += NT) {
+      const int e = i / NP, n = i - e * NP;
+      const int ii = n / (N1 * N1), jj = (n / N1) % N1, kk = n % N1;
+      const R* Xe = sg + e * GEO_HEX;
+      R G[9], J;
+      if (Xe[HX_AFF] != R(0)) {
+#pragma unroll
+        for (int a = 0; a < 9; ++a) G[a] = Xe[HX_G + a];
+        J = Xe[HX_J];
+      } else {
+        J = hex_metric<R>(Xe, sx[ii], sx[jj], sx[kk], G);
+      }
+      const R wJ = sw1[ii] * sw1[jj] * sw1[kk] * J;
+      const R* u = sq + e * 4 * NP + n;
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+        spre[(e * 3 + c) * NP + n] =
+            wJ * (G[3 * c] * u[NP] + G[3 * c + 1] * u[2 * NP] + G[3 * c + 2] * u[3 * NP]);
+    }
+    __syncthreads();
+  }
+
   R acc[S][4], minv[S];
 #pragma unroll
   for (int s = 0; s < S; ++s) {
@@ -711,6 +739,16 @@ __global__ void HW_HEX_BOUNDS hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi E,
       }
       acc[s][0] = -div;
       minv[s] = siw1[ii] * siw1[jj] * siw1[kk] * iJ;
+      if (skew) {
+        const R* pr = spre + e * 3 * NP;
+        R a = R(0);
+#pragma unroll
+        for (int l = 0; l < N1; ++l)
+          a += sD[l * N1 + ii] * pr[(l * N1 + jj) * N1 + kk] +
+               sD[l * N1 + jj] * pr[NP + (ii * N1 + l) * N1 + kk] +
+               sD[l * N1 + kk] * pr[2 * NP + (ii * N1 + jj) * N1 + l];
+        acc[s][0] = a * minv[s];
+      }
     }
   }
 
@@ -778,7 +816,7 @@ __global__ void HW_HEX_BOUNDS hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi E,
     }
     R tp, tu, fp, fu;
     penalties(Xv[HX_Z + 2 * f], Xv[HX_Z + 2 * f + 1], pen, tp, tu);
-    upwind_flux(own[0], um, pp, up, nrm, tp, tu, TY.form == HW_FORM_SKEW, fp, fu);
+    upwind_flux(own[0], um, pp, up, nrm, tp, tu, SK, fp, fu);
     R* o = sf + e * 4 * NFP + j;        // [field][face point]: conflict-free
     o[0] = fp * wJs;
     o[NFP] = nrm[0] * fu * wJs;

@@ -104,7 +104,9 @@ __device__ __forceinline__ void tet_rows(S* dst, const S* src, const int* sk, in
   }
 }
 
-template <int N, typename S>
+// SK: skew form (forms_override testing hook) as a compile-time variant so
+// the production strong-form kernel carries none of its code
+template <int N, typename S, bool SK = false>
 __global__ void __launch_bounds__(TetMma<N, S>::NTH, TetMma<N, S>::MINB)
     tet_mma_kernel(hw_mesh_t M, hw_fields_t Q, Epi E, const int32_t* __restrict__ list,
                    int64_t nwork) {
@@ -194,18 +196,21 @@ __global__ void __launch_bounds__(TetMma<N, S>::NTH, TetMma<N, S>::MINB)
   // ---- P2: volume GEMMs on DMMA
   const int rt = warp / L::CT, ct = warp - rt * L::CT;
   const int bk = lane & 3, bcol = ct * 8 + (lane >> 2);
+  constexpr bool skew = SK;
   R dp[3][2] = {{0, 0}, {0, 0}, {0, 0}}, dv[2] = {0, 0};
   {
     const R* Dg = (const R*)TY.op[2];   // [3][RT][NPK/4][32] A fragments, zero padded
+    const R* Bg = (const R*)TY.op[5];   // skew: invM D_c^T M fragments
     const S* bq = sq + bcol * EQ + bk;
     const S* bv = sv + bcol * EV + bk;
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
 #pragma unroll
       for (int ks = 0; ks < NPK / 4; ++ks) {
-        const R a = ldg(Dg + (((c * L::RT + rt) * (NPK / 4) + ks) << 5) + lane);
+        const int fi = (((c * L::RT + rt) * (NPK / 4) + ks) << 5) + lane;
+        const R a = ldg(Dg + fi);
         dmma884(dp[c][0], dp[c][1], a, bq[ks * 4]);
-        dmma884(dv[0], dv[1], a, bv[c * NPK + ks * 4]);
+        dmma884(dv[0], dv[1], skew ? ldg(Bg + fi) : a, bv[c * NPK + ks * 4]);
       }
     }
   }
@@ -239,7 +244,7 @@ __global__ void __launch_bounds__(TetMma<N, S>::NTH, TetMma<N, S>::MINB)
     }
     R tp, tu, fp, fu;
     penalties(R(g[4]), R(g[5]), pen, tp, tu);
-    upwind_flux(pm, um, pp, up, nrm, tp, tu, false, fp, fu);
+    upwind_flux(pm, um, pp, up, nrm, tp, tu, skew, fp, fu);
     sfp[e * EF + f * NFK + jj] = S(fp * R(g[3]));
     sfu[e * EF + f * NFK + jj] = S(fu * R(g[3]));
   }
@@ -252,7 +257,7 @@ __global__ void __launch_bounds__(TetMma<N, S>::NTH, TetMma<N, S>::MINB)
 
   // ---- P4: lift on DMMA, combine, epilogue
   const int col0 = ct * 8 + (lane & 3) * 2;
-  R accp[2] = {-dv[0], -dv[1]};
+  R accp[2] = {skew ? dv[0] : -dv[0], skew ? dv[1] : -dv[1]};
   R accu[3][2];
 #pragma unroll
   for (int i = 0; i < 2; ++i) {

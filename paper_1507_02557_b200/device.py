@@ -163,8 +163,6 @@ def pack_mesh(disc):
     face_offsets = {t: (d["face_offsets"], int(d["face_offsets"][-1])) for t, d in dops_all.items()}
     for t in disc.types:
         form = disc.forms[t]
-        if t in ("hex", "tet") and form != "strong":
-            raise NotImplementedError(f"device {t} kernel implements the strong form only")
         if t == "wedge" and form != "skew":
             raise NotImplementedError("device wedge kernel implements the skew form only")
         verts = mesh.element_vertices(t)
@@ -179,8 +177,7 @@ def pack_mesh(disc):
             "geo": geometry_records(t, verts, face_impedance_avg(mesh, t)),
             "mat": material_records(np.asarray(mesh.materials[t], dtype=float)),
             "nbr_elem": elem, "nbr_code": code,
-            "op": {**_pack_ops(t, dops),
-                   **({4: disc.ops[t].M_ref} if t == "tet" else {})},   # tet: energy mass
+            "op": {**_pack_ops(t, dops), **(_tet_extra_ops(disc.ops[t], dops) if t == "tet" else {})},
             "iop": _pack_iops(t, dops, disc.N, mesh, perm_tri, face_offsets, dops_all,
                               perm_quad, disc.formulation.kind == "SEM"),
             "nfp": int(dops["face_offsets"][-1]),
@@ -192,7 +189,19 @@ def pack_mesh(disc):
 
 
 # operator slots read as fp64 DMMA fragments by the tensor-core kernels
-MMA_SLOTS = {"hex": (), "tet": (2, 3), "wedge": (2, 3, 4, 7), "pyramid": (2, 3, 4, 7)}
+MMA_SLOTS = {"hex": (), "tet": (2, 3, 5), "wedge": (2, 3, 4, 7), "pyramid": (2, 3, 4, 7)}
+
+
+def _tet_extra_ops(ops, d):
+    """tet op[4] = M_ref (hw_energy); op[5] = the skew-form volume operators
+    B_c = invM_ref D_c^T M_ref (rhs_p = sum_c B_c v_c after the mass inverse,
+    hybridwave/dg.py:413-416) as padded DMMA fragments."""
+    Np = d["Np"]
+    rt8, npk = -(-Np // 8) * 8, -(-Np // 4) * 4
+    B = np.zeros((3, rt8, npk))
+    for c, Dc in enumerate((d["Dr"], d["Ds"], d["Dt"])):
+        B[c, :Np, :Np] = ops.invM_ref @ Dc.T @ ops.M_ref
+    return {4: ops.M_ref, 5: mma_fragments(B)}
 
 
 def mma_fragments(A):

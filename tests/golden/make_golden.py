@@ -221,7 +221,30 @@ def forcing_fixtures():
     print("forcing fixtures written")
 
 
+def forms_fixtures():
+    """compute_rhs with the forms_override testing hook (skew hex / tet,
+    strong pyramid SEM) on random states."""
+    fd = {}
+    cases = [("hyb2_skew", "hybrid:2", 2, "GL", {"hex": "skew", "tet": "skew"}),
+             ("hyb3_skew", "hybrid:2", 3, "SEM", {"hex": "skew", "tet": "skew"}),
+             ("hex2_skew", "hex:2", 3, "GL", {"hex": "skew"}),
+             ("tet2_skew", "tet:2", 3, "GL", {"tet": "skew"})]
+    for tag, spec, N, form, over in cases:
+        mesh = build_mesh(spec)
+        set_random_materials(mesh, 9)
+        d = Discretization(mesh, N, form, forms_override=over)
+        rng = np.random.default_rng(11)
+        st = {t: rng.standard_normal((d.n_elems[t], 4, d.ops[t].Np)) for t in d.types}
+        rhs = d.compute_rhs(st, 0.0)
+        for t in d.types:
+            fd[f"{tag}/rhs/{t}"] = rhs[t]
+    np.savez_compressed(os.path.join(HERE, "forms.npz"), **fd)
+    print("forms fixtures written")
+
+
 if __name__ == "__main__":
     if sys.argv[1:] == ["forcing"]:
         sys.exit(forcing_fixtures())
+    if sys.argv[1:] == ["forms"]:
+        sys.exit(forms_fixtures())
     sys.exit(main())

@@ -143,6 +143,14 @@ def test_energy_matches_host(native_lib, spec, N, form):
     assert abs(got - ref) <= 1e-12 * abs(ref)
 
 
+def test_skew_nonaffine_hex(native_lib):
+    from paper_1507_02557_b200.dg import Discretization
+    d = Discretization(_perturbed("hex:3", 0.04, 5), 3, "GL", forms_override={"hex": "skew"})
+    rng = np.random.default_rng(6)
+    st = {t: rng.standard_normal((d.n_elems[t], 4, d.ops[t].Np)) for t in d.types}
+    assert rel_err(d.compute_rhs(st), oracle.compute_rhs(d, st)) < 1e-11
+
+
 def test_energy_nonaffine_hex(native_lib):
     from paper_1507_02557_b200.dg import Discretization, discrete_energy
     d = Discretization(_perturbed("hex:3", 0.04, 7), 3, "GL")
@@ -261,6 +269,26 @@ def test_mrab_forcing_matches_reference(native_lib):
     plan.dt_min = float(G["mrab/dt_min"])
     s, _ = mrab_run(d, plan, st0, float(G["mrab/T"]))
     assert _l2rel(s, {t: G[f"mrab/{t}"] for t in d.types}) < 1e-10
+
+
+@pytest.mark.parametrize("tag,spec,N,form,over", [
+    ("hyb2_skew", "hybrid:2", 2, "GL", {"hex": "skew", "tet": "skew"}),
+    ("hyb3_skew", "hybrid:2", 3, "SEM", {"hex": "skew", "tet": "skew"}),
+    ("hex2_skew", "hex:2", 3, "GL", {"hex": "skew"}),
+    ("tet2_skew", "tet:2", 3, "GL", {"tet": "skew"})])
+def test_skew_forms_match_reference(tag, spec, N, form, over, native_lib):
+    """forms_override (the reference's testing hook): skew hex and tet
+    volume + flux on the device against the reference's own RHS."""
+    from paper_1507_02557_b200.dg import Discretization
+    from conftest import set_random_materials
+    G = load_golden("forms")
+    m = build_mesh(spec)
+    set_random_materials(m, 9)
+    d = Discretization(m, N, form, forms_override=over)
+    rng = np.random.default_rng(11)
+    st = {t: rng.standard_normal((d.n_elems[t], 4, d.ops[t].Np)) for t in d.types}
+    assert rel_err(d.compute_rhs(st), {t: G[f"{tag}/rhs/{t}"] for t in d.types}) < 1e-12
+    assert rel_err(d.compute_rhs(st), oracle.compute_rhs(d, st)) < 1e-12
 
 
 def _perturbed(spec, amp, seed):
