@@ -187,7 +187,10 @@ __device__ __forceinline__ void dense_mma_body(const hw_mesh_t& M, const hw_fiel
   const int64_t w0 = (int64_t)blockIdx.x * EB;
   const int ne = (int)((nwork - w0) < EB ? (nwork - w0) : EB);
   const bool lsrk = E.mode == MODE_LSRK;
+  // flux form from the type's form; the wedge volume is always the LSC-DG
+  // skew two-pass (hybridwave/dg.py:423-444 has no strong branch)
   const bool skew = TY.form == HW_FORM_SKEW;
+  const bool vskew = skew || T == HW_WEDGE;
 
   if (tid < EB) sk[tid] = tid < ne ? (list ? list[w0 + tid] : (int)(w0 + tid)) : 0;
   // zero K paddings (node rows NP..NPK and the per-face lift padding)
@@ -293,7 +296,7 @@ __device__ __forceinline__ void dense_mma_body(const hw_mesh_t& M, const hw_fiel
     };
     auto vol_p = [&]() {
       const S* bv = sv + bcol * EV + bk;
-      const R* AV = skew ? AT : A;
+      const R* AV = vskew ? AT : A;
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
         const R* ac = AV + (((c * L::RT + rt) * L::KPP) << 6) + 2 * lane;
@@ -364,8 +367,8 @@ __device__ __forceinline__ void dense_mma_body(const hw_mesh_t& M, const hw_fiel
   const R* LF = (const R*)TY.op[4];     // [RT][NFKT/4][32] lift fragments
   R acc[3][2], accp[2];
   auto lift_p = [&]() {
-    accp[0] = skew ? dv[0] : -dv[0];
-    accp[1] = skew ? dv[1] : -dv[1];
+    accp[0] = vskew ? dv[0] : -dv[0];
+    accp[1] = vskew ? dv[1] : -dv[1];
     const S* bp = sfp + bcol * EF + bk;
     const R* lf = LF + ((rt * L::KPL) << 6) + 2 * lane;
     double2 pr;

@@ -406,7 +406,8 @@ __global__ void __launch_bounds__(NT) dense_kernel(hw_mesh_t M, hw_fields_t Q, E
   }
   __syncthreads();
 
-  const bool skew = TY.form == HW_FORM_SKEW;
+  const bool skew = TY.form == HW_FORM_SKEW;             // flux form
+  const bool vskew = skew || T == HW_WEDGE;              // volume (wedge: always skew)
   const R* AT = (const R*)TY.op[0];
   const R* AR = (const R*)TY.op[1];
   R acc[S][4];
@@ -420,7 +421,7 @@ __global__ void __launch_bounds__(NT) dense_kernel(hw_mesh_t M, hw_fields_t Q, E
       R div = R(0), dp0 = R(0), dp1 = R(0), dp2 = R(0);
       const R* p = sq + e * 4 * NP;
       const R* v = sv + e * 3 * NP;
-      if (skew) {
+      if (vskew) {
 #pragma unroll 4
         for (int m = 0; m < NP; ++m) {
           const R pm = p[m];
@@ -444,7 +445,7 @@ __global__ void __launch_bounds__(NT) dense_kernel(hw_mesh_t M, hw_fields_t Q, E
         }
       }
       const R* G = sg + e * X::GEO;
-      acc[s][0] = skew ? div : -div;
+      acc[s][0] = vskew ? div : -div;
 #pragma unroll
       for (int x = 0; x < 3; ++x) acc[s][1 + x] = -(G[x] * dp0 + G[3 + x] * dp1 + G[6 + x] * dp2);
     }

@@ -163,8 +163,6 @@ def pack_mesh(disc):
     face_offsets = {t: (d["face_offsets"], int(d["face_offsets"][-1])) for t, d in dops_all.items()}
     for t in disc.types:
         form = disc.forms[t]
-        if t == "wedge" and form != "skew":
-            raise NotImplementedError("device wedge kernel implements the skew form only")
         verts = mesh.element_vertices(t)
         _affine_check(t, verts, disc.N)
         dops = dops_all[t]

@@ -228,7 +228,9 @@ def forms_fixtures():
     cases = [("hyb2_skew", "hybrid:2", 2, "GL", {"hex": "skew", "tet": "skew"}),
              ("hyb3_skew", "hybrid:2", 3, "SEM", {"hex": "skew", "tet": "skew"}),
              ("hex2_skew", "hex:2", 3, "GL", {"hex": "skew"}),
-             ("tet2_skew", "tet:2", 3, "GL", {"tet": "skew"})]
+             ("tet2_skew", "tet:2", 3, "GL", {"tet": "skew"}),
+             ("hyb2_wstrong", "hybrid:2", 2, "GL", {"wedge": "strong", "pyramid": "skew"}),
+             ("hyb2_pstrong", "hybrid:2", 2, "SEM", {"pyramid": "strong"})]
     for tag, spec, N, form, over in cases:
         mesh = build_mesh(spec)
         set_random_materials(mesh, 9)

@@ -275,7 +275,9 @@ def test_mrab_forcing_matches_reference(native_lib):
     ("hyb2_skew", "hybrid:2", 2, "GL", {"hex": "skew", "tet": "skew"}),
     ("hyb3_skew", "hybrid:2", 3, "SEM", {"hex": "skew", "tet": "skew"}),
     ("hex2_skew", "hex:2", 3, "GL", {"hex": "skew"}),
-    ("tet2_skew", "tet:2", 3, "GL", {"tet": "skew"})])
+    ("tet2_skew", "tet:2", 3, "GL", {"tet": "skew"}),
+    ("hyb2_wstrong", "hybrid:2", 2, "GL", {"wedge": "strong", "pyramid": "skew"}),
+    ("hyb2_pstrong", "hybrid:2", 2, "SEM", {"pyramid": "strong"})])
 def test_skew_forms_match_reference(tag, spec, N, form, over, native_lib):
     """forms_override (the reference's testing hook): skew hex and tet
     volume + flux on the device against the reference's own RHS."""
