@@ -868,7 +868,38 @@ __global__ void HW_HEX_BOUNDS hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi E,
   }
   if (!sem && E.mode != MODE_RHS && M.tr_out[HW_HEX] != nullptr) {
     __syncthreads();
-    publish_traces<N, HW_HEX, R>(M, sq, sg, sk, ne, (R*)M.tr_out[HW_HEX]);
+    // GL hex traces of the new state: one thread per (element, axis, line)
+    // reads the line once and interpolates to both end faces of the axis
+    R* tro = (R*)M.tr_out[HW_HEX];
+    for (int it = tid; it < ne * 3 * NFQ; it += NT) {
+      const int e = it / (3 * NFQ), r = it - e * 3 * NFQ;
+      const int a = r / NFQ, uv = r - a * NFQ, u = uv / N1, v = uv - u * N1;
+      // base node (axis index 0) and stride along the axis
+      const int ii = a == 0 ? 0 : u, jj = a == 0 ? u : (a == 1 ? 0 : v), kk = a == 2 ? 0 : v;
+      const int base = (ii * N1 + jj) * N1 + kk;
+      const int stride = a == 0 ? N1 * N1 : (a == 1 ? N1 : 1);
+      const R* qe = sq + e * 4 * NP + base;
+      R t0[4] = {R(0), R(0), R(0), R(0)}, t1[4] = {R(0), R(0), R(0), R(0)};
+#pragma unroll
+      for (int l = 0; l < N1; ++l) {
+        const R w0 = sve[l], w1 = sve[N1 + l];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const R x = qe[c * NP + l * stride];
+          t0[c] += w0 * x;
+          t1[c] += w1 * x;
+        }
+      }
+      R* o = tro + (size_t)sk[e] * 4 * NFP;
+#pragma unroll
+      for (int end = 0; end < 2; ++end) {
+        const int f = 2 * a + end;
+        const int* cf = spc + 4 * f;
+        const int pt = cf[0] * ii + cf[1] * jj + cf[2] * kk + cf[3];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) o[c * NFP + f * NFQ + pt] = end ? t1[c] : t0[c];
+      }
+    }
   }
 }
 
