@@ -760,11 +760,11 @@ __global__ void HW_HEX_BOUNDS hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi E,
   for (int i = tid; i < ne * NFP; i += NT) {
     const int e = i / NFP, j = i - e * NFP;
     const int f = j / NFQ, jj = j - f * NFQ;
-    const int* tab = TY.iop[0] + 3 * j;
-    const int base = __ldg(tab), stride = __ldg(tab + 1), end = __ldg(tab + 2);
     const R* qe = sq + e * 4 * NP;
     R own[4];
     if (sem) {
+      const int* tab = TY.iop[0] + 3 * j;
+      const int base = __ldg(tab), stride = __ldg(tab + 1), end = __ldg(tab + 2);
       const int node = base + (end ? N : 0) * stride;
 #pragma unroll
       for (int c = 0; c < 4; ++c) own[c] = qe[c * NP + node];
