@@ -627,7 +627,7 @@ __global__ void HW_HEX_BOUNDS hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi E,
   __syncthreads();
   // group 1 (volume inputs): state rows, records, links
   copy_rows16<4 * NP, 4 * NP, NT, EPB>(sq, (const R*)Q.p[HW_HEX], sk, ne);
-  copy_rows<GEO_HEX, GEO_HEX, NT, EPB>(sg, (const R*)TY.geo, sk, ne);
+  copy_rows16<GEO_HEX, GEO_HEX, NT, EPB>(sg, (const R*)TY.geo, sk, ne);   // 72 words
   copy_rows<4, 4, NT, EPB>(smat, (const R*)TY.mat, sk, ne);
   for (int i = tid; i < ne * 6; i += NT)
     snc[i] = __ldg(TY.nbr_code + (size_t)sk[i / 6] * 6 + i % 6);
