@@ -6,7 +6,7 @@
 
 namespace hw {
 
-constexpr int NT = 256;  // threads per block for every RHS kernel
+constexpr int NT = 256;  // threads per block of the scalar dense and trace kernels
 
 template <int N>
 struct Dims {

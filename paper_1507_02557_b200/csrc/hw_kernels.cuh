@@ -1,14 +1,18 @@
-// Fused per-element-type RHS + time-update kernels (sm_100a), v2.
+// Fused per-element-type RHS + time-update kernels (sm_100a): the hex
+// kernel, the scalar dense kernel (high-N / debug fallback for wedge,
+// pyramid, tet), the hw_traces and hw_energy kernels, and the shared
+// traits, copy helpers and epilogues (the DMMA tet / wedge / pyramid
+// kernels are in hw_tet_mma.cuh / hw_dense_mma.cuh).
 //
 // One launch per element type per stage.  A block owns EPB elements:
-//   P0 load       q, geometry record, material, neighbour links -> smem
-//   P1 stage      cp.async (LDGSTS) of every neighbour's face data and of
-//                 the LSRK residual -> smem; fire-and-forget, so the L2
-//                 round trips overlap the volume work below
-//   P2 volume     strong/skew volume term, mass inverse folded out
-//   P3 flux       own + neighbour traces from smem, upwind flux x face Jacobian
-//   P4 lift       face-to-volume lift, mass inverse, materials, epilogue
-//                 (RHS / LSRK stage / AB step)
+//   P0 load       q rows, geometry records, materials, links (cp.async) and
+//                 every face point's neighbour value through the host gather
+//                 index (cp.async for hex, registers for the DMMA kernels),
+//                 the LSRK residual behind the volume / lift work
+//   P1 volume     strong/skew volume term, mass inverse folded out
+//   P2 flux       own + neighbour traces, upwind flux x face Jacobian
+//   P3 lift       face-to-volume lift, mass inverse, materials, epilogue
+//                 (RHS / LSRK stage / AB step), publish the new traces
 // Reference data flow: hybridwave/dg.py:299-506.
 #pragma once
 #include "hw_common.cuh"
