@@ -3,8 +3,9 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <set>
+#include <utility>
 #include <string>
-#include <unordered_set>
 
 #include "hw_kernels.cuh"
 #include "hw_tet_mma.cuh"
@@ -32,9 +33,11 @@ static int check_launch(const char* what) {
 template <typename KernelT>
 static int set_smem(KernelT kernel, size_t bytes) {
   static std::mutex mu;
-  static std::unordered_set<const void*> done;
+  static std::set<std::pair<int, const void*>> done;   // (device, kernel): per-device attribute
   std::lock_guard<std::mutex> lock(mu);
-  const void* key = (const void*)kernel;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const std::pair<int, const void*> key(dev, (const void*)kernel);
   if (done.count(key)) return 0;
   if (bytes > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
