@@ -43,6 +43,9 @@ __host__ __device__ constexpr int frag_stride(int n) {
 }
 
 // elements per block (tuning: HW_TET_E2 / HW_TET_E4 for N = 2 / 4)
+#ifndef HW_TET_E1
+#define HW_TET_E1 32
+#endif
 #ifndef HW_TET_E2
 #define HW_TET_E2 16
 #endif
@@ -62,7 +65,7 @@ template <int N, typename S = double>
 struct TetMma {
   using D = Dims<N>;
   static constexpr int NP = D::NP_TET, NFN = D::NFN, NFP = 4 * D::NFN;
-  static constexpr int E = (N == 1) ? 32 : (N == 2 ? HW_TET_E2 : (N == 4 ? HW_TET_E4 : 8));
+  static constexpr int E = (N == 1) ? HW_TET_E1 : (N == 2 ? HW_TET_E2 : (N == 4 ? HW_TET_E4 : 8));
   static constexpr int CT = E / 8;
   static constexpr int RT = (NP + 7) / 8;
   static constexpr int NPK = ((NP + 3) / 4) * 4;
