@@ -99,14 +99,20 @@ template <typename L, typename S>
 __device__ __forceinline__ void copy_q_rows(S* dst, const S* src, const int* sk, int ne) {
   constexpr int NP = L::NP, V = L::V16;
   if (NP % V == 0) {
-    constexpr int CF = NP / V, CH = 4 * CF, TOT = L::E * CH;   // 16-byte chunks
+    // warp per element: sk and the bases are warp-uniform
+    constexpr int CF = NP / V, CH = 4 * CF;   // 16-byte chunks per field / element
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int e = warp; e < ne; e += L::W) {
+      const S* s = src + (size_t)sk[e] * 4 * NP;
+      S* d = dst + e * L::EQ;
 #pragma unroll
-    for (int u = 0; u < (TOT + L::NTH - 1) / L::NTH; ++u) {
-      const int i = (int)threadIdx.x + u * L::NTH;
-      if ((TOT % L::NTH) && i >= TOT) break;
-      const int e = i / CH, r = i - e * CH, fld = r / CF, c = r - fld * CF;
-      if (e >= ne) break;
-      cp_async16(dst + e * L::EQ + fld * L::QF + V * c, src + (size_t)sk[e] * 4 * NP + fld * NP + V * c);
+      for (int c0 = 0; c0 < CH; c0 += 32) {
+        const int r = c0 + lane;
+        if (r < CH) {
+          const int fld = r / CF, c = r - fld * CF;
+          cp_async16(d + fld * L::QF + V * c, s + fld * NP + V * c);
+        }
+      }
     }
   } else {
     for (int i = threadIdx.x; i < ne * 4 * NP; i += L::NTH) {
@@ -209,9 +215,9 @@ __device__ __forceinline__ void dense_mma_body(const hw_mesh_t& M, const hw_fiel
   const S* resg = (const S*)E.res[T];
   copy_q_rows<L>(sq, q, sk, ne);
   {   // own traces of the input state (published by the previous stage)
-    copy_rows16<4 * NFP, ETR, NTH, EB>(str, (const S*)M.tr_in[T], sk, ne);
+    copy_rows16_w<4 * NFP, ETR, L::W>(str, (const S*)M.tr_in[T], sk, ne);
   }
-  copy_rows<GEO, L::GEOS, NTH, EB>(sg, (const S*)TY.geo, sk, ne);
+  copy_rows_w<GEO, L::GEOS, L::W>(sg, (const S*)TY.geo, sk, ne);
   copy_rows<4, 4, NTH, EB>(smat, (const S*)TY.mat, sk, ne);
   for (int i = tid; i < ne * NF; i += NTH)
     snc[i] = __ldg(TY.nbr_code + (size_t)sk[i / NF] * NF + i % NF);

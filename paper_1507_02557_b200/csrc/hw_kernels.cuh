@@ -120,6 +120,33 @@ __device__ __forceinline__ void copy_rows16(R* dst, const R* src, const int* sk,
   }
 }
 
+// warp-per-element variants: warp w copies the rows of elements w, w + NW,
+// ...; sk and the row bases are warp-uniform, one add per copy remains
+template <int W, int DW, int NW, typename R>
+__device__ __forceinline__ void copy_rows16_w(R* dst, const R* src, const int* sk, int ne) {
+  constexpr int V = 16 / sizeof(R), CH = W / V;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int e = warp; e < ne; e += NW) {
+    const R* s = src + (size_t)sk[e] * W;
+    R* d = dst + e * DW;
+#pragma unroll
+    for (int c0 = 0; c0 < CH; c0 += 32)
+      if (c0 + lane < CH) cp_async16(d + (c0 + lane) * V, s + (c0 + lane) * V);
+  }
+}
+
+template <int W, int DW, int NW, typename R>
+__device__ __forceinline__ void copy_rows_w(R* dst, const R* src, const int* sk, int ne) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int e = warp; e < ne; e += NW) {
+    const R* s = src + (size_t)sk[e] * W;
+    R* d = dst + e * DW;
+#pragma unroll
+    for (int c0 = 0; c0 < W; c0 += 32)
+      if (c0 + lane < W) cp_async(d + c0 + lane, s + c0 + lane);
+  }
+}
+
 // the same with one scalar per copy (rows of odd length, e.g. records)
 template <int W, int DW, int NTHR, int EMAX, typename R>
 __device__ __forceinline__ void copy_rows(R* dst, const R* src, const int* sk, int ne) {
