@@ -293,6 +293,23 @@ def test_skew_forms_match_reference(tag, spec, N, form, over, native_lib):
     assert rel_err(d.compute_rhs(st), oracle.compute_rhs(d, st)) < 1e-12
 
 
+@pytest.mark.parametrize("scheme,levels", [("lsrk", 1), ("ab3", 1), ("ab3", 3)])
+def test_solve_run_cavity(scheme, levels, native_lib):
+    """app.solve_run (the reference's cavity driver) on the device: L2 error
+    of the standing wave small, discrete energy (tracked on the device every
+    step) non-increasing under the upwind flux and equal to the host value."""
+    from paper_1507_02557_b200.app import RunConfig, cavity_fields, solve_run
+    from paper_1507_02557_b200.dg import discrete_energy
+    cfg = RunConfig(mesh="hybrid:3", N=3, formulation="GL", cfl=0.3, n_levels=levels,
+                    T_final=0.05, scheme=scheme)
+    out = solve_run(cfg, verbose=False)
+    assert out["errors"]["total"] < 5e-3
+    en = [e for _, e in out["energies"]]
+    assert len(en) >= 2 and all(b <= a * (1 + 1e-12) for a, b in zip(en, en[1:]))
+    d = out["disc"]
+    assert abs(en[-1] - discrete_energy(out["state"], d)) <= 1e-10 * en[-1]
+
+
 def _perturbed(spec, amp, seed):
     from paper_1507_02557_b200.mesh import HybridMesh
     m = build_mesh(spec)
