@@ -244,7 +244,23 @@ def forms_fixtures():
     print("forms fixtures written")
 
 
+def convergence_fixtures():
+    """The reference's own h-convergence studies of the cavity mode (AB3,
+    cfl 0.5, T = 0.1): errors and least-squares rates."""
+    from hybridwave.app import RunConfig, convergence_study
+    fd = {}
+    for N, form in [(1, "GL"), (2, "GL"), (3, "GL"), (2, "SEM"), (3, "SEM")]:
+        cfg = RunConfig(mesh="hybrid:2", N=N, formulation=form, cfl=0.5, T_final=0.1)
+        errs, rate = convergence_study(cfg, [2, 3, 4], verbose=False)
+        fd[f"N{N}_{form}/errs"] = np.asarray(errs)
+        fd[f"N{N}_{form}/rate"] = np.array(rate)
+    np.savez_compressed(os.path.join(HERE, "convergence.npz"), **fd)
+    print("convergence fixtures written")
+
+
 if __name__ == "__main__":
+    if sys.argv[1:] == ["convergence"]:
+        sys.exit(convergence_fixtures())
     if sys.argv[1:] == ["forcing"]:
         sys.exit(forcing_fixtures())
     if sys.argv[1:] == ["forms"]:

@@ -310,6 +310,19 @@ def test_solve_run_cavity(scheme, levels, native_lib):
     assert abs(en[-1] - discrete_energy(out["state"], d)) <= 1e-10 * en[-1]
 
 
+@pytest.mark.parametrize("N,form", [(1, "GL"), (2, "GL"), (3, "GL"), (2, "SEM"), (3, "SEM")])
+def test_convergence_matches_reference(N, form, native_lib):
+    """app.convergence_study on the device reproduces the reference's own
+    cavity errors and h-convergence rate (hybrid:2,3,4, AB3, T = 0.1)."""
+    from paper_1507_02557_b200.app import RunConfig, convergence_study
+    G = load_golden("convergence")
+    cfg = RunConfig(mesh="hybrid:2", N=N, formulation=form, cfl=0.5, T_final=0.1)
+    errs, rate = convergence_study(cfg, [2, 3, 4], verbose=False)
+    ref = G[f"N{N}_{form}/errs"]
+    assert np.abs(errs - ref).max() <= 1e-8 * ref.max()
+    assert abs(rate - float(G[f"N{N}_{form}/rate"])) < 1e-6
+
+
 def _perturbed(spec, amp, seed):
     from paper_1507_02557_b200.mesh import HybridMesh
     m = build_mesh(spec)
