@@ -28,8 +28,10 @@ def test_rhs_fp64_matches_reference(case, native_lib):
     assert rel_err(r, ref) < 1e-12
 
 
-@pytest.mark.parametrize("case", [0, 2, 5, 6, 14])
+@pytest.mark.parametrize("case", range(len(RHS_CASES)))
 def test_rhs_fp32(case, native_lib):
+    """fp32 storage (fp64 arithmetic in the kernels) on every reference case:
+    within the north star's fp32 bound (1e-4), in practice ~1e-7."""
     d, st = make_case(case, dtype=torch.float32)
     r = d.compute_rhs(st)
     ref = {t: RHS[f"{case}/{t}"] for t in d.types}
