@@ -34,7 +34,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "GDOF·stage/s per LSRK step (N=1..5, hybrid mesh, 1/2/4/8 B200); kernel GB/s vs HBM"
 UNIT = "GDOF*stage/s"
-GEO_WORDS = {"hex": 72, "wedge": 40, "pyramid": 39, "tet": 33}
+GEO_WORDS = {"hex": 72, "wedge": 40, "pyramid": 40, "tet": 33}
 NFACES = {"hex": 6, "wedge": 5, "pyramid": 5, "tet": 4}
 
 

@@ -43,7 +43,9 @@ enum { HW_GL = 0, HW_SEM = 1 };
  *                if affine: G[3][3], J, per face (n_x, n_y, n_z, Js), 1/J
  *   wedge    40: G[3][3] (G[c][x] = d r_c / d x_x), 1/sqrt(J), 5 faces x FS
  *                (scale = Js/sqrt(J))
- *   pyramid  39: G[3][3], 5 faces x FS (scale = Js/J)
+ *   pyramid  40: G[3][3], 5 faces x FS (scale = Js/J; non-affine: Js), non-affine
+ *                flag (then op[8] = (K, Np, 10) G, J per node, op[9] =
+ *                (K, NFQ, 4) base-face normal, Js per point)
  *   tet      33: G[3][3], 4 faces x FS (scale = Js/J)
  * mat: per element (kappa, 1/rho, rho*c, 0).
  * op/iop: constant operators and index tables, layouts documented in

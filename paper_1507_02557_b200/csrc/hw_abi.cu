@@ -263,9 +263,10 @@ static int launch_rhs_all(const hw_mesh_t& M, const hw_fields_t& Q, const Epi& E
         rc = !tet_scalar() ? launch_dense_mma<N, HW_WEDGE, R>(M, Q, E, list, n, st)
                            : launch_dense<N, HW_WEDGE, R>(M, Q, E, list, n, st);
         break;
-      case HW_PYRAMID:
-        rc = !tet_scalar() ? launch_dense_mma<N, HW_PYRAMID, R>(M, Q, E, list, n, st)
-                           : launch_dense<N, HW_PYRAMID, R>(M, Q, E, list, n, st);
+      case HW_PYRAMID:   // non-affine pyramids present (op[8]): scalar kernel
+        rc = (!tet_scalar() && M.t[HW_PYRAMID].op[8] == nullptr)
+                 ? launch_dense_mma<N, HW_PYRAMID, R>(M, Q, E, list, n, st)
+                 : launch_dense<N, HW_PYRAMID, R>(M, Q, E, list, n, st);
         break;
       case HW_TET:
         if (tet_scalar() && M.t[HW_TET].form == HW_FORM_SKEW)

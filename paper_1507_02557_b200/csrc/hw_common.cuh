@@ -29,7 +29,10 @@ struct Dims {
 // avg(rho c), 1/avg(rho c)).  Hex: 8 vertices, per face (avg, 1/avg), an
 // affine flag, then for affine hexes G[3][3], J and per face (n, Js).
 constexpr int FS = 6;
-constexpr int GEO_HEX = 72, GEO_WEDGE = 10 + 5 * FS, GEO_PYR = 9 + 5 * FS,
+// pyramid: word 39 = non-affine flag (per-node geometry in op[8], base-face
+// points in op[9]; scalar kernel)
+constexpr int PY_NAFF = 9 + 5 * FS;
+constexpr int GEO_HEX = 72, GEO_WEDGE = 10 + 5 * FS, GEO_PYR = 9 + 5 * FS + 1,
               GEO_TET = 9 + 4 * FS;
 constexpr int HX_Z = 24, HX_AFF = 36, HX_G = 37, HX_J = 46, HX_F = 47, HX_IJ = 71;
 constexpr int NF_HEX = 6, NF_WEDGE = 5, NF_PYR = 5, NF_TET = 4;

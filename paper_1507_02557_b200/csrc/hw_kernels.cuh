@@ -426,19 +426,33 @@ __global__ void __launch_bounds__(NT) dense_kernel(hw_mesh_t M, hw_fields_t Q, E
   const int ne = (int)((nwork - w0) < EPB ? (nwork - w0) : EPB);
   prologue<N, T, R>(M, Q, E, list, w0, ne, sm, sk, snc, sne);
 
-  // contravariant velocity components v_c = sum_x G[c][x] u_x
+  const bool skew = TY.form == HW_FORM_SKEW;             // flux form
+  const bool vskew = skew || T == HW_WEDGE;              // volume (wedge: always skew)
+  // non-affine pyramids (record flag): G and J at every level node from
+  // op[8] (K, Np, 10), base-face normals and Js at its points from op[9]
+  // (hybridwave/dg.py:446-463, 479-490: J stays inside the skew volume sum
+  // and the mass inverse divides by J per node)
+  const R* ngeo = (T == HW_PYRAMID) ? (const R*)TY.op[8] : nullptr;
+  auto naff = [&](int e) { return T == HW_PYRAMID && sg[e * X::GEO + PY_NAFF] != R(0); };
+
+  // contravariant velocity components v_c = sum_x G[c][x] u_x (x J for the
+  // non-affine skew pyramid)
   for (int i = tid; i < ne * NP; i += NT) {
     const int e = i / NP, n = i - e * NP;
     const R* G = sg + e * X::GEO;
+    R sc = R(1);
+    if (naff(e)) {
+      G = ngeo + ((size_t)sk[e] * NP + n) * 10;
+      if (vskew) sc = G[9];
+    }
     const R* u = sq + e * 4 * NP + NP + n;
 #pragma unroll
     for (int c = 0; c < 3; ++c)
-      sv[(e * 3 + c) * NP + n] = G[c * 3] * u[0] + G[c * 3 + 1] * u[NP] + G[c * 3 + 2] * u[2 * NP];
+      sv[(e * 3 + c) * NP + n] =
+          sc * (G[c * 3] * u[0] + G[c * 3 + 1] * u[NP] + G[c * 3 + 2] * u[2 * NP]);
   }
   __syncthreads();
 
-  const bool skew = TY.form == HW_FORM_SKEW;             // flux form
-  const bool vskew = skew || T == HW_WEDGE;              // volume (wedge: always skew)
   const R* AT = (const R*)TY.op[0];
   const R* AR = (const R*)TY.op[1];
   R acc[S][4];
@@ -462,6 +476,29 @@ __global__ void __launch_bounds__(NT) dense_kernel(hw_mesh_t M, hw_fields_t Q, E
           div += ldg(AR + (0 * NP + m) * NP + n) * v[m] + ldg(AR + (1 * NP + m) * NP + n) * v[NP + m] +
                  ldg(AR + (2 * NP + m) * NP + n) * v[2 * NP + m];
         }
+      } else if (naff(e)) {
+        // strong non-affine pyramid: div u(n) = sum_{c,x} G(n)[c][x] (D_c u_x)(n)
+        const R* Gn = ngeo + ((size_t)sk[e] * NP + n) * 10;
+        R du[3][3] = {{R(0), R(0), R(0)}, {R(0), R(0), R(0)}, {R(0), R(0), R(0)}};
+#pragma unroll 2
+        for (int m = 0; m < NP; ++m) {
+          const R pm = p[m];
+          const R a[3] = {ldg(AT + (0 * NP + m) * NP + n), ldg(AT + (1 * NP + m) * NP + n),
+                          ldg(AT + (2 * NP + m) * NP + n)};
+          dp0 += a[0] * pm;
+          dp1 += a[1] * pm;
+          dp2 += a[2] * pm;
+#pragma unroll
+          for (int x = 0; x < 3; ++x) {
+            const R um = p[(1 + x) * NP + m];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) du[x][c] += a[c] * um;
+          }
+        }
+#pragma unroll
+        for (int x = 0; x < 3; ++x)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) div += Gn[3 * c + x] * du[x][c];
       } else {
 #pragma unroll 4
         for (int m = 0; m < NP; ++m) {
@@ -476,7 +513,12 @@ __global__ void __launch_bounds__(NT) dense_kernel(hw_mesh_t M, hw_fields_t Q, E
         }
       }
       const R* G = sg + e * X::GEO;
-      acc[s][0] = vskew ? div : -div;
+      R iJ = R(1);
+      if (naff(e)) {
+        G = ngeo + ((size_t)sk[e] * NP + n) * 10;
+        iJ = R(1) / G[9];
+      }
+      acc[s][0] = vskew ? div * iJ : -div;   // affine: J folded into the operators
 #pragma unroll
       for (int x = 0; x < 3; ++x) acc[s][1 + x] = -(G[x] * dp0 + G[3 + x] * dp1 + G[6 + x] * dp2);
     }
@@ -504,7 +546,13 @@ __global__ void __launch_bounds__(NT) dense_kernel(hw_mesh_t M, hw_fields_t Q, E
     }
     const R um[3] = {own[1], own[2], own[3]};
     const R* g = sg + e * X::GEO + X::GF + FS * f;
-    const R nrm[3] = {g[0], g[1], g[2]};
+    R nrm[3] = {g[0], g[1], g[2]};
+    R fscale = g[3];
+    if (T == HW_PYRAMID && f == 0 && naff(e)) {   // bilinear base: per-point n, Js
+      const R* bp = (const R*)TY.op[9] + ((size_t)sk[e] * Dims<N>::NFQ + jj) * 4;
+      nrm[0] = ldg(bp); nrm[1] = ldg(bp + 1); nrm[2] = ldg(bp + 2);
+      fscale = ldg(bp + 3);
+    }
     const int code = snc[e * NF + f];
     R pp, up[3];
     if (code & HW_NBR_BOUNDARY) {
@@ -517,8 +565,8 @@ __global__ void __launch_bounds__(NT) dense_kernel(hw_mesh_t M, hw_fields_t Q, E
     R tp, tu, fp, fu;
     penalties(g[4], g[5], pen, tp, tu);
     upwind_flux(own[0], um, pp, up, nrm, tp, tu, skew, fp, fu);
-    sf[(e * NFP + j) * 2 + 0] = fp * g[3];
-    sf[(e * NFP + j) * 2 + 1] = fu * g[3];
+    sf[(e * NFP + j) * 2 + 0] = fp * fscale;
+    sf[(e * NFP + j) * 2 + 1] = fu * fscale;
   }
   __syncthreads();
 
@@ -530,22 +578,40 @@ __global__ void __launch_bounds__(NT) dense_kernel(hw_mesh_t M, hw_fields_t Q, E
     if (e >= ne) continue;
     const R* fl = sf + e * NFP * 2;
     const R* g = sg + e * X::GEO + X::GF;
+    const bool na = naff(e);
+    R lift[4] = {R(0), R(0), R(0), R(0)};
 #pragma unroll
     for (int f = 0; f < NF; ++f) {
-      R tp = R(0), tu = R(0);
+      R tp = R(0), tu = R(0), tux[3] = {R(0), R(0), R(0)};
       const int j0 = X::off(f);
+      const bool pnrm = T == HW_PYRAMID && f == 0 && na;   // per-point normals
 #pragma unroll 4
       for (int jj = 0; jj < X::cnt(f); ++jj) {
         const int j = j0 + jj;
         const R l = ldg(LT + j * NP + n);
         tp += l * fl[2 * j];
-        tu += l * fl[2 * j + 1];
+        if (pnrm) {
+          const R* bp = (const R*)TY.op[9] + ((size_t)sk[e] * Dims<N>::NFQ + jj) * 4;
+          const R lu = l * fl[2 * j + 1];
+          tux[0] += lu * ldg(bp); tux[1] += lu * ldg(bp + 1); tux[2] += lu * ldg(bp + 2);
+        } else {
+          tu += l * fl[2 * j + 1];
+        }
       }
-      acc[s][0] += tp;
-      acc[s][1] += g[FS * f + 0] * tu;
-      acc[s][2] += g[FS * f + 1] * tu;
-      acc[s][3] += g[FS * f + 2] * tu;
+      lift[0] += tp;
+      if (pnrm) {
+        lift[1] += tux[0]; lift[2] += tux[1]; lift[3] += tux[2];
+      } else {
+        lift[1] += g[FS * f + 0] * tu;
+        lift[2] += g[FS * f + 1] * tu;
+        lift[3] += g[FS * f + 2] * tu;
+      }
     }
+    // mass inverse: affine J is folded into the face scale; non-affine
+    // pyramids divide by J at the node
+    const R liJ = na ? R(1) / ldg(ngeo + ((size_t)sk[e] * NP + n) * 10 + 9) : R(1);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[s][c] += lift[c] * liJ;
     const R kap = smat[e * 4 + 0], irho = smat[e * 4 + 1];
     const size_t base = (size_t)sk[e] * 4 * NP + n;
     R* qe = sq + e * 4 * NP + n;

@@ -25,10 +25,11 @@ _INTERIOR_ABC = {"tet": np.array([[-0.5, -0.5, -0.5]]), "wedge": np.array([[0.0,
 
 
 def _affine_check(t, verts, N):
-    """The nodal-face representation needs affine wedges/pyramids (constant
-    J); tets are always affine."""
+    """The nodal-face representation of the LSC-DG wedge needs affine wedges
+    (its traces carry 1/sqrt(J)); non-affine pyramids run through per-node
+    geometry (pyramid_node_geometry); tets are always affine."""
     from .refelem import affine_mask
-    if t not in ("wedge", "pyramid") or len(verts) == 0:
+    if t != "wedge" or len(verts) == 0:
         return
     bad = ~affine_mask(t, verts, tol=1e-10)
     if bad.any():
@@ -80,18 +81,27 @@ def geometry_records(t, verts, zavg):
     _, J, G, _ = geometric_factors_batch(t, verts, _INTERIOR_ABC[t], label=t)
     J, G = J[:, 0], G[:, 0]
     cols = [G.reshape(K, 9)]
+    naff = None
     if t == "wedge":
         isj = 1.0 / np.sqrt(J)
         cols.append(isj[:, None])
         scale = isj
     else:
         scale = 1.0 / J
+        if t == "pyramid":
+            # non-affine pyramids: face scale Js only (the kernel divides the
+            # lift by J at each node); flag in the last word
+            from .refelem import affine_mask
+            naff = ~affine_mask(t, verts, tol=1e-10)
+            scale = np.where(naff, 1.0, scale)
     for f, (ftype, _) in enumerate(FACES[t]):
         _, Js, nrm = face_geometry_batch(t, verts, f, _CENTROID2D[ftype])
         cols.append(nrm[:, 0, :])
         cols.append((Js[:, 0] * scale)[:, None])
         cols.append(zavg[:, f:f + 1])
         cols.append(1.0 / zavg[:, f:f + 1])
+    if naff is not None:
+        cols.append(naff.astype(float)[:, None])
     return np.hstack(cols)
 
 
@@ -132,6 +142,18 @@ def hex_node_face_points(dops, N):
             idx = (n // (n1 * n1), (n // n1) % n1, n % n1)
             out[f, n] = lut[n - idx[axis] * strides[axis]]
     return out
+
+
+def pyramid_node_geometry(verts, ops, dops):
+    """Non-affine pyramids (hybridwave/dg.py:135-152, 446-463): op[8] =
+    (K, Np, 10) G[c][x] and J at the level nodes, op[9] = (K, NFQ, 4) unit
+    normal and Js at the bilinear base face's points (the device face order)."""
+    _, J, G, _ = geometric_factors_batch("pyramid", verts, ops.level_abc, label="pyramid")
+    K, Np = J.shape
+    node = np.concatenate([G.reshape(K, Np, 9), J[..., None]], axis=2)
+    _, Js, nrm = face_geometry_batch("pyramid", verts, 0, dops["quad2d"])
+    base = np.concatenate([nrm, Js[..., None]], axis=2)
+    return node, base
 
 
 def hex_face_point_coefficients(dops, N):
@@ -175,7 +197,8 @@ def pack_mesh(disc):
             "geo": geometry_records(t, verts, face_impedance_avg(mesh, t)),
             "mat": material_records(np.asarray(mesh.materials[t], dtype=float)),
             "nbr_elem": elem, "nbr_code": code,
-            "op": {**_pack_ops(t, dops), **(_tet_extra_ops(disc.ops[t], dops) if t == "tet" else {})},
+            "op": {**_pack_ops(t, dops), **(_tet_extra_ops(disc.ops[t], dops) if t == "tet" else {}),
+                   **(_pyramid_extra_ops(verts, disc.ops[t], dops) if t == "pyramid" else {})},
             "iop": _pack_iops(t, dops, disc.N, mesh, perm_tri, face_offsets, dops_all,
                               perm_quad, disc.formulation.kind == "SEM"),
             "nfp": int(dops["face_offsets"][-1]),
@@ -188,6 +211,16 @@ def pack_mesh(disc):
 
 # operator slots read as fp64 DMMA fragments by the tensor-core kernels
 MMA_SLOTS = {"hex": (), "tet": (2, 3, 5), "wedge": (2, 3, 4, 7), "pyramid": (2, 3, 4, 7)}
+
+
+def _pyramid_extra_ops(verts, ops, dops):
+    """op[8], op[9] only when the mesh has non-affine pyramids (their
+    presence routes the pyramids to the per-node-geometry scalar kernel)."""
+    from .refelem import affine_mask
+    if len(verts) == 0 or affine_mask("pyramid", verts, tol=1e-10).all():
+        return {}
+    node, base = pyramid_node_geometry(verts, ops, dops)
+    return {8: node, 9: base}
 
 
 def _tet_extra_ops(ops, d):

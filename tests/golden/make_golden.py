@@ -258,7 +258,33 @@ def convergence_fixtures():
     print("convergence fixtures written")
 
 
+def nonaffine_fixtures():
+    """compute_rhs on jittered (non-affine) pyramid and hex meshes, random
+    states; same perturbation as tests/test_gpu_parity.py::_perturbed."""
+    from hybridwave.mesh import HybridMesh
+    fd = {}
+    for tag, spec, N, form, seed in [("pyr3_gl2", "pyramid:3", 2, "GL", 3),
+                                     ("pyr3_sem3", "pyramid:3", 3, "SEM", 4),
+                                     ("pyr2_gl4", "pyramid:2", 4, "GL", 5)]:
+        m = build_mesh(spec)
+        rng = np.random.default_rng(seed)
+        X = m.vertices.copy()
+        inner = np.all((X > 1e-9) & (X < 1 - 1e-9), axis=1)
+        X[inner] += 0.04 * rng.uniform(-1, 1, (inner.sum(), 3))
+        m = HybridMesh(X, m.blocks)
+        d = Discretization(m, N, form)
+        rng = np.random.default_rng(seed + 10)
+        st = {t: rng.standard_normal((d.n_elems[t], 4, d.ops[t].Np)) for t in d.types}
+        rhs = d.compute_rhs(st, 0.0)
+        for t in d.types:
+            fd[f"{tag}/rhs/{t}"] = rhs[t]
+    np.savez_compressed(os.path.join(HERE, "nonaffine.npz"), **fd)
+    print("non-affine fixtures written")
+
+
 if __name__ == "__main__":
+    if sys.argv[1:] == ["nonaffine"]:
+        sys.exit(nonaffine_fixtures())
     if sys.argv[1:] == ["convergence"]:
         sys.exit(convergence_fixtures())
     if sys.argv[1:] == ["forcing"]:
