@@ -55,6 +55,9 @@ __host__ __device__ constexpr int frag_stride(int n) {
 #ifndef HW_TET_MINB
 #define HW_TET_MINB 6
 #endif
+#ifndef HW_TET_MINB_XW
+#define HW_TET_MINB_XW 7
+#endif
 #ifndef HW_TET_MINB32
 #define HW_TET_MINB32 12
 #endif
@@ -71,7 +74,14 @@ struct TetMma {
   static constexpr int NPK = ((NP + 3) / 4) * 4;
   static constexpr int NFK = ((NFN + 3) / 4) * 4;
   static constexpr int W = RT * CT;
-  static constexpr int NTH = 32 * W;
+#ifndef HW_TET_XW
+#define HW_TET_XW 1
+#endif
+  // XW extra warps join the copy / flux phases only (GEMM warps: W).
+  // Measured (hybrid:38): fp64 N=3 tet 188.5 -> 180.4 us with one extra warp
+  // (MINB 7); slower for fp32 N=3 (141 -> 148) and fp64 N=1,2,4,5.
+  static constexpr int XW = (sizeof(S) == 8 && N == 3) ? HW_TET_XW : 0;
+  static constexpr int NTH = 32 * (W + XW);
   static constexpr bool VEC = (NPK == NP) && ((4 * NP * sizeof(S)) % 16 == 0);  // 16-byte rows
   static constexpr int EQ = frag_stride<S>(4 * NPK);        // q / res element stride
   static constexpr int EV = frag_stride<S>(3 * NPK);        // v_c
@@ -86,7 +96,7 @@ struct TetMma {
 #ifndef HW_TET_MINB_MID
 #define HW_TET_MINB_MID 4
 #endif
-  static constexpr int MINB = (W <= 4) ? (sizeof(S) == 8 ? HW_TET_MINB : HW_TET_MINB32)
+  static constexpr int MINB = (W <= 4) ? (sizeof(S) == 8 ? (XW ? HW_TET_MINB_XW : HW_TET_MINB) : HW_TET_MINB32)
                                        : ((W <= 8) ? HW_TET_MINB_MID : 1);
   // flux items (element, face point) per thread
   static constexpr int IT = (E * NFP + NTH - 1) / NTH;
@@ -201,7 +211,8 @@ __global__ void __launch_bounds__(TetMma<N, S>::NTH, TetMma<N, S>::MINB)
   const int bk = lane & 3, bcol = ct * 8 + (lane >> 2);
   constexpr bool skew = SK;
   R dp[3][2] = {{0, 0}, {0, 0}, {0, 0}}, dv[2] = {0, 0};
-  {
+  const bool gw = warp < L::W;   // GEMM warp
+  if (gw) {
     const R* Dg = (const R*)TY.op[2];   // [3][RT][NPK/4][32] A fragments, zero padded
     const R* Bg = (const R*)TY.op[5];   // skew: invM D_c^T M fragments
     const S* bq = sq + bcol * EQ + bk;
@@ -269,7 +280,7 @@ __global__ void __launch_bounds__(TetMma<N, S>::NTH, TetMma<N, S>::MINB)
     for (int x = 0; x < 3; ++x)
       accu[x][i] = -(R(G[x]) * dp[0][i] + R(G[3 + x]) * dp[1][i] + R(G[6 + x]) * dp[2][i]);
   }
-  {
+  if (gw) {
     const R* Lg = (const R*)TY.op[3];   // [4][RT][NFK/4][32] A fragments
     const S* bp = sfp + bcol * EF + bk;
     const S* bu = sfu + bcol * EF + bk;
@@ -296,7 +307,7 @@ __global__ void __launch_bounds__(TetMma<N, S>::NTH, TetMma<N, S>::MINB)
     __syncthreads();
   }
   const int n = rt * 8 + (lane >> 2);
-  if (n < NP) {
+  if (gw && n < NP) {
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
       const int e = col0 + i;
