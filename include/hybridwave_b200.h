@@ -42,7 +42,9 @@ enum { HW_GL = 0, HW_SEM = 1 };
  *   hex      72: 8 vertices (x, y, z); per face (avg, 1/avg); affine flag;
  *                if affine: G[3][3], J, per face (n_x, n_y, n_z, Js), 1/J
  *   wedge    40: G[3][3] (G[c][x] = d r_c / d x_x), 1/sqrt(J), 5 faces x FS
- *                (scale = Js/sqrt(J))
+ *                (scale = Js/sqrt(J)); non-affine wedges in the mesh: op[8] =
+ *                per-element cubature geometry, op[9] = cubature operators
+ *                (layout: struct Naw, csrc/hw_kernels.cuh), scalar kernel
  *   pyramid  40: G[3][3], 5 faces x FS (scale = Js/J; non-affine: Js), non-affine
  *                flag (then op[8] = (K, Np, 10) G, J per node, op[9] =
  *                (K, NFQ, 4) base-face normal, Js per point)

@@ -76,10 +76,15 @@ template <int N, int T, typename R>
 static int launch_dense(const hw_mesh_t& M, const hw_fields_t& Q, const Epi& E,
                         const int32_t* list, int64_t n, cudaStream_t st) {
   using L = Smem<N, T, R>;
+  // non-affine wedges: cubature scratch (Naw) behind the layout
+  constexpr size_t NAW_BYTES =
+      (T == HW_WEDGE) ? 16 + sizeof(R) * (size_t)L::EPB * Naw<N>::CS : 0;
+  static_assert(L::BYTES + NAW_BYTES <= 227 * 1024, "dense_kernel shared memory");
+  const size_t bytes = L::BYTES + (M.t[T].op[8] != nullptr ? NAW_BYTES : 0);
   int rc;
-  if ((rc = set_smem(dense_kernel<N, T, R>, L::BYTES))) return rc;
-  dense_kernel<N, T, R><<<(unsigned)((n + L::EPB - 1) / L::EPB), NT, L::BYTES, st>>>(M, Q, E,
-                                                                                    list, n);
+  if ((rc = set_smem(dense_kernel<N, T, R>, L::BYTES + NAW_BYTES))) return rc;
+  dense_kernel<N, T, R><<<(unsigned)((n + L::EPB - 1) / L::EPB), NT, bytes, st>>>(M, Q, E,
+                                                                                  list, n);
   return check_launch("dense_kernel");
 }
 
@@ -205,7 +210,9 @@ static int launch_traces_all(const hw_mesh_t& M, const hw_fields_t& Q, const hw_
     subset_of(sub, t, K, &list, &n);
     if (n <= 0) continue;
     if (t == HW_HEX) rc = launch_traces_t<N, HW_HEX, R>(M, Q, TR, list, n, st);
-    else if (t == HW_WEDGE) rc = launch_traces_mma<N, HW_WEDGE, R>(M, Q, TR, list, n, st);
+    else if (t == HW_WEDGE)   // non-affine wedges (op[8]): per-point 1/sqrt(J), scalar kernel
+      rc = M.t[HW_WEDGE].op[8] == nullptr ? launch_traces_mma<N, HW_WEDGE, R>(M, Q, TR, list, n, st)
+                                          : launch_traces_t<N, HW_WEDGE, R>(M, Q, TR, list, n, st);
     else rc = launch_traces_mma<N, HW_PYRAMID, R>(M, Q, TR, list, n, st);
     if (rc) return rc;
   }
@@ -259,9 +266,10 @@ static int launch_rhs_all(const hw_mesh_t& M, const hw_fields_t& Q, const Epi& E
         rc = check_launch("hex_kernel");
         break;
       }
-      case HW_WEDGE:   // fp64 DMMA for both storage precisions
-        rc = !tet_scalar() ? launch_dense_mma<N, HW_WEDGE, R>(M, Q, E, list, n, st)
-                           : launch_dense<N, HW_WEDGE, R>(M, Q, E, list, n, st);
+      case HW_WEDGE:   // fp64 DMMA for both storage precisions; non-affine wedges (op[8]): scalar
+        rc = (!tet_scalar() && M.t[HW_WEDGE].op[8] == nullptr)
+                 ? launch_dense_mma<N, HW_WEDGE, R>(M, Q, E, list, n, st)
+                 : launch_dense<N, HW_WEDGE, R>(M, Q, E, list, n, st);
         break;
       case HW_PYRAMID:   // non-affine pyramids present (op[8]): scalar kernel
         rc = (!tet_scalar() && M.t[HW_PYRAMID].op[8] == nullptr)

@@ -48,6 +48,29 @@ struct TT<N, HW_WEDGE> {
   __host__ __device__ static constexpr int stage(int f) { return 4 * cnt(f); }
 };
 
+// Non-affine LSC-DG wedges (op[8] present: every wedge of the mesh runs the
+// scalar dense kernel).  The reference's two cubature passes with G and
+// grad J at every volume cubature point (hybridwave/dg.py:423-444) and, on
+// the triangle faces, its face cubature (dg.py:300-357): own and neighbour
+// traces are published / staged as their polynomial part at the nodal face
+// points, interpolated to the cubature points (exact: degree N) and scaled
+// by each side's 1/sqrt(J) there.  Quad faces keep the device points (the
+// reference's quad cubature) with per-point n, Js, 1/sqrt(J).
+//   op[8] (K, GW): [NQ][12] w G[c][x], w gJfac[x] | [NFP][5] n, Js/sqrt(J),
+//                  1/sqrt(J) (quad points) | [2][NQT][3] 1/sqrt(J) own,
+//                  1/sqrt(J) neighbour, w Js/sqrt(J) (triangle cubature)
+//   op[9]: V, Dr3, Ds3, Dt3 as [m][q] | the same as [q][m] | Lq [2][NQT][NFN]
+//          | Vf [2][NQT][NP] (triangle faces)
+template <int N>
+struct Naw {
+  using D = Dims<N>;
+  static constexpr int NP = D::NP_WEDGE, NQ = D::NQ_WEDGE, NQT = 6 * D::N1 * D::N1,
+                       NFN = D::NFN, NFP = D::NFP_WEDGE;
+  static constexpr int GF = NQ * 12, GT = GF + NFP * 5, GW = GT + 2 * NQT * 3;
+  static constexpr int CVN = 4 * NP * NQ, CLQ = 8 * NP * NQ, CVF = CLQ + 2 * NQT * NFN;
+  static constexpr int CS = 7 * NQ + 4 * NQT;   // smem scratch per element
+};
+
 template <int N>
 struct TT<N, HW_PYRAMID> {
   using D = Dims<N>;
@@ -272,7 +295,11 @@ __device__ __forceinline__ void publish_traces(const hw_mesh_t& M, const R* sq, 
         a0 += ev * qe[m]; a1 += ev * qe[NP + m]; a2 += ev * qe[2 * NP + m]; a3 += ev * qe[3 * NP + m];
       }
       if (T == HW_WEDGE) {
-        const R isj = sg[e * X::GEO + 9];
+        R isj = sg[e * X::GEO + 9];
+        if (TY.op[8] != nullptr)   // non-affine: quad points x 1/sqrt(J), triangles polynomial
+          isj = j < 2 * D::NFN ? R(1)
+                               : ldg((const R*)TY.op[8] + (size_t)sk[e] * Naw<N>::GW +
+                                     Naw<N>::GF + j * 5 + 4);
         a0 *= isj; a1 *= isj; a2 *= isj; a3 *= isj;
       }
     }
@@ -434,6 +461,45 @@ __global__ void __launch_bounds__(NT) dense_kernel(hw_mesh_t M, hw_fields_t Q, E
   // and the mass inverse divides by J per node)
   const R* ngeo = (T == HW_PYRAMID) ? (const R*)TY.op[8] : nullptr;
   auto naff = [&](int e) { return T == HW_PYRAMID && sg[e * X::GEO + PY_NAFF] != R(0); };
+  // non-affine wedges (Naw): cubature scratch behind the int arrays
+  using W8 = Naw<N>;
+  const bool naw = T == HW_WEDGE && TY.op[8] != nullptr;
+  const R* wgeo = (const R*)TY.op[8];
+  const R* wcst = (const R*)TY.op[9];
+  R* cs = reinterpret_cast<R*>(
+      (reinterpret_cast<uintptr_t>(sne + EPB * NF) + 15) & ~uintptr_t(15));
+  if (T == HW_WEDGE && naw) {
+    // trial pass at the volume cubature points: w grad p (incl. the
+    // -p grad J / 2J term), w G u, w gJfac . u (hybridwave/dg.py:430-443)
+    for (int i = tid; i < ne * W8::NQ; i += NT) {
+      const int e = i / W8::NQ, qp = i - e * W8::NQ;
+      const R* qe = sq + e * 4 * NP;
+      R U[4] = {R(0), R(0), R(0), R(0)}, dc[3] = {R(0), R(0), R(0)};
+#pragma unroll 2
+      for (int m = 0; m < NP; ++m) {
+        const R v = ldg(wcst + m * W8::NQ + qp), pm = qe[m];
+        U[0] += v * pm;
+        U[1] += v * qe[NP + m];
+        U[2] += v * qe[2 * NP + m];
+        U[3] += v * qe[3 * NP + m];
+        dc[0] += ldg(wcst + (NP + m) * W8::NQ + qp) * pm;
+        dc[1] += ldg(wcst + (2 * NP + m) * W8::NQ + qp) * pm;
+        dc[2] += ldg(wcst + (3 * NP + m) * W8::NQ + qp) * pm;
+      }
+      const R* gq = wgeo + (size_t)sk[e] * W8::GW + qp * 12;
+      R gl[12];
+#pragma unroll
+      for (int r = 0; r < 12; ++r) gl[r] = ldg(gq + r);
+      R* c = cs + e * W8::CS + qp;
+#pragma unroll
+      for (int x = 0; x < 3; ++x)
+        c[x * W8::NQ] = gl[x] * dc[0] + gl[3 + x] * dc[1] + gl[6 + x] * dc[2] + gl[9 + x] * U[0];
+#pragma unroll
+      for (int cc = 0; cc < 3; ++cc)
+        c[(3 + cc) * W8::NQ] = gl[3 * cc] * U[1] + gl[3 * cc + 1] * U[2] + gl[3 * cc + 2] * U[3];
+      c[6 * W8::NQ] = gl[9] * U[1] + gl[10] * U[2] + gl[11] * U[3];
+    }
+  }
 
   // contravariant velocity components v_c = sum_x G[c][x] u_x (x J for the
   // non-affine skew pyramid)
@@ -462,7 +528,23 @@ __global__ void __launch_bounds__(NT) dense_kernel(hw_mesh_t M, hw_fields_t Q, E
     const int e = i / NP, n = i - e * NP;
 #pragma unroll
     for (int c = 0; c < 4; ++c) acc[s][c] = R(0);
-    if (e < ne) {
+    if (T == HW_WEDGE && naw && e < ne) {
+      // test pass: R_u = -V^T (w grad p), R_p = sum_c D3_c^T (w G u)_c + V^T (w gJ . u)
+      const R* vn = wcst + W8::CVN;
+      const R* c = cs + e * W8::CS;
+      R a0 = R(0), a1 = R(0), a2 = R(0), a3 = R(0);
+#pragma unroll 2
+      for (int qp = 0; qp < W8::NQ; ++qp) {
+        const R v = ldg(vn + qp * NP + n), dr = ldg(vn + (W8::NQ + qp) * NP + n),
+                ds = ldg(vn + (2 * W8::NQ + qp) * NP + n), dt = ldg(vn + (3 * W8::NQ + qp) * NP + n);
+        a1 -= v * c[qp];
+        a2 -= v * c[W8::NQ + qp];
+        a3 -= v * c[2 * W8::NQ + qp];
+        a0 += dr * c[3 * W8::NQ + qp] + ds * c[4 * W8::NQ + qp] + dt * c[5 * W8::NQ + qp] +
+              v * c[6 * W8::NQ + qp];
+      }
+      acc[s][0] = a0; acc[s][1] = a1; acc[s][2] = a2; acc[s][3] = a3;
+    } else if (e < ne) {
       R div = R(0), dp0 = R(0), dp1 = R(0), dp2 = R(0);
       const R* p = sq + e * 4 * NP;
       const R* v = sv + e * 3 * NP;
@@ -533,6 +615,7 @@ __global__ void __launch_bounds__(NT) dense_kernel(hw_mesh_t M, hw_fields_t Q, E
     const int e = i / NFP, j = i - e * NFP;
     int jj;
     const int f = face_of_point<N, T>(j, jj);
+    if (T == HW_WEDGE && naw && f < 2) continue;   // triangle faces: cubature loop below
     const R* qe = sq + e * 4 * NP;
     R own[4];
     if (T == HW_TET) {
@@ -553,6 +636,11 @@ __global__ void __launch_bounds__(NT) dense_kernel(hw_mesh_t M, hw_fields_t Q, E
       nrm[0] = ldg(bp); nrm[1] = ldg(bp + 1); nrm[2] = ldg(bp + 2);
       fscale = ldg(bp + 3);
     }
+    if (T == HW_WEDGE && naw) {   // bilinear quad face: per-point n, Js/sqrt(J)
+      const R* fb = wgeo + (size_t)sk[e] * W8::GW + W8::GF + j * 5;
+      nrm[0] = ldg(fb); nrm[1] = ldg(fb + 1); nrm[2] = ldg(fb + 2);
+      fscale = ldg(fb + 3);
+    }
     const int code = snc[e * NF + f];
     R pp, up[3];
     if (code & HW_NBR_BOUNDARY) {
@@ -567,6 +655,49 @@ __global__ void __launch_bounds__(NT) dense_kernel(hw_mesh_t M, hw_fields_t Q, E
     upwind_flux(own[0], um, pp, up, nrm, tp, tu, skew, fp, fu);
     sf[(e * NFP + j) * 2 + 0] = fp * fscale;
     sf[(e * NFP + j) * 2 + 1] = fu * fscale;
+  }
+  if (T == HW_WEDGE && naw) {
+    // triangle faces at the reference's face cubature points
+    const R* LQ = wcst + W8::CLQ;
+    R* sfc = cs + 7 * W8::NQ;
+    for (int i = tid; i < ne * 2 * W8::NQT; i += NT) {
+      const int e = i / (2 * W8::NQT), r = i - e * 2 * W8::NQT;
+      const int f = r / W8::NQT, qt = r - f * W8::NQT;
+      const R* lq = LQ + (f * W8::NQT + qt) * W8::NFN;
+      const R* te = sm + L::STR + e * 4 * NFP + f * W8::NFN;   // own polynomial traces
+      const int code = snc[e * NF + f];
+      const bool bnd = code & HW_NBR_BOUNDARY;
+      R own[4] = {R(0), R(0), R(0), R(0)}, nb[4] = {R(0), R(0), R(0), R(0)};
+      for (int jj = 0; jj < W8::NFN; ++jj) {
+        const R l = ldg(lq + jj);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) own[c] += l * te[c * NFP + jj];
+        if (!bnd) {
+          R tr[4];
+          staged_trace<N, T, R>(M, code, f, jj, sm + L::SST + e * L::STG, tr);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) nb[c] += l * tr[c];
+        }
+      }
+      const R* tb = wgeo + (size_t)sk[e] * W8::GW + W8::GT + (f * W8::NQT + qt) * 3;
+      const R io = ldg(tb), inb = ldg(tb + 1), sc = ldg(tb + 2);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) own[c] *= io;
+      const R um[3] = {own[1], own[2], own[3]};
+      R pp, up[3];
+      if (bnd) {
+        pp = -own[0]; up[0] = um[0]; up[1] = um[1]; up[2] = um[2];
+      } else {
+        pp = nb[0] * inb; up[0] = nb[1] * inb; up[1] = nb[2] * inb; up[2] = nb[3] * inb;
+      }
+      const R* g = sg + e * X::GEO + X::GF + FS * f;
+      const R nrm[3] = {g[0], g[1], g[2]};   // planar triangle
+      R tp, tu, fp, fu;
+      penalties(g[4], g[5], pen, tp, tu);
+      upwind_flux(own[0], um, pp, up, nrm, tp, tu, skew, fp, fu);
+      sfc[(e * W8::CS) + (f * W8::NQT + qt) * 2 + 0] = fp * sc;
+      sfc[(e * W8::CS) + (f * W8::NQT + qt) * 2 + 1] = fu * sc;
+    }
   }
   __syncthreads();
 
@@ -584,14 +715,31 @@ __global__ void __launch_bounds__(NT) dense_kernel(hw_mesh_t M, hw_fields_t Q, E
     for (int f = 0; f < NF; ++f) {
       R tp = R(0), tu = R(0), tux[3] = {R(0), R(0), R(0)};
       const int j0 = X::off(f);
-      const bool pnrm = T == HW_PYRAMID && f == 0 && na;   // per-point normals
+      if (T == HW_WEDGE && naw && f < 2) {   // triangle: Vf^T at the cubature points
+        const R* vf = wcst + W8::CVF + f * W8::NQT * NP + n;
+        const R* fc = cs + e * W8::CS + 7 * W8::NQ + f * W8::NQT * 2;
+        for (int qt = 0; qt < W8::NQT; ++qt) {
+          const R l = ldg(vf + qt * NP);
+          tp += l * fc[2 * qt];
+          tu += l * fc[2 * qt + 1];
+        }
+        lift[0] += tp;
+        lift[1] += g[FS * f + 0] * tu;
+        lift[2] += g[FS * f + 1] * tu;
+        lift[3] += g[FS * f + 2] * tu;
+        continue;
+      }
+      // per-point normals: bilinear pyramid base, non-affine wedge quads
+      const bool pnrm = (T == HW_PYRAMID && f == 0 && na) || (T == HW_WEDGE && naw);
 #pragma unroll 4
       for (int jj = 0; jj < X::cnt(f); ++jj) {
         const int j = j0 + jj;
         const R l = ldg(LT + j * NP + n);
         tp += l * fl[2 * j];
         if (pnrm) {
-          const R* bp = (const R*)TY.op[9] + ((size_t)sk[e] * Dims<N>::NFQ + jj) * 4;
+          const R* bp = T == HW_WEDGE
+                            ? wgeo + (size_t)sk[e] * W8::GW + W8::GF + j * 5
+                            : (const R*)TY.op[9] + ((size_t)sk[e] * Dims<N>::NFQ + jj) * 4;
           const R lu = l * fl[2 * j + 1];
           tux[0] += lu * ldg(bp); tux[1] += lu * ldg(bp + 1); tux[2] += lu * ldg(bp + 2);
         } else {

@@ -24,18 +24,69 @@ _INTERIOR_ABC = {"tet": np.array([[-0.5, -0.5, -0.5]]), "wedge": np.array([[0.0,
                  "pyramid": np.array([[0.0, 0.0, 0.0]])}
 
 
-def _affine_check(t, verts, N):
-    """The nodal-face representation of the LSC-DG wedge needs affine wedges
-    (its traces carry 1/sqrt(J)); non-affine pyramids run through per-node
-    geometry (pyramid_node_geometry); tets are always affine."""
+def _affine_check(disc, t, verts):
+    """Non-affine wedges run the cubature form of the scalar kernel
+    (wedge_cubature_ops); their triangle faces are integrated at the
+    reference's face cubature, which the device reproduces exactly only when
+    the neighbour across the triangle is a wedge too (or the boundary): a
+    tet or pyramid there would need its own face cubature."""
     from .refelem import affine_mask
-    if t != "wedge" or len(verts) == 0:
-        return
-    bad = ~affine_mask(t, verts, tol=1e-10)
+    if t != "wedge" or len(verts) == 0 or affine_mask(t, verts, tol=1e-10).all():
+        return False
+    nb = disc.mesh.nbr["wedge"][:, :2, 0]
+    bad = (nb >= 0) & (nb != 1)
     if bad.any():
         raise NotImplementedError(
-            f"{int(bad.sum())} non-affine {t} elements; the device path currently requires "
-            "affine wedges and pyramids (DESIGN.md, scope)")
+            f"non-affine wedges with {int(bad.sum())} triangle faces shared with tets or "
+            "pyramids (DESIGN.md, scope)")
+    return True
+
+
+def wedge_cubature_ops(disc, dops):
+    """op[8] / op[9] of the non-affine wedge path (layout: Naw in
+    csrc/hw_kernels.cuh), from the reference-layout geometry
+    (hybridwave/dg.py:139-192): volume cubature G and gJfac premultiplied by
+    the weights, per-point quad-face n, Js/sqrt(J), 1/sqrt(J), and at the
+    triangle-face cubature points the own and the neighbour's 1/sqrt(J)
+    (through the reference gather index, dg.py:284-298) and w Js/sqrt(J)."""
+    from .operators import _tri_lagrange
+    ops = disc.ops["wedge"]
+    d = disc.data["wedge"]
+    K, Np = disc.n_elems["wedge"], ops.Np
+    w = ops.cub.weights
+    nq = len(w)
+    vol = np.concatenate([(w[None, :, None, None] * d.G).reshape(K, nq, 9),
+                          w[None, :, None] * d.gJfac], axis=2)
+    roffs = np.asarray(ops.face_offsets)
+    doffs = dops["face_offsets"]
+    tot = int(roffs[-1])
+    quad = np.zeros((K, int(doffs[-1]), 5))
+    for f in range(2, 5):
+        rs, ds = slice(roffs[f], roffs[f + 1]), slice(doffs[f], doffs[f + 1])
+        quad[:, ds, :3] = d.normals[:, rs]
+        quad[:, ds, 3] = d.wJs[:, rs] / ops.face_wts[f][None, :] * d.invsqrtJ_face[:, rs]
+        quad[:, ds, 4] = d.invsqrtJ_face[:, rs]
+    nqt = int(roffs[1] - roffs[0])
+    tri = np.zeros((K, 2, nqt, 3))
+    base = disc.trace_bases["wedge"]
+    gidx = np.asarray(disc.gather_idx)
+    bnd = np.asarray(disc.bnd_mask)
+    for f in range(2):
+        rs = slice(roffs[f], roffs[f + 1])
+        flat = base + np.arange(K)[:, None] * tot + np.arange(roffs[f], roffs[f + 1])[None, :]
+        g = gidx[flat] - base
+        ok = ~bnd[flat] & (g >= 0) & (g < K * tot)
+        gc = np.where(ok, g, 0)
+        tri[:, f, :, 0] = d.invsqrtJ_face[:, rs]
+        tri[:, f, :, 1] = np.where(ok, d.invsqrtJ_face[gc // tot, gc % tot], 0.0)
+        tri[:, f, :, 2] = d.wJs[:, rs] * d.invsqrtJ_face[:, rs]
+    geo = np.concatenate([vol.reshape(K, -1), quad.reshape(K, -1), tri.reshape(K, -1)], axis=1)
+    mats = [ops.V, ops.Dr3, ops.Ds3, ops.Dt3]
+    Lq = np.stack([_tri_lagrange(dops["tri2d"], ops.face_pts2d[f], disc.N) for f in range(2)])
+    Vf = np.stack([ops.Vf[roffs[f]:roffs[f + 1]] for f in range(2)])
+    const = np.concatenate([np.stack([m.T for m in mats]).ravel(), np.stack(mats).ravel(),
+                            Lq.ravel(), Vf.ravel()])
+    return {8: geo, 9: const}
 
 
 def face_impedance_avg(mesh, t):
@@ -186,7 +237,7 @@ def pack_mesh(disc):
     for t in disc.types:
         form = disc.forms[t]
         verts = mesh.element_vertices(t)
-        _affine_check(t, verts, disc.N)
+        naw = _affine_check(disc, t, verts)
         dops = dops_all[t]
         dops_any = dops
         perm_tri = face_symmetry_perms("tri", dops["tri2d"])
@@ -198,7 +249,8 @@ def pack_mesh(disc):
             "mat": material_records(np.asarray(mesh.materials[t], dtype=float)),
             "nbr_elem": elem, "nbr_code": code,
             "op": {**_pack_ops(t, dops), **(_tet_extra_ops(disc.ops[t], dops) if t == "tet" else {}),
-                   **(_pyramid_extra_ops(verts, disc.ops[t], dops) if t == "pyramid" else {})},
+                   **(_pyramid_extra_ops(verts, disc.ops[t], dops) if t == "pyramid" else {}),
+                   **(wedge_cubature_ops(disc, dops) if naw else {})},
             "iop": _pack_iops(t, dops, disc.N, mesh, perm_tri, face_offsets, dops_all,
                               perm_quad, disc.formulation.kind == "SEM"),
             "nfp": int(dops["face_offsets"][-1]),

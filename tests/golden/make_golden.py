@@ -259,13 +259,17 @@ def convergence_fixtures():
 
 
 def nonaffine_fixtures():
-    """compute_rhs on jittered (non-affine) pyramid and hex meshes, random
+    """compute_rhs on jittered (non-affine) pyramid and wedge meshes, random
     states; same perturbation as tests/test_gpu_parity.py::_perturbed."""
     from hybridwave.mesh import HybridMesh
     fd = {}
     for tag, spec, N, form, seed in [("pyr3_gl2", "pyramid:3", 2, "GL", 3),
                                      ("pyr3_sem3", "pyramid:3", 3, "SEM", 4),
-                                     ("pyr2_gl4", "pyramid:2", 4, "GL", 5)]:
+                                     ("pyr2_gl4", "pyramid:2", 4, "GL", 5),
+                                     ("wed2_gl1", "wedge:2", 1, "GL", 6),
+                                     ("wed3_gl2", "wedge:3", 2, "GL", 7),
+                                     ("wed3_sem3", "wedge:3", 3, "SEM", 8),
+                                     ("wed2_gl5", "wedge:2", 5, "GL", 9)]:
         m = build_mesh(spec)
         rng = np.random.default_rng(seed)
         X = m.vertices.copy()

@@ -222,3 +222,89 @@ def rhs(pack, disc, state):
         acc[:, 1:] *= mat[:, 1][:, None, None]
         out[t] = acc
     return out
+
+
+def naw_rhs(pack, disc, state):
+    """Model of the non-affine wedge path (Naw in csrc/hw_kernels.cuh) for
+    all-wedge meshes: cubature volume passes, per-point quad faces, triangle
+    faces at the reference's cubature through the nodal polynomial traces."""
+    N = disc.N
+    d = _dims(N)
+    P = pack["types"]["wedge"]
+    K = P["K"]
+    q = np.asarray(state["wedge"], dtype=float)
+    Np = q.shape[2]
+    nq, nqt, nfn = (N + 1) ** 3, 6 * (N + 1) ** 2, d["NFN"]
+    lay = face_layout("wedge", N)
+    nfp = lay[-1][1] + lay[-1][2]
+    GF, GT = nq * 12, nq * 12 + nfp * 5
+    g8, cst = P["op"][8], P["op"][9]
+    o = np.cumsum([0, 4 * Np * nq, 4 * Np * nq, 2 * nqt * nfn])
+    VT = cst[o[0]:o[1]].reshape(4, Np, nq)
+    VN = cst[o[1]:o[2]].reshape(4, nq, Np)
+    LQ = cst[o[2]:o[3]].reshape(2, nqt, nfn)
+    VF = cst[o[3]:].reshape(2, nqt, Np)
+    vol = g8[:, :GF].reshape(K, nq, 12)
+    fq = g8[:, GF:GT].reshape(K, nfp, 5)
+    tb = g8[:, GT:].reshape(K, 2, nqt, 3)
+    geo, mat = P["geo"], P["mat"]
+    acc = np.zeros((K, 4, Np))
+    U = np.einsum("mq,kfm->kfq", VT[0], q)
+    dc = np.einsum("cmq,km->kcq", VT[1:], q[:, 0])
+    wG = vol[..., :9].reshape(K, nq, 3, 3)
+    wgJ = vol[..., 9:]
+    gp = np.einsum("kqcx,kcq->kxq", wG, dc) + wgJ.transpose(0, 2, 1) * U[:, 0][:, None, :]
+    up = np.einsum("kqcx,kxq->kcq", wG, U[:, 1:])
+    uj = np.einsum("kqx,kxq->kq", wgJ, U[:, 1:])
+    acc[:, 1:] = -np.einsum("qn,kxq->kxn", VN[0], gp)
+    acc[:, 0] = np.einsum("cqn,kcq->kn", VN[1:], up) + uj @ VN[0]
+    # published traces: quad points x 1/sqrt(J), triangle points polynomial
+    tr = q @ P["op"][5]
+    isj = np.ones((K, nfp))
+    isj[:, 2 * nfn:] = fq[:, 2 * nfn:, 4]
+    tr = tr * isj[:, None, :]
+    LT = P["op"][6]
+    for f, (ft, off, cnt) in enumerate(lay):
+        own = tr[:, :, off:off + cnt]
+        code = P["nbr_code"][:, f]
+        k2 = P["nbr_elem"][:, f]
+        b = (code & BND) != 0
+        oth = np.zeros_like(own)
+        sel = ~b
+        if sel.any():
+            f2 = (code[sel] >> 2) & 7
+            pc = (code[sel] >> 5) & 15
+            perm = (pack["perm_tri"] if ft == "tri" else pack["perm_quad"])[pc]
+            off2 = np.array([lay[x][1] for x in f2])
+            cols = off2[:, None] + perm
+            oth[sel] = np.take_along_axis(tr[k2[sel]], np.repeat(cols[:, None, :], 4, axis=1),
+                                          axis=2)
+        if ft == "tri":
+            own = np.einsum("qj,kcj->kcq", LQ[f], own) * tb[:, f, None, :, 0]
+            oth = np.einsum("qj,kcj->kcq", LQ[f], oth) * tb[:, f, None, :, 1]
+            npts = nqt
+            nrm = np.repeat(geo[:, 10 + 6 * f:13 + 6 * f][:, None, :], npts, axis=1)
+            scale = tb[:, f, :, 2]
+        else:
+            npts = cnt
+            nrm = fq[:, off:off + cnt, :3]
+            scale = fq[:, off:off + cnt, 3]
+        oth[b, 0] = -own[b, 0]
+        oth[b, 1:] = own[b, 1:]
+        avg, inv = geo[:, 10 + 6 * f + 4], geo[:, 10 + 6 * f + 5]
+        tp = disc.penalty_scale * inv
+        tu = disc.penalty_scale * avg
+        unm = np.einsum("kpx,kxp->kp", nrm, own[:, 1:])
+        unp = np.einsum("kpx,kxp->kp", nrm, oth[:, 1:])
+        dp_ = oth[:, 0] - own[:, 0]
+        dun = unp - unm
+        skew = P["form"] == "skew"
+        fp = (0.5 * tp[:, None] * dp_ - 0.5 * (unp + unm)) if skew else \
+            0.5 * (tp[:, None] * dp_ - dun)
+        fu = 0.5 * (tu[:, None] * dun - dp_)
+        L = VF[f] if ft == "tri" else LT[off:off + cnt]
+        acc[:, 0] += (fp * scale) @ L
+        acc[:, 1:] += np.einsum("kpx,kp,pn->kxn", nrm, fu * scale, L)
+    acc[:, 0] *= mat[:, 0][:, None]
+    acc[:, 1:] *= mat[:, 1][:, None, None]
+    return {"wedge": acc}

@@ -414,3 +414,50 @@ def test_partitioned_lsrk_loopback(form, nparts, method, native_lib):
             g = p.part.global_ids[t][:p.part.n_owned[t]]
             r_ = ref[t][g]
             assert np.abs(own[t].cpu().numpy() - r_).max() <= 1e-12 * np.abs(r_).max()
+
+
+NAW_CASES = [("wed2_gl1", "wedge:2", 1, "GL", 6), ("wed3_gl2", "wedge:3", 2, "GL", 7),
+             ("wed3_sem3", "wedge:3", 3, "SEM", 8), ("wed2_gl5", "wedge:2", 5, "GL", 9)]
+
+
+@pytest.mark.parametrize("tag,spec,N,form,seed", NAW_CASES)
+def test_nonaffine_wedges_match_reference(tag, spec, N, form, seed, native_lib):
+    """Jittered (non-affine) LSC-DG wedges: the cubature path of the scalar
+    kernel (volume G / grad J at the cubature points, triangle faces at the
+    reference's face cubature) against the reference's own RHS."""
+    from paper_1507_02557_b200.dg import Discretization
+    G = load_golden("nonaffine")
+    d = Discretization(_perturbed(spec, 0.04, seed), N, form)
+    rng = np.random.default_rng(seed + 10)
+    st = {t: rng.standard_normal((d.n_elems[t], 4, d.ops[t].Np)) for t in d.types}
+    r = d.compute_rhs(st)
+    assert rel_err(r, {"wedge": G[f"{tag}/rhs/wedge"]}) < 1e-11
+    assert rel_err(r, oracle.compute_rhs(d, st)) < 1e-11
+
+
+def test_nonaffine_wedges_fp32(native_lib):
+    from paper_1507_02557_b200.dg import Discretization
+    G = load_golden("nonaffine")
+    d = Discretization(_perturbed("wedge:3", 0.04, 8), 3, "SEM", dtype=torch.float32)
+    rng = np.random.default_rng(18)
+    st = {t: rng.standard_normal((d.n_elems[t], 4, d.ops[t].Np)) for t in d.types}
+    assert _l2rel(d.compute_rhs(st), {"wedge": G["wed3_sem3/rhs/wedge"]}) < 1e-4
+
+
+@pytest.mark.parametrize("spec,N,form,steps", [("wedge:3", 2, "GL", 20), ("wedge:3", 3, "SEM", 20),
+                                               ("hybrid:2", 2, "GL", 10),
+                                               ("hybrid:2", 3, "SEM", 10)])
+def test_nonaffine_wedge_lsrk(spec, N, form, steps, native_lib):
+    """LSRK-45 on jittered meshes (hybrid: non-affine wedges next to
+    non-affine pyramids and trilinear hexes on their quad faces) against the
+    oracle: the per-point published wedge traces of the cubature path."""
+    from paper_1507_02557_b200.app import cavity_fields
+    from paper_1507_02557_b200.dg import Discretization
+    from paper_1507_02557_b200.stability import local_timesteps
+    from paper_1507_02557_b200.timeint import lsrk_run
+    d = Discretization(_perturbed(spec, 0.04, 11), N, form)
+    st = d.project(cavity_fields, 0.0)
+    dt = 0.5 * min(float(v.min()) for v in local_timesteps(d, 0.5).values())
+    s = lsrk_run(d, st, dt, steps * dt)
+    ref = oracle.lsrk_run(lambda q, tau: oracle.compute_rhs(d, q), st, dt, steps * dt)
+    assert _l2rel(s, ref) < 1e-10

@@ -51,3 +51,52 @@ def test_hex_face_point_map_is_affine(N, form):
     n = np.arange(n1 ** 3)
     I = np.stack([n // (n1 * n1), (n // n1) % n1, n % n1, np.ones_like(n)], axis=1)
     assert np.array_equal(I @ c.T.astype(np.int64), tab.T)
+
+
+def _perturbed(spec, amp, seed):
+    from conftest import build_mesh
+    from paper_1507_02557_b200.mesh import HybridMesh
+    m = build_mesh(spec)
+    rng = np.random.default_rng(seed)
+    X = m.vertices.copy()
+    inner = np.all((X > 1e-9) & (X < 1 - 1e-9), axis=1)
+    X[inner] += amp * rng.uniform(-1, 1, (inner.sum(), 3))
+    return HybridMesh(X, m.blocks)
+
+
+NAW_CASES = [("wed2_gl1", "wedge:2", 1, "GL", 6), ("wed3_gl2", "wedge:3", 2, "GL", 7),
+             ("wed3_sem3", "wedge:3", 3, "SEM", 8)]
+
+
+@pytest.mark.parametrize("tag,spec,N,form,seed", NAW_CASES)
+def test_nonaffine_wedge_layout_matches_reference(tag, spec, N, form, seed):
+    """Non-affine wedges: the packed cubature data (op[8], op[9]) through the
+    model of the kernel's cubature path reproduce the reference's RHS."""
+    from layout_model import naw_rhs
+    from paper_1507_02557_b200.dg import Discretization
+    G = load_golden("nonaffine")
+    d = Discretization(_perturbed(spec, 0.04, seed), N, form)
+    rng = np.random.default_rng(seed + 10)
+    st = {t: rng.standard_normal((d.n_elems[t], 4, d.ops[t].Np)) for t in d.types}
+    pack = pack_mesh(d)
+    assert set(pack["types"]["wedge"]["op"]) >= {8, 9}
+    assert rel_err(naw_rhs(pack, d, st), {"wedge": G[f"{tag}/rhs/wedge"]}) < 1e-12
+    assert rel_err(oracle.compute_rhs(d, st), {"wedge": G[f"{tag}/rhs/wedge"]}) < 1e-12
+
+
+def test_nonaffine_wedge_next_to_tets_is_refused():
+    """A non-affine wedge whose triangle face touches a tet (or pyramid) has
+    no exact nodal-face representation on the tet side: refused, not wrong.
+    (The generator meshes put only wedges on wedge triangle faces.)"""
+    from paper_1507_02557_b200.dg import Discretization
+    from paper_1507_02557_b200.mesh import HybridMesh
+    def mesh(x4):
+        X = np.array([(0, 0, 0), (0, 1, 1), (0, 1, 0), (1, 0, 0), (x4, 1, 1), (1, 1, 0),
+                      (2.0, 0.7, 0.3)])
+        return HybridMesh(X, {"wedge": np.array([[0, 1, 2, 3, 4, 5]]),
+                              "tet": np.array([[3, 5, 4, 6]])})
+    m = mesh(1.2)
+    assert 3 in m.nbr["wedge"][0, :2, 0]
+    with pytest.raises(NotImplementedError):
+        pack_mesh(Discretization(m, 2, "GL"))
+    pack_mesh(Discretization(mesh(1.0), 2, "GL"))   # affine: packs
