@@ -51,6 +51,9 @@ def parse():
     ap.add_argument("--cpu-mesh", default=None, help="reference-arm sample mesh")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--jitter", type=float, default=0.0,
+                    help="perturb interior vertices by this fraction of the mesh spacing "
+                         "(non-affine hexes, pyramids and wedges: the per-point geometry paths)")
     ap.add_argument("--scheme", default="lsrk", choices=["lsrk", "mrab"],
                     help="mrab: multi-rate AB3 (active levels only), --levels levels")
     ap.add_argument("--levels", type=int, default=3)
@@ -62,6 +65,15 @@ def parse():
 def build_mesh(spec):
     from paper_1507_02557_b200.app import build_mesh as bm
     return bm(spec)
+
+
+def jittered(mesh, amp, seed=0):
+    from paper_1507_02557_b200.mesh import HybridMesh
+    rng = np.random.default_rng(seed)
+    X = mesh.vertices.copy()
+    inner = np.all((X > 1e-9) & (X < 1 - 1e-9), axis=1)
+    X[inner] += amp * rng.uniform(-1, 1, (inner.sum(), 3))
+    return HybridMesh(X, mesh.blocks)
 
 
 def n_dof(disc):
@@ -232,6 +244,8 @@ def main():
         return partitioned(args, world, rank, local, dev, dtype, s_bytes)
     t_setup = time.perf_counter()
     mesh = build_mesh(args.mesh)
+    if args.jitter > 0:
+        mesh = jittered(mesh, args.jitter / int(args.mesh.split(":")[1]))
     disc = Discretization(mesh, args.order, args.form, dtype=dtype, device=dev)
     host_state = disc.project(cavity_fields, 0.0)
     dt = min(float(v.min()) for v in local_timesteps(disc, 0.5).values())
@@ -368,7 +382,8 @@ def main():
                 "dtype": args.dtype,
                 "data": "synthetic (cavity eigenmode projected on the mesh), per-rank replica",
                 "config": {"workload": f"{args.mesh} N={args.order} {args.form} LSRK-45 "
-                                       f"(configs[2])",
+                                       f"(configs[2])" + (f", jitter {args.jitter}" if args.jitter
+                                                          else ""),
                            "elements": {t: disc.n_elems[t] for t in disc.types},
                            "n_dof_per_rank": disc.n_dof, "dt": dt,
                            "l2_policy": "inputs larger than L2 (state+res+q_out "
