@@ -67,6 +67,14 @@ def build_mesh(spec):
     return bm(spec)
 
 
+def config_index(spec):
+    """BASELINE.json config a mesh spec stands for (hex:4 -> configs[0],
+    tet:* -> [1], hybrid:* -> [2], hexdom:* -> [3], graded:* -> [4])."""
+    kind = spec.split(":")[0]
+    idx = {"hex": 0, "tet": 1, "hybrid": 2, "hexdom": 3, "graded": 4}.get(kind)
+    return f"configs[{idx}]" if idx is not None else "custom mesh"
+
+
 def jittered(mesh, amp, seed=0):
     from paper_1507_02557_b200.mesh import HybridMesh
     rng = np.random.default_rng(seed)
@@ -382,8 +390,8 @@ def main():
                 "dtype": args.dtype,
                 "data": "synthetic (cavity eigenmode projected on the mesh), per-rank replica",
                 "config": {"workload": f"{args.mesh} N={args.order} {args.form} LSRK-45 "
-                                       f"(configs[2])" + (f", jitter {args.jitter}" if args.jitter
-                                                          else ""),
+                                       f"({config_index(args.mesh)})" +
+                                       (f", jitter {args.jitter}" if args.jitter else ""),
                            "elements": {t: disc.n_elems[t] for t in disc.types},
                            "n_dof_per_rank": disc.n_dof, "dt": dt,
                            "l2_policy": "inputs larger than L2 (state+res+q_out "
