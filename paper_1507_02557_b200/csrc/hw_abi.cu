@@ -366,11 +366,32 @@ static int run_rhs(const hw_mesh_t* M, const hw_fields_t* Q, const Epi& E,
 // out = q + dt (c0 h0 + c1 h1 + c2 h2) on the listed element rows (MRAB
 // dense output); dt == 0 is a plain row copy (no history reads).  Element
 // rows (4 Np scalars) are even-length: two scalars per thread.
+// all element types in one launch (blockIdx.y = type): the multi-rate
+// dense-output pass runs it on small per-level subsets, where per-type
+// launches were latency-bound
+struct Axpy3Types {
+  const void* q[HW_NTYPES];
+  void* out[HW_NTYPES];
+  const void* h0[HW_NTYPES];
+  const void* h1[HW_NTYPES];
+  const void* h2[HW_NTYPES];
+  const int32_t* list[HW_NTYPES];
+  int64_t n[HW_NTYPES];
+  int chunk[HW_NTYPES];
+};
+
 template <typename R>
-__global__ void axpy3_kernel(const R* __restrict__ q, R* __restrict__ out, const R* __restrict__ h0,
-                             const R* __restrict__ h1, const R* __restrict__ h2, int nh, R c0,
-                             R c1, R c2, R dt, const int32_t* __restrict__ list, int64_t n,
-                             int chunk) {
+__global__ void axpy3_kernel(Axpy3Types a, int nh, R c0, R c1, R c2, R dt) {
+  const int t = blockIdx.y;
+  const int64_t n = a.n[t];
+  if (n <= 0) return;
+  const R* __restrict__ q = (const R*)a.q[t];
+  R* __restrict__ out = (R*)a.out[t];
+  const R* __restrict__ h0 = (const R*)a.h0[t];
+  const R* __restrict__ h1 = (const R*)a.h1[t];
+  const R* __restrict__ h2 = (const R*)a.h2[t];
+  const int32_t* __restrict__ list = a.list[t];
+  const int chunk = a.chunk[t];
   const int half = chunk >> 1;
   const int64_t total = n * half;
   const bool copy = dt == R(0);
@@ -561,29 +582,31 @@ int hw_axpy3(const hw_mesh_t* mesh, const hw_fields_t* q, hw_fields_t* out,
              double c0, double c1, double c2, double dt, const hw_subset_t* subset,
              void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
+  Axpy3Types a{};
+  unsigned g = 0;
   for (int t = 0; t < HW_NTYPES; ++t) {
     const int64_t K = mesh->t[t].K;
+    a.n[t] = 0;
     if (K <= 0) continue;
-    const int32_t* list;
-    int64_t n;
-    subset_of(subset, t, K, &list, &n);
-    if (n <= 0) continue;
-    const int chunk = 4 * np_of(t, mesh->N);
-    const unsigned g = grid_for(n * chunk / 2);
-    if (mesh->dtype == HW_F64)
-      axpy3_kernel<double><<<g, 256, 0, st>>>(
-          (const double*)q->p[t], (double*)out->p[t], (const double*)h0->p[t],
-          h1 ? (const double*)h1->p[t] : nullptr, h2 ? (const double*)h2->p[t] : nullptr,
-          n_hist, c0, c1, c2, dt, list, n, chunk);
-    else
-      axpy3_kernel<float><<<g, 256, 0, st>>>(
-          (const float*)q->p[t], (float*)out->p[t], (const float*)h0->p[t],
-          h1 ? (const float*)h1->p[t] : nullptr, h2 ? (const float*)h2->p[t] : nullptr, n_hist,
-          (float)c0, (float)c1, (float)c2, (float)dt, list, n, chunk);
-    int rc = check_launch("axpy3_kernel");
-    if (rc) return rc;
+    subset_of(subset, t, K, &a.list[t], &a.n[t]);
+    if (a.n[t] <= 0) continue;
+    a.chunk[t] = 4 * np_of(t, mesh->N);
+    a.q[t] = q->p[t];
+    a.out[t] = out->p[t];
+    a.h0[t] = h0->p[t];
+    a.h1[t] = h1 ? h1->p[t] : nullptr;
+    a.h2[t] = h2 ? h2->p[t] : nullptr;
+    const unsigned gt = grid_for(a.n[t] * a.chunk[t] / 2);
+    g = gt > g ? gt : g;
   }
-  return 0;
+  if (g == 0) return 0;
+  const dim3 grid(g, HW_NTYPES);
+  if (mesh->dtype == HW_F64)
+    axpy3_kernel<double><<<grid, 256, 0, st>>>(a, n_hist, c0, c1, c2, dt);
+  else
+    axpy3_kernel<float><<<grid, 256, 0, st>>>(a, n_hist, (float)c0, (float)c1, (float)c2,
+                                              (float)dt);
+  return check_launch("axpy3_kernel");
 }
 
 int hw_hist_push(const hw_mesh_t* mesh, hw_fields_t* h0, hw_fields_t* h1, hw_fields_t* h2,

@@ -268,7 +268,8 @@ class PartMRAB:
         for tick in range(2 ** (L - 1)):
             stepping = [lev for lev in range(1, L + 1) if tick % (2 ** (L - lev)) == 0]
             n += npack + len(pub) + sum(step_types[lev] for lev in stepping)
-            n += sum(eff_types[(tick, lev)] for lev in range(1, L + 1))
+            # dense output: one multi-type launch per level with a subset
+            n += sum(1 for lev in range(1, L + 1) if eff_types[(tick, lev)])
         self.launches_per_macro = n
 
     def _pack(self):
