@@ -68,7 +68,9 @@ struct Naw {
                        NFN = D::NFN, NFP = D::NFP_WEDGE;
   static constexpr int GF = NQ * 12, GT = GF + NFP * 5, GW = GT + 2 * NQT * 3;
   static constexpr int CVN = 4 * NP * NQ, CLQ = 8 * NP * NQ, CVF = CLQ + 2 * NQT * NFN;
-  static constexpr int CS = 7 * NQ + 4 * NQT;   // smem scratch per element
+  // smem scratch per element: the trial-pass values, then (after the test
+  // pass) the triangle-face fluxes
+  static constexpr int CS = (7 * NQ > 4 * NQT) ? 7 * NQ : 4 * NQT;
 };
 
 template <int N>
@@ -659,7 +661,7 @@ __global__ void __launch_bounds__(NT) dense_kernel(hw_mesh_t M, hw_fields_t Q, E
   if (T == HW_WEDGE && naw) {
     // triangle faces at the reference's face cubature points
     const R* LQ = wcst + W8::CLQ;
-    R* sfc = cs + 7 * W8::NQ;
+    R* sfc = cs;   // trial-pass values are dead after the test pass
     for (int i = tid; i < ne * 2 * W8::NQT; i += NT) {
       const int e = i / (2 * W8::NQT), r = i - e * 2 * W8::NQT;
       const int f = r / W8::NQT, qt = r - f * W8::NQT;
@@ -717,7 +719,7 @@ __global__ void __launch_bounds__(NT) dense_kernel(hw_mesh_t M, hw_fields_t Q, E
       const int j0 = X::off(f);
       if (T == HW_WEDGE && naw && f < 2) {   // triangle: Vf^T at the cubature points
         const R* vf = wcst + W8::CVF + f * W8::NQT * NP + n;
-        const R* fc = cs + e * W8::CS + 7 * W8::NQ + f * W8::NQT * 2;
+        const R* fc = cs + e * W8::CS + f * W8::NQT * 2;
         for (int qt = 0; qt < W8::NQT; ++qt) {
           const R l = ldg(vf + qt * NP);
           tp += l * fc[2 * qt];
