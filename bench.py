@@ -343,12 +343,15 @@ def main():
         prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
     except Exception:
         pass
-    tr_ent = prof.get(f"{args.mesh}/N{args.order}/{args.form}/{args.dtype}/{dom}")
+    # (jittered meshes run other kernels than the captured ones: no traffic)
+    tr_ent = None if args.jitter else prof.get(f"{args.mesh}/N{args.order}/{args.form}/{args.dtype}/{dom}")
     traffic = tr_ent["bytes"] if isinstance(tr_ent, dict) else tr_ent
     kname = {"hex": f"hex_kernel<{args.order},{'double' if s_bytes == 8 else 'float'}>",
              "wedge": f"dense_mma_kernel<{args.order},1>", "pyramid": f"dense_mma_kernel<{args.order},2>",
              "tet": f"tet_mma_kernel<{args.order}>"}[dom] if s_bytes == 8 else \
         f"{dom}_kernel<{args.order},float>"
+    if args.jitter and dom in ("wedge", "pyramid"):   # non-affine: the scalar per-point kernel
+        kname = f"dense_kernel<{args.order},{1 if dom == 'wedge' else 2}>"
     roof = {"bound": "hbm", "kernel": kname,
             "achieved": per_type[dom]["GBps"], "peak": hbm, "unit": "GB/s",
             "frac": per_type[dom]["GBps"] / hbm, "traffic": traffic,
