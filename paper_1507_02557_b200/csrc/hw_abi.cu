@@ -156,7 +156,7 @@ static int launch_dense_mma(const hw_mesh_t& M, const hw_fields_t& Q, const Epi&
   int rc;
   const size_t bytes = L::BYTES > smem_floor() ? L::BYTES : smem_floor();
   const unsigned grid = (unsigned)((n + L::E - 1) / L::E);
-  if (L::SPLIT) {
+  if constexpr (L::SPLIT) {   // only the launched layout is instantiated
     if ((rc = set_smem(dense_mma_kernel<N, T, R>, bytes))) return rc;
     dense_mma_kernel<N, T, R><<<grid, L::NTH, bytes, st>>>(M, Q, E, list, n);
   } else {
