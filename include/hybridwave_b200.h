@@ -149,6 +149,11 @@ int hw_energy(const hw_mesh_t* mesh, const hw_fields_t* q, double* out,
 
 const char* hw_last_error(void);
 int hw_version(void);
+/* kernel launches this library has issued so far (all devices, all
+ * threads; captured launches count once, at capture, not per graph replay).
+ * Instrumentation for the benchmark's gpu_launches; no reference
+ * counterpart. */
+long long hw_launch_count(void);
 /* the N values compiled into this library (bit N set) */
 int hw_supported_orders(void);
 

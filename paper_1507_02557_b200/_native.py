@@ -79,13 +79,15 @@ def lib():
                      "hw_hist_push", "hw_halo_pack", "hw_energy", "hw_version",
                      "hw_supported_orders"):
             getattr(L, name).restype = c_int
+        L.hw_launch_count.restype = ctypes.c_longlong
+        L.hw_launch_count.argtypes = []
         _lib = L
     return _lib
 
 
 EXPORTED_SYMBOLS = ("hw_rhs", "hw_traces", "hw_lsrk_stage", "hw_ab_step", "hw_axpy3", "hw_hist_push",
                     "hw_halo_pack", "hw_energy", "hw_last_error", "hw_version",
-                    "hw_supported_orders")
+                    "hw_supported_orders", "hw_launch_count")
 
 
 def check(rc):

@@ -5,6 +5,7 @@
 #include <mutex>
 #include <set>
 #include <utility>
+#include <atomic>
 #include <string>
 
 #include "hw_kernels.cuh"
@@ -19,7 +20,13 @@ static int fail(const char* msg) {
   return 1;
 }
 
+// kernel launches issued through this library (every launch site calls
+// check_launch once; a CUDA-graph replay issues its captured launches
+// without passing here)
+static std::atomic<long long> g_launches{0};
+
 static int check_launch(const char* what) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     g_err = std::string(what) + ": " + cudaGetErrorString(e);
@@ -504,6 +511,8 @@ static int dispatch_energy(const hw_mesh_t& M, const hw_fields_t& Q, double* out
 extern "C" {
 
 int hw_version(void) { return 1; }
+
+long long hw_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
 int hw_supported_orders(void) {
   int m = 0;

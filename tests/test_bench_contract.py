@@ -50,7 +50,8 @@ def test_product_arm_line():
     assert BASE_KEYS <= set(line)
     assert line["n_gpus"] == 1 and line["warmup"] >= 3 and line["steps"] == 3
     assert line["value"] > 0 and line["dtype"] == "f64"
-    assert line["gpu_launches"] > 0
+    # LSRK-45: one fused kernel per element type per stage (hw_launch_count)
+    assert line["gpu_launches"] == 3 * 5 * 4
     assert "workload" in line["config"] and "l2_policy" in line["config"]
     r = line["roofline"]
     assert r["bound"] in ("hbm", "tensor") and r["unit"] == "GB/s"
@@ -60,3 +61,12 @@ def test_product_arm_line():
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     c = line["clocks"]
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(c)
+
+
+@pytest.mark.gpu
+def test_mrab_line():
+    (line,) = run_bench(["--scheme", "mrab", "--mesh", "graded:6", "--order", "2",
+                         "--steps", "3", "--warmup", "3"])
+    assert BASE_KEYS <= set(line)
+    assert line["value"] > 0 and line["gpu_launches"] > 0
+    assert line["e2e"]["value"] > 0 and line["e2e"]["h2d_bytes_per_step"] > 0
