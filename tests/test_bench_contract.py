@@ -70,3 +70,14 @@ def test_mrab_line():
     assert BASE_KEYS <= set(line)
     assert line["value"] > 0 and line["gpu_launches"] > 0
     assert line["e2e"]["value"] > 0 and line["e2e"]["h2d_bytes_per_step"] > 0
+
+
+@pytest.mark.gpu
+def test_partitioned_line_one_rank():
+    """The element-partitioned (NCCL) stepper at world size 1: same contract;
+    with no peers every stage is the interior launch of each type."""
+    (line,) = run_bench(["--partitioned", "--mesh", "hybrid:8", "--order", "2", "--steps", "3",
+                         "--warmup", "3"])
+    assert BASE_KEYS <= set(line)
+    assert line["value"] > 0 and line["gpu_launches"] == 3 * 5 * 4
+    assert line["e2e"]["value"] > 0
