@@ -14,7 +14,10 @@ on subsets), so partitioned runs reproduce single-GPU results to rounding
 (tests/test_gpu_parity.py::test_partitioned_lsrk_loopback).
 """
 
+import functools
+
 import numpy as np
+
 import torch
 
 from . import _native as nat
@@ -171,6 +174,22 @@ class PartStepper:
         return {t: self.S.q[t][:self.part.n_owned[t]] for t in self.disc.types}
 
 
+@functools.lru_cache(maxsize=None)
+def _ab_coeffs(nh):
+    """AB coefficients of a full step, padded to 3 (hybridwave/timeint.py:21-38)."""
+    from .timeint import ab_coefficients
+    return tuple(float(x) for x in ab_coefficients(nh)) + (0.0,) * (3 - nh)
+
+
+@functools.lru_cache(maxsize=None)
+def _dense_coeffs(nh, frac, period):
+    """Dense-output coefficients c(theta) - c(1), theta = frac / period
+    (hybridwave/timeint.py:144-173), padded to 3."""
+    from .timeint import ab_coefficients
+    c = ab_coefficients(nh, frac / period) - ab_coefficients(nh, 1.0)
+    return tuple(float(x) for x in c) + (0.0,) * (3 - nh)
+
+
 class PartMRAB:
     """Multi-rate AB3 (timeint.MRABDriver's tick pattern) on one rank's local
     part.  Each tick: dense-output (effective) state of the owned elements
@@ -193,6 +212,7 @@ class PartMRAB:
         self.q = d.to_device(state_local)
         self.eff = d.empty_state()
         self.ring = [d.zeros_state() for _ in range(3)]
+        self._fcache = {}
         self.n_hist = np.zeros(L + 1, dtype=int)
         self.steps = np.zeros(L + 1, dtype=int)
         self.send_idx = {peer: {t: torch.as_tensor(idx, dtype=torch.int32, device=dev)
@@ -280,13 +300,20 @@ class PartMRAB:
                                           idx.data_ptr(), idx.numel(),
                                           self.sendbuf[peer][t].data_ptr(), st))
 
+    def _fields(self, s_):
+        """HWFields of a persistent state dict (q, eff, ring slots), built
+        once: the per-tick launches are bound by host overhead."""
+        f = self._fcache.get(id(s_))
+        if f is None:
+            f = self._fcache[id(s_)] = (s_, nat.fields(self.disc.slots(s_)))
+        return f[1]
+
     def tick_effective(self, tick, dt_min):
         """Dense output of this tick's owned read / sent elements, packed for
         the peers."""
-        from .timeint import ab_coefficients
         d, L = self.disc, self.L
         lib, dm, st = nat.lib(), d.device_mesh, d.stream_ptr()
-        F = lambda s_: nat.fields(d.slots(s_))
+        F = self._fields
         for lev in range(1, L + 1):
             sub = self.eff_sub[(tick, lev)]
             if sub is None:
@@ -298,8 +325,7 @@ class PartMRAB:
                 nat.check(lib.hw_axpy3(dm.struct, F(self.q), F(self.eff), F(self.ring[0]), None,
                                        None, 1, 0.0, 0.0, 0.0, 0.0, sub, st))
                 continue
-            c = ab_coefficients(nh, frac / period) - ab_coefficients(nh, 1.0)
-            c = list(c) + [0.0] * (3 - nh)
+            c = _dense_coeffs(nh, frac, period)
             s0 = self.steps[lev] % 3
             h = [self.ring[s0], self.ring[(s0 - 1) % 3], self.ring[(s0 - 2) % 3]]
             nat.check(lib.hw_axpy3(dm.struct, F(self.q), F(self.eff), F(h[0]), F(h[1]), F(h[2]),
@@ -314,10 +340,9 @@ class PartMRAB:
     def tick_step(self, tick, dt_min, handle):
         """Wait for the ghosts' effective state, traces of the read set, and
         the fused RHS + AB3 update of the owned stepping elements."""
-        from .timeint import ab_coefficients
         d, L = self.disc, self.L
         lib, dm, st = nat.lib(), d.device_mesh, d.stream_ptr()
-        F = lambda s_: nat.fields(d.slots(s_))
+        F = self._fields
         self.transport.wait(handle)
         dm.compute_traces(F(self.eff), 0, st, subset=self.trace_sub[tick])
         dm.set_traces(0, None)
@@ -330,7 +355,7 @@ class PartMRAB:
             s0 = self.steps[lev] % 3
             h0, h1, h2 = self.ring[s0], self.ring[(s0 - 1) % 3], self.ring[(s0 - 2) % 3]
             nh = self.n_hist[lev]
-            c = list(ab_coefficients(nh)) + [0.0] * (3 - nh)
+            c = _ab_coeffs(nh)
             nat.check(lib.hw_ab_step(dm.struct, F(self.eff), F(self.q), F(h0), F(h1), F(h2), nh,
                                      c[0], c[1], c[2], dt_min * 2 ** (L - lev), sub, st))
 
