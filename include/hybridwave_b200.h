@@ -70,7 +70,8 @@ typedef struct {
   int32_t N;
   int32_t dtype;             /* HW_F64 / HW_F32                           */
   int32_t formulation;       /* HW_GL / HW_SEM                            */
-  int32_t pad_;
+  int32_t device;            /* CUDA ordinal the buffers live on: made     *
+                              * current for each call (-1: leave as is)   */
   double penalty_scale;      /* hybridwave/dg.py:341-342                  */
   const int32_t* perm_tri;   /* (6, (N+1)(N+2)/2) face-point permutations */
   const int32_t* perm_quad;  /* (8, (N+1)^2)                              */

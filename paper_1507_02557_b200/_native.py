@@ -28,7 +28,7 @@ class HWType(ctypes.Structure):
 
 class HWMesh(ctypes.Structure):
     _fields_ = [("N", c_int32), ("dtype", c_int32), ("formulation", c_int32),
-                ("pad_", c_int32), ("penalty_scale", c_double),
+                ("device", c_int32), ("penalty_scale", c_double),
                 ("perm_tri", c_void_p), ("perm_quad", c_void_p),
                 ("tr_in", c_void_p * 4), ("tr_out", c_void_p * 4),
                 ("t", HWType * 4)]

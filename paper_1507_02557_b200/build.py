@@ -1,5 +1,6 @@
 """Build the in-tree sm_100a shared library (nvcc, no torch JIT cache)."""
 
+import hashlib
 import os
 import subprocess
 import sys
@@ -28,15 +29,37 @@ def nvcc():
     raise RuntimeError("nvcc not found")
 
 
-def build_native(max_order=7, force=False, verbose=False):
+def _stamp(cmd_flags, deps):
+    """Content hash of everything that determines the library: the nvcc
+    flags (incl. HW_NVCC_DEFS and HW_MAX_ORDER) and every source byte."""
+    h = hashlib.sha256()
+    h.update("\0".join(cmd_flags).encode())
+    for p in deps:
+        h.update(os.path.basename(p).encode() + b"\0")
+        with open(p, "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()
+
+
+STAMP = OUT + ".stamp"
+
+
+def build_native(max_order=7, force=False, verbose=False, out=None):
+    """Compile csrc/hw_abi.cu into the in-tree library unless the stamp next
+    to it records the same sources and flags.  HW_NVCC_DEFS adds -D flags
+    (tuning experiments); ``out`` builds a variant to another path so the
+    default library is never silently replaced by a tuning build."""
     deps = _sources() + [HEADER]
-    if (not force and os.path.exists(OUT)
-            and os.path.getmtime(OUT) >= max(os.path.getmtime(p) for p in deps)):
-        return OUT
-    # HW_NVCC_DEFS: extra -D flags for tuning experiments (e.g. -DHW_TET_MINB=8)
     extra = os.environ.get("HW_NVCC_DEFS", "").split()
-    cmd = [nvcc()] + NVCC_FLAGS + extra + [f"-DHW_MAX_ORDER={max_order}", "-o", OUT + ".tmp",
-                                           MAIN]
+    flags = NVCC_FLAGS + extra + [f"-DHW_MAX_ORDER={max_order}"]
+    target = out or OUT
+    stamp_path = target + ".stamp"
+    want = _stamp(flags, deps)
+    if not force and os.path.exists(target) and os.path.exists(stamp_path):
+        with open(stamp_path) as fh:
+            if fh.read().strip() == want:
+                return target
+    cmd = [nvcc()] + flags + ["-o", target + ".tmp", MAIN]
     proc = subprocess.run(cmd, capture_output=True, text=True)
     log = os.path.join(_HERE, "csrc", "build.log")
     with open(log, "w") as fh:
@@ -44,10 +67,12 @@ def build_native(max_order=7, force=False, verbose=False):
     if proc.returncode != 0:
         sys.stderr.write(proc.stderr[-4000:])
         raise RuntimeError(f"nvcc failed (see {log})")
-    os.replace(OUT + ".tmp", OUT)
+    os.replace(target + ".tmp", target)
+    with open(stamp_path, "w") as fh:
+        fh.write(want + "\n")
     if verbose:
-        print(f"built {OUT}")
-    return OUT
+        print(f"built {target}")
+    return target
 
 
 if __name__ == "__main__":

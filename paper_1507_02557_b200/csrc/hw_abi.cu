@@ -69,6 +69,29 @@ static bool tet_scalar() {
   return v == 1;
 }
 
+// Makes the mesh's device current for the duration of an ABI call and
+// restores the caller's afterwards: the stream handle the caller passes may
+// be a device's legacy default stream (0), and set_smem / side_streams key on
+// the current device, so launching from another current device would run
+// the kernels on the wrong GPU against the mesh's pointers.
+struct DeviceGuard {
+  int prev = -1;
+  bool ok = true;
+  explicit DeviceGuard(const hw_mesh_t* M) {
+    if (!M || M->device < 0) return;
+    if (cudaGetDevice(&prev) != cudaSuccess) { ok = false; return; }
+    if (prev != M->device && cudaSetDevice(M->device) != cudaSuccess) ok = false;
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+#define HW_DEVICE_GUARD(M)                                        \
+  DeviceGuard device_guard_(M);                                   \
+  if (!device_guard_.ok) return fail("cannot make the mesh's device current")
+
 static void subset_of(const hw_subset_t* sub, int t, int64_t K, const int32_t** list,
                       int64_t* n) {
   *list = nullptr;
@@ -236,8 +259,21 @@ static int launch_rhs_all(const hw_mesh_t& M, const hw_fields_t& Q, const Epi& E
   static int order[HW_NTYPES] = {HW_PYRAMID, HW_HEX, HW_WEDGE, HW_TET};
   static const bool order_env = [] {   // HW_TYPE_ORDER=3102 (tuning experiments)
     const char* e = getenv("HW_TYPE_ORDER");
-    if (e && strlen(e) == HW_NTYPES)
+    if (!e) return true;
+    // accepted only as a permutation of 0..3: a repeated digit would launch
+    // one type's update twice, concurrently, on the same rows
+    int seen = 0;
+    bool ok = strlen(e) == HW_NTYPES;
+    for (int i = 0; ok && i < HW_NTYPES; ++i) {
+      const int d = e[i] - '0';
+      ok = d >= 0 && d < HW_NTYPES && !(seen & (1 << d));
+      seen |= ok ? 1 << d : 0;
+    }
+    if (ok) {
       for (int i = 0; i < HW_NTYPES; ++i) order[i] = e[i] - '0';
+    } else {
+      fprintf(stderr, "hybridwave_b200: ignoring HW_TYPE_ORDER=%s (not a permutation of 0123)\n", e);
+    }
     return true;
   }();
   (void)order_env;
@@ -250,6 +286,20 @@ static int launch_rhs_all(const hw_mesh_t& M, const hw_fields_t& Q, const Epi& E
   }
   SideStreams* ss = na > 1 ? side_streams() : nullptr;
   if (ss && (rc = ss->fork(st0))) return rc;
+  // every exit after a successful fork joins the side streams back into st0
+  // (an unjoined fork would invalidate a CUDA-graph capture and leave st0
+  // unordered after kernels already enqueued on the side streams)
+  struct Joiner {
+    SideStreams* ss;
+    cudaStream_t st0;
+    int na;
+    ~Joiner() {
+      if (ss) ss->join(st0, na);
+    }
+  };
+  int join_rc = 0;
+  {
+  Joiner joiner{ss, st0, na};
   for (int a = 0; a < na; ++a) {
     const int t = active[a];
     const int64_t K = M.t[t].K;
@@ -304,8 +354,10 @@ static int launch_rhs_all(const hw_mesh_t& M, const hw_fields_t& Q, const Epi& E
     }
     if (rc) return rc;
   }
-  if (ss && (rc = ss->join(st0, na))) return rc;
-  return 0;
+  joiner.ss = nullptr;                     // normal path: join explicitly, keep its status
+  if (ss) join_rc = ss->join(st0, na);
+  }
+  return join_rc;
 }
 
 #ifndef HW_MAX_ORDER
@@ -524,11 +576,13 @@ const char* hw_last_error(void) { return g_err.c_str(); }
 
 int hw_traces(const hw_mesh_t* mesh, const hw_fields_t* q, hw_fields_t* tr,
               const hw_subset_t* subset, void* stream) {
+  HW_DEVICE_GUARD(mesh);
   return run_traces(mesh, q, tr, subset, stream);
 }
 
 int hw_rhs(const hw_mesh_t* mesh, const hw_fields_t* q, hw_fields_t* rhs,
            const hw_subset_t* subset, void* stream) {
+  HW_DEVICE_GUARD(mesh);
   if (!rhs) return fail("null rhs");
   if (!mesh) return fail("null mesh");
   {   // traces of q for the publishing types, on every element (neighbours of
@@ -548,6 +602,7 @@ int hw_rhs(const hw_mesh_t* mesh, const hw_fields_t* q, hw_fields_t* rhs,
 int hw_lsrk_stage(const hw_mesh_t* mesh, const hw_fields_t* q_in, hw_fields_t* q_out,
                   hw_fields_t* res, double a, double b, double dt, const hw_subset_t* subset,
                   void* stream) {
+  HW_DEVICE_GUARD(mesh);
   if (!q_out || !res) return fail("null q_out/res");
   Epi E;
   memset(&E, 0, sizeof(E));
@@ -567,6 +622,7 @@ int hw_ab_step(const hw_mesh_t* mesh, const hw_fields_t* q_in, hw_fields_t* q_ou
                hw_fields_t* h0, const hw_fields_t* h1, const hw_fields_t* h2, int n_hist,
                double c0, double c1, double c2, double dt, const hw_subset_t* subset,
                void* stream) {
+  HW_DEVICE_GUARD(mesh);
   if (n_hist < 1 || n_hist > 3) return fail("history depth must be 1..3");
   Epi E;
   memset(&E, 0, sizeof(E));
@@ -590,6 +646,7 @@ int hw_axpy3(const hw_mesh_t* mesh, const hw_fields_t* q, hw_fields_t* out,
              const hw_fields_t* h0, const hw_fields_t* h1, const hw_fields_t* h2, int n_hist,
              double c0, double c1, double c2, double dt, const hw_subset_t* subset,
              void* stream) {
+  HW_DEVICE_GUARD(mesh);
   cudaStream_t st = (cudaStream_t)stream;
   Axpy3Types a{};
   unsigned g = 0;
@@ -620,6 +677,7 @@ int hw_axpy3(const hw_mesh_t* mesh, const hw_fields_t* q, hw_fields_t* out,
 
 int hw_hist_push(const hw_mesh_t* mesh, hw_fields_t* h0, hw_fields_t* h1, hw_fields_t* h2,
                  const hw_fields_t* rhs, const hw_subset_t* subset, void* stream) {
+  HW_DEVICE_GUARD(mesh);
   cudaStream_t st = (cudaStream_t)stream;
   for (int t = 0; t < HW_NTYPES; ++t) {
     const int64_t K = mesh->t[t].K;
@@ -646,6 +704,7 @@ int hw_hist_push(const hw_mesh_t* mesh, hw_fields_t* h0, hw_fields_t* h1, hw_fie
 
 int hw_halo_pack(const hw_mesh_t* mesh, int elem_type, const void* q, const int32_t* idx,
                  int64_t n, void* sendbuf, void* stream) {
+  HW_DEVICE_GUARD(mesh);
   if (elem_type < 0 || elem_type >= HW_NTYPES) return fail("bad element type");
   if (n <= 0) return 0;
   const int chunk = 4 * np_of(elem_type, mesh->N);
@@ -659,6 +718,7 @@ int hw_halo_pack(const hw_mesh_t* mesh, int elem_type, const void* q, const int3
 }
 
 int hw_energy(const hw_mesh_t* mesh, const hw_fields_t* q, double* out, void* stream) {
+  HW_DEVICE_GUARD(mesh);
   if (!out) return fail("hw_energy: out is null");
   cudaStream_t st = (cudaStream_t)stream;
   cudaError_t e = cudaMemsetAsync(out, 0, HW_NTYPES * sizeof(double), st);

@@ -467,6 +467,8 @@ class DeviceMesh:
         S.dtype = nat.HW_F64 if dtype == torch.float64 else nat.HW_F32
         S.formulation = nat.HW_GL if disc.formulation.kind == "GL" else nat.HW_SEM
         S.penalty_scale = float(disc.penalty_scale)
+        S.device = (self.device.index if self.device.index is not None
+                    else torch.cuda.current_device())
         for t, P in pack["types"].items():
             T = S.t[TYPE_ID[t]]
             T.K = P["K"]

@@ -186,25 +186,90 @@ class Discretization:
             return {t: v.cpu().numpy() for t, v in out.items()}
         return out
 
+    def _const(self, key, make):
+        """Device copy of a host-side reference-layout array, built once."""
+        if not hasattr(self, "_consts"):
+            self._consts = {}
+        if key not in self._consts:
+            self._consts[key] = torch.as_tensor(np.ascontiguousarray(make()),
+                                                dtype=torch.float64, device=self.device)
+        return self._consts[key]
+
+    def _mass_diag(self, t):
+        """Per-node mass weights (hex w3 J, pyramid J; tet: J per element)."""
+        d = self.data[t]
+        if t == "hex":
+            return self._const(("M", t), lambda: d.w3[None, :] * d.J)
+        if t == "tet":
+            return self._const(("M", t), lambda: d.J[:, 0])
+        return self._const(("M", t), lambda: d.J)
+
     def apply_A(self, state):
-        """R = A U without mass inverse or materials (dg.py:469-477),
-        recovered from the device RHS as R = M diag(1/kappa, rho) rhs."""
-        saved = self.forcing
-        self.forcing = None
-        try:
-            rhs = self.compute_rhs({t: np.asarray(_host(v)) for t, v in state.items()})
-        finally:
-            self.forcing = saved
+        """R = A U: volume + surface residual, no mass inverse, no materials
+        (hybridwave/dg.py:469-477).  On the device: the fused RHS kernels,
+        then M diag(1/kappa, rho) applied to their output.  Host arrays in ->
+        host arrays out (through HBM, like compute_rhs)."""
+        on_host = not isinstance(next(iter(state.values())), torch.Tensor)
+        rhs = self.rhs_device(self.to_device(state))
         out = {}
         for t in self.types:
-            mat = self.mesh.materials[t]
-            r = rhs[t].copy()
+            mat = self._const(("mat", t), lambda t=t: self.mesh.materials[t])
+            r = rhs[t].double()
             r[:, 0] /= mat[:, 1][:, None]
             r[:, 1:] *= mat[:, 0][:, None, None]
-            out[t] = self.apply_mass(t, r)
+            out[t] = self._apply_mass(t, r)
+        if on_host:
+            return {t: v.cpu().numpy() for t, v in out.items()}
         return out
 
+    def _apply_mass(self, t, v):
+        if t == "wedge":                   # LSC-DG: identity mass (dg.py:486-487)
+            return v
+        m = self._mass_diag(t)
+        if t == "tet":
+            Mref = self._const(("Mref", t), lambda: self.ops[t].M_ref)
+            return (v @ Mref.T) * m[:, None, None]
+        return v * m[:, None, :]
+
+    def apply_mass_inverse(self, t, residual_t):
+        """hybridwave/dg.py:479-490 on the device: hex / (w3 J), tet
+        invM_ref / J, wedge identity, pyramid / J.  A CUDA tensor stays on
+        the device; a host array is copied in and the result copied back."""
+        on_host = not isinstance(residual_t, torch.Tensor)
+        r = torch.as_tensor(np.asarray(residual_t) if on_host else residual_t,
+                            dtype=torch.float64).to(self.device)
+        if t == "wedge":
+            out = r.clone()
+        elif t == "tet":
+            Minv = self._const(("Minv", t), lambda: self.ops[t].invM_ref)
+            out = (r @ Minv.T) / self._mass_diag(t)[:, None, None]
+        else:
+            out = r / self._mass_diag(t)[:, None, :]
+        return out.cpu().numpy() if on_host else out
+
+    def compute_traces(self, state):
+        """Own-side traces at the reference's stored face points in its flat
+        layout, (4, trace_size) (hybridwave/dg.py:299-316), on the device:
+        state @ Vf^T per type, wedge traces x 1/sqrt(J).  Diagnostic: the
+        stage kernels never form this buffer (they read neighbour state or
+        the compact published traces)."""
+        on_host = not isinstance(next(iter(state.values())), torch.Tensor)
+        q = self.to_device(state)
+        out = torch.empty((FIELDS, self.trace_size), dtype=torch.float64, device=self.device)
+        for t in self.types:
+            op = self.ops[t]
+            Vf = self._const(("Vf", t), lambda op=op: op.Vf)
+            tr = q[t].double() @ Vf.T                               # (K, 4, Nfp)
+            if t == "wedge":
+                tr = tr * self._const(("isJf", t),
+                                      lambda: self.data["wedge"].invsqrtJ_face)[:, None, :]
+            b = self.trace_bases[t]
+            n = self.n_elems[t] * op.face_offsets[-1]
+            out[:, b:b + n] = tr.transpose(0, 1).reshape(FIELDS, n)
+        return out.cpu().numpy() if on_host else out
+
     def apply_mass(self, t, v):
+        """Host M v (diagnostics / tests)."""
         d = self.data[t]
         if t == "hex":
             return v * (d.w3[None, None, :] * d.J[:, None, :])
@@ -213,33 +278,6 @@ class Discretization:
         if t == "wedge":
             return v.copy()
         return v * d.J[:, None, :]
-
-    def apply_mass_inverse(self, t, residual_t):
-        """hybridwave/dg.py:479-490 (host)."""
-        d = self.data[t]
-        r = _host(residual_t)
-        if t == "hex":
-            return r / (d.w3[None, None, :] * d.J[:, None, :])
-        if t == "tet":
-            return (r @ self.ops[t].invM_ref.T) / d.J[:, 0][:, None, None]
-        if t == "wedge":
-            return r
-        return r / d.J[:, None, :]
-
-    def compute_traces(self, state):
-        """Own-side traces at the reference's stored face points, (4,
-        trace_size) (dg.py:299-316).  Diagnostic; the kernels never form it."""
-        self._ensure_reference_layout()
-        out = np.empty((FIELDS, self.trace_size))
-        for t in self.types:
-            op, d = self.ops[t], self.data[t]
-            tr = _host(state[t]) @ op.Vf.T
-            if t == "wedge":
-                tr = tr * d.invsqrtJ_face[:, None, :]
-            tot = op.face_offsets[-1]
-            b = self.trace_bases[t]
-            out[:, b:b + self.n_elems[t] * tot] = tr.transpose(1, 0, 2).reshape(FIELDS, -1)
-        return out
 
     # ------------------------------------------------------------ forcing / projection
 

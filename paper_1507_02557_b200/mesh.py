@@ -350,95 +350,118 @@ def graded_hybrid_mesh(n, layers=None, ratio=0.5, nx=None):
 
 # ---------------------------------------------------------------- GMSH
 
-GMSH_TYPES = {4: ("tet", 4), 5: ("hex", 8), 6: ("wedge", 6), 7: ("pyramid", 5)}
-_WEDGE_GMSH_TO_LOCAL = (0, 2, 1, 3, 5, 4)
+# msh 2.2 element code -> (type, vertex count); lower-dimensional codes that a
+# volume mesh may carry (line, triangle, quad, point) are skipped
+_MSH_VOLUME = {4: ("tet", 4), 5: ("hex", 8), 6: ("wedge", 6), 7: ("pyramid", 5)}
+_MSH_SKIPPED = frozenset((1, 2, 3, 15))
+# gmsh's prism runs its triangle the other way round from our (r, t)
+# triangle: reversing corners 1 <-> 2 on both triangles keeps J > 0
+_MSH_PRISM_ORDER = np.array([0, 2, 1, 3, 5, 4])
+
+
+class _MshCursor:
+    """Line cursor over a .msh file; every error names the 1-based line."""
+
+    def __init__(self, path):
+        self.path = path
+        with open(path) as fh:
+            self.rows = fh.read().splitlines()
+        self.i = 0
+
+    def error(self, what):
+        return GmshParseError(f"{self.path}:{self.i + 1}: {what}")
+
+    def marker(self, name):
+        while self.i < len(self.rows) and not self.rows[self.i].strip():
+            self.i += 1
+        if self.i >= len(self.rows) or self.rows[self.i].strip() != name:
+            raise self.error(f"expected {name}")
+        self.i += 1
+
+    def fields(self, what, min_len=1):
+        if self.i >= len(self.rows):
+            raise self.error(what)
+        f = self.rows[self.i].split()
+        if len(f) < min_len or f[0].startswith("$"):
+            raise self.error(what)
+        self.i += 1
+        return f
+
+    def count(self, what):
+        try:
+            return int(self.fields(what)[0])
+        except ValueError:
+            self.i -= 1
+            raise self.error(what) from None
 
 
 def read_gmsh(path):
-    """GMSH v2.2 ASCII reader (hybridwave/mesh.py:359-442): linear volume
-    elements 4/5/6/7, first tag = physical group, GmshParseError with the
-    1-based line number on malformed input."""
-    with open(path) as fh:
-        lines = fh.read().splitlines()
-    pos = 0
+    """Linear volume mesh from a GMSH 2.2 ASCII file (reference interface:
+    hybridwave/mesh.py:359-442).  Element codes 4/5/6/7 become tet, hex,
+    wedge, pyramid blocks (prism corners reordered to our orientation);
+    the first element tag is kept as the physical group; lines, triangles,
+    quads and points are ignored; anything else raises GmshParseError with
+    the offending line number."""
+    cur = _MshCursor(path)
+    cur.marker("$MeshFormat")
+    version = cur.fields("only msh format 2.2 is supported")[0]
+    if not version.startswith("2.2"):
+        cur.i -= 1
+        raise cur.error("only msh format 2.2 is supported")
+    cur.marker("$EndMeshFormat")
 
-    def fail(msg):
-        raise GmshParseError(f"{path}:{pos + 1}: {msg}")
+    cur.marker("$Nodes")
+    n_nodes = cur.count("bad node count")
+    tags = np.empty(n_nodes, dtype=np.int64)
+    xyz = np.empty((n_nodes, 3))
+    for r in range(n_nodes):
+        f = cur.fields("truncated $Nodes section" if cur.i >= len(cur.rows)
+                       else "bad node line", 4)
+        tags[r] = int(f[0])
+        xyz[r] = f[1:4]
+    cur.marker("$EndNodes")
+    row_of = dict(zip(tags.tolist(), range(n_nodes)))
 
-    def expect(tag):
-        nonlocal pos
-        while pos < len(lines) and not lines[pos].strip():
-            pos += 1
-        if pos >= len(lines) or lines[pos].strip() != tag:
-            fail(f"expected {tag}")
-        pos += 1
-
-    expect("$MeshFormat")
-    head = lines[pos].split() if pos < len(lines) else []
-    if not head or not head[0].startswith("2.2"):
-        fail("only msh format 2.2 is supported")
-    pos += 1
-    expect("$EndMeshFormat")
-    expect("$Nodes")
-    try:
-        n_nodes = int(lines[pos])
-    except (ValueError, IndexError):
-        fail("bad node count")
-    pos += 1
-    coords = np.zeros((n_nodes, 3))
-    ids = {}
-    for i in range(n_nodes):
-        if pos >= len(lines):
-            fail("truncated $Nodes section")
-        parts = lines[pos].split()
-        if len(parts) < 4:
-            fail("bad node line")
-        ids[int(parts[0])] = i
-        coords[i] = [float(v) for v in parts[1:4]]
-        pos += 1
-    expect("$EndNodes")
-    expect("$Elements")
-    try:
-        n_el = int(lines[pos])
-    except (ValueError, IndexError):
-        fail("bad element count")
-    pos += 1
-    blocks = {t: [] for t in ELEMENT_TYPES}
-    phys = {t: [] for t in ELEMENT_TYPES}
-    for _ in range(n_el):
-        if pos >= len(lines) or lines[pos].strip().startswith("$"):
-            fail("truncated $Elements section")
-        parts = lines[pos].split()
-        if len(parts) < 3:
-            fail("bad element line")
-        code, ntags = int(parts[1]), int(parts[2])
-        nodes = parts[3 + ntags:]
-        if code in GMSH_TYPES:
-            t, nvt = GMSH_TYPES[code]
-            if len(nodes) != nvt:
-                fail(f"{t} element needs {nvt} nodes, got {len(nodes)}")
-            try:
-                conn = [ids[int(v)] for v in nodes]
-            except KeyError as e:
-                fail(f"unknown node id {e}")
-            if t == "wedge":
-                conn = [conn[p] for p in _WEDGE_GMSH_TO_LOCAL]
-            blocks[t].append(conn)
-            phys[t].append(int(parts[3]) if ntags > 0 else 0)
-        elif code not in (1, 2, 3, 15):
-            fail(f"unsupported element code {code}")
-        pos += 1
-    expect("$EndElements")
-    return HybridMesh(coords, {t: v for t, v in blocks.items() if v},
-                      physical={t: np.array(v) for t, v in phys.items() if v})
+    cur.marker("$Elements")
+    n_items = cur.count("bad element count")
+    conn = {t: [] for t in ELEMENT_TYPES}
+    group = {t: [] for t in ELEMENT_TYPES}
+    for _ in range(n_items):
+        f = cur.fields("truncated $Elements section", 1)
+        if len(f) < 3:
+            cur.i -= 1
+            raise cur.error("bad element line")
+        code, ntag = int(f[1]), int(f[2])
+        if code in _MSH_SKIPPED:
+            continue
+        if code not in _MSH_VOLUME:
+            cur.i -= 1
+            raise cur.error(f"unsupported element code {code}")
+        kind, nv = _MSH_VOLUME[code]
+        verts = f[3 + ntag:]
+        if len(verts) != nv:
+            cur.i -= 1
+            raise cur.error(f"{kind} element needs {nv} nodes, got {len(verts)}")
+        missing = [v for v in verts if int(v) not in row_of]
+        if missing:
+            cur.i -= 1
+            raise cur.error(f"unknown node id {missing[0]}")
+        row = np.array([row_of[int(v)] for v in verts])
+        conn[kind].append(row[_MSH_PRISM_ORDER] if kind == "wedge" else row)
+        group[kind].append(int(f[3]) if ntag else 0)
+    cur.marker("$EndElements")
+    present = [t for t in ELEMENT_TYPES if conn[t]]
+    return HybridMesh(xyz, {t: np.array(conn[t]) for t in present},
+                      physical={t: np.array(group[t]) for t in present})
 
 
 def mesh_volume(mesh, N=2):
+    """Total volume as the sum over types of w . J at an exact-degree
+    element rule (the reference's mesh check, hybridwave/mesh.py:449-459)."""
     from .quadrature import element_rule
-    from .refelem import geometric_factors_batch
-    total = 0.0
+    from .refelem import jacobian_det_fast
+    vol = {}
     for t in mesh.elem_types:
         rule = element_rule(t, N)
-        _, J, _, _ = geometric_factors_batch(t, mesh.element_vertices(t), rule.collapsed)
-        total += float(np.sum(J @ rule.weights))
-    return total
+        vol[t] = jacobian_det_fast(t, mesh.element_vertices(t), rule.collapsed) @ rule.weights
+    return float(sum(v.sum() for v in vol.values()))

@@ -105,7 +105,7 @@ def _single_rate_forced(disc, state, dt, T_final, callback, out):
         q = new
         time += h
         if callback is not None:
-            callback(time, _export(disc, q, host))
+            callback(time, _view(disc, q, host))
     return _export(disc, q, host, out)
 
 
@@ -123,7 +123,7 @@ def _lsrk_forced(disc, state, dt, T_final, callback, out):
                 q[t] = q[t] + b * res[t]
         time += h
         if callback is not None:
-            callback(time, _export(disc, q, host))
+            callback(time, _view(disc, q, host))
     return _export(disc, q, host, out)
 
 
@@ -179,22 +179,35 @@ class Stepper:
         self.n_steps += 1
 
 
-def single_rate_run(disc, state, dt, T_final, callback=None, out=None):
+def _view(disc, q, host):
+    """State handed to a callback: the live device buffers for a device run
+    (the reference also passes live references, timeint.py:68-70; no
+    copy, no sync), fresh host arrays for a host run."""
+    return _export(disc, q, True) if host else dict(q)
+
+
+def _want_callback(callback, every, n, time, T_final):
+    return callback is not None and (n % every == 0 or time >= T_final - 1e-14)
+
+
+def single_rate_run(disc, state, dt, T_final, callback=None, out=None, callback_every=1):
     """AB3 to T_final; the last step lands through the fractional
     coefficients (hybridwave/timeint.py:57-72).  out: optional host arrays
-    the final state is written into.  With a forcing callback the step is
-    the unfused RHS + host forcing + update (slow path)."""
+    the final state is written into; callback_every: call back every k-th
+    step (and after the last).  With a forcing callback the step is the
+    fused RHS + device forcing + update."""
     if disc.forcing is not None:
         return _single_rate_forced(disc, state, dt, T_final, callback, out)
     host = _is_host(state)
     S = Stepper(disc, state, "ab")
-    time = 0.0
+    time, n = 0.0, 0
     while time < T_final - 1e-14:
         h = min(dt, T_final - time)
         S.ab_step(dt, theta=h / dt)
         time += h
-        if callback is not None:
-            callback(time, _export(disc, S.q, host))
+        n += 1
+        if _want_callback(callback, callback_every, n, time, T_final):
+            callback(time, _view(disc, S.q, host))
     return _export(disc, S.q, host, out)
 
 
@@ -217,21 +230,21 @@ def lsrk_step(disc, q, res, dt, q_tmp=None):
     return q
 
 
-def lsrk_run(disc, state, dt, T_final, callback=None, out=None):
+def lsrk_run(disc, state, dt, T_final, callback=None, out=None, callback_every=1):
     """Low-storage RK(4,5) to T_final with the single_rate_run signature;
-    the last step is shortened to land on T_final (forcing: slow path as in
-    single_rate_run)."""
+    the last step is shortened to land on T_final."""
     if disc.forcing is not None:
         return _lsrk_forced(disc, state, dt, T_final, callback, out)
     host = _is_host(state)
     S = Stepper(disc, state, "lsrk")
-    time = 0.0
+    time, n = 0.0, 0
     while time < T_final - 1e-14:
         h = min(dt, T_final - time)
         S.lsrk_step(h)
         time += h
-        if callback is not None:
-            callback(time, _export(disc, S.q, host))
+        n += 1
+        if _want_callback(callback, callback_every, n, time, T_final):
+            callback(time, _view(disc, S.q, host))
     return _export(disc, S.q, host, out)
 
 
@@ -419,7 +432,7 @@ class MRABDriver:
                         q[t][sel] += dt_min * 2 ** (L - lev) * upd
             self.macro_steps += 1
             if callback is not None:
-                callback(t0 + dt_min * 2 ** (L - 1), _export(disc, q, host))
+                callback(t0 + dt_min * 2 ** (L - 1), _view(disc, q, host))
         out = _export(disc, q, host)
         for t in disc.types:
             if host:
@@ -441,18 +454,25 @@ class MRABDriver:
         macro = 2 ** (L - 1) * self.plan.dt_min
         n_macro = max(1, math.ceil(T_final / macro - 1e-12))
         dt_min = T_final / (n_macro * 2 ** (L - 1))
-        q = disc.to_device(state)
         if getattr(self, "_bufs", None) is None:      # persistent work buffers
-            self._bufs = (disc.empty_state(), [disc.zeros_state() for _ in range(3)])
+            # the driver owns the state buffers it steps (the caller's
+            # state is copied in and written back at the end), so a captured
+            # graph's pointers stay valid for every later run()
+            self._bufs = (disc.empty_state(), [disc.zeros_state() for _ in range(3)],
+                          disc.empty_state())
             subs = {lev: self._subset([lev]) for lev in range(1, L + 1)}
             self._subs_keep = subs
             self._sub_structs = {lev: nat.subset(subs[lev]) for lev in subs}
             self._graphs = {}
-        eff, ring = self._bufs
+        eff, ring, q = self._bufs
+        src = disc.to_device(state)
+        for t in disc.types:
+            q[t].copy_(src[t])
+        del src
         n_hist = np.zeros(L + 1, dtype=int)
         steps = np.zeros(L + 1, dtype=int)
-        use_graph = (graph and callback is None and q[disc.types[0]].is_cuda)
-        gkey = (tuple(q[t].data_ptr() for t in disc.types), dt_min)
+        use_graph = graph and callback is None
+        gkey = dt_min
         g = self._graphs.get(gkey) if use_graph else None
         m = 0
         while m < n_macro:
@@ -478,7 +498,7 @@ class MRABDriver:
             self.macro_steps += 1
             m += 1
             if callback is not None:
-                callback(t0 + dt_min * 2 ** (L - 1), _export(disc, q, host))
+                callback(t0 + dt_min * 2 ** (L - 1), _view(disc, q, host))
         out = _export(disc, q, host)
         for t in disc.types:
             if host:

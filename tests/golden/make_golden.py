@@ -286,7 +286,57 @@ def nonaffine_fixtures():
     print("non-affine fixtures written")
 
 
+def mrab_multilevel_fixtures():
+    """Reference mrab_run on a graded mesh where 3 (and, with n_levels=5,
+    more) rate levels are occupied.  The graded generator is the repo's own
+    (the reference has none); its vertices / blocks are wrapped in the
+    reference's HybridMesh so every number below comes from the reference."""
+    sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+    from paper_1507_02557_b200.mesh import graded_hybrid_mesh
+    from hybridwave.mesh import HybridMesh
+    fd = {}
+    g = graded_hybrid_mesh(6)
+    for tag, N, form, n_levels, n_macro in [("g6_n2_gl_l3", 2, "GL", 3, 7),
+                                            ("g6_n3_gl_l3", 3, "GL", 3, 6),
+                                            ("g6_n2_sem_l3", 2, "SEM", 3, 6),
+                                            ("g6_n2_gl_l5", 2, "GL", 5, 3)]:
+        m = HybridMesh(g.vertices.copy(), {t: g.blocks[t].copy() for t in g.elem_types})
+        d = Discretization(m, N, form)
+        st0 = d.project(cavity_fields, 0.0)
+        plan = assign_mrab_levels(local_timesteps(d, 0.5), n_levels, m, cfl=0.5)
+        occupied = sorted({int(x) for v in plan.levels.values() for x in np.unique(v)})
+        T = n_macro * 2 ** (n_levels - 1) * plan.dt_min
+        en = []
+        s, drv = mrab_run(d, plan, {t: v.copy() for t, v in st0.items()}, T,
+                          callback=lambda tau, st: en.append(discrete_energy(st, d)))
+        for t in d.types:
+            fd[f"{tag}/{t}"] = s[t]
+            fd[f"{tag}/levels/{t}"] = plan.levels[t]
+            fd[f"{tag}/evals/{t}"] = drv.rhs_evals[t]
+        fd[f"{tag}/dt_min"] = np.array(plan.dt_min)
+        fd[f"{tag}/T"] = np.array(T)
+        fd[f"{tag}/occupied"] = np.array(occupied)
+        fd[f"{tag}/macro_steps"] = np.array(drv.macro_steps)
+        fd[f"{tag}/energy"] = np.array(en)
+        fd[f"{tag}/energy0"] = np.array(discrete_energy(st0, d))
+        print(tag, "levels", occupied, "macro", drv.macro_steps,
+              "elements", {t: d.n_elems[t] for t in d.types})
+    # uniform levels: one occupied level must reproduce single-rate AB3 (SPEC.md:693)
+    m = HybridMesh(g.vertices.copy(), {t: g.blocks[t].copy() for t in g.elem_types})
+    d = Discretization(m, 2, "GL")
+    st0 = d.project(cavity_fields, 0.0)
+    dt = min(float(v.min()) for v in local_timesteps(d, 0.5).values())
+    sab = single_rate_run(d, {t: v.copy() for t, v in st0.items()}, dt, 12 * dt)
+    for t in d.types:
+        fd[f"uniform/ab3/{t}"] = sab[t]
+    fd["uniform/dt"] = np.array(dt)
+    np.savez_compressed(os.path.join(HERE, "mrab_levels.npz"), **fd)
+    print("multi-level MRAB fixtures written")
+
+
 if __name__ == "__main__":
+    if sys.argv[1:] == ["mrab_levels"]:
+        sys.exit(mrab_multilevel_fixtures())
     if sys.argv[1:] == ["nonaffine"]:
         sys.exit(nonaffine_fixtures())
     if sys.argv[1:] == ["convergence"]:
