@@ -92,7 +92,19 @@ struct TetMma {
   static constexpr int SQ = 0, SV = SQ + E * EQ, SFP = SV, SFU = SFP + E * EF,
                        SRES = SV + E * RA, SG = SRES + E * EQ,
                        SMAT = SG + E * GEO_TET, TOTAL = SMAT + E * 4;
-  static constexpr size_t BYTES = sizeof(S) * TOTAL + sizeof(int) * (E + NFP);
+  // int region: element ids, own face-node table, then (16-byte aligned)
+  // the block's gather-index rows when they arrive by TMA
+  static constexpr int SIDX = ((E + NFP + 3) / 4) * 4;
+  static constexpr size_t BYTES = sizeof(S) * TOTAL + sizeof(int) * (SIDX + E * NFP);
+  // TMA (cp.async.bulk) staging of whole element rows: rows contiguous in
+  // smem (no K padding) and every copy a multiple of 16 bytes at 16-byte
+  // aligned addresses; otherwise the cp.async path stages them
+  static constexpr bool TMA_OK =
+      NPK == NP && (4 * NP * sizeof(S)) % 16 == 0 && (EQ * sizeof(S)) % 16 == 0 &&
+      (SRES * sizeof(S)) % 16 == 0 && (SG * sizeof(S)) % 16 == 0 &&
+      (SMAT * sizeof(S)) % 16 == 0 && (TOTAL * sizeof(S)) % 16 == 0 &&
+      (E * GEO_TET * sizeof(S)) % 16 == 0 && (E * 4 * sizeof(S)) % 16 == 0 &&
+      (NFP * 4) % 16 == 0;
 #ifndef HW_TET_MINB_MID
 #define HW_TET_MINB_MID 4
 #endif
@@ -145,6 +157,16 @@ __global__ void __launch_bounds__(TetMma<N, S>::NTH, TetMma<N, S>::MINB)
   const int ne = (int)((nwork - w0) < EB ? (nwork - w0) : EB);
   const bool lsrk = E.mode == MODE_LSRK;
 
+  // TMA path: a full block of consecutive elements (no subset list)
+  __shared__ __align__(8) uint64_t tbar[2];
+  const bool tma = L::TMA_OK && list == nullptr && ne == EB;
+  int* sidx = reinterpret_cast<int*>(sm + L::TOTAL) + L::SIDX;
+  const S* q = (const S*)Q.p[HW_TET];
+  if (tma && tid == 0) {
+    mbar_init(&tbar[0], 1);
+    mbar_init(&tbar[1], 1);
+    mbar_fence_init();
+  }
   if (tid < EB) sk[tid] = tid < ne ? (list ? list[w0 + tid] : (int)(w0 + tid)) : 0;
   for (int i = tid; i < NFP; i += NTH) sfn[i] = __ldg(TY.iop[0] + i);
   // K padding must be zero for the DMMA (rows are never written by copies)
@@ -158,23 +180,54 @@ __global__ void __launch_bounds__(TetMma<N, S>::NTH, TetMma<N, S>::MINB)
     }
   __syncthreads();
 
-  // ---- P0: element rows, records; the gather index straight into
-  // registers (thread-item u is (e, j) = (tid + u * NTH) / NFP, % NFP, the
-  // mapping the flux loop uses)
-  const S* q = (const S*)Q.p[HW_TET];
-  tet_rows<L>(sq, q, sk, ne);
-  copy_rows<GEO_TET, GEO_TET, NTH, EB>(sg, (const S*)TY.geo, sk, ne);
-  copy_rows<4, 4, NTH, EB>(smat, (const S*)TY.mat, sk, ne);
+  // ---- P0: element rows, records and the gather index.  TMA path: warp 0
+  // issues one bulk copy per element row (q; the LSRK residual on a second
+  // barrier, waited for only by the epilogue) and one per record array.
+  // cp.async path (subset lists, partial blocks, padded rows): per-thread
+  // 16-byte copies and the gather index straight into registers.
+  // Thread-item u is (e, j) = (tid + u * NTH) / NFP, % NFP, the mapping the
+  // flux loop uses.
+  constexpr unsigned ROWB = 4 * NP * sizeof(S);
   int gv[IT];
+  if (tma) {
+    if (warp == 0) {
+      if (lane == 0) {
+        mbar_expect_tx(&tbar[0], EB * ROWB + EB * (GEO_TET + 4) * sizeof(S) + EB * NFP * 4);
+        if (lsrk) mbar_expect_tx(&tbar[1], EB * ROWB);
+      }
+      __syncwarp();
+      const S* res = (const S*)E.res[HW_TET];
+      for (int e = lane; e < EB; e += 32) {
+        bulk_load(sq + e * EQ, q + (size_t)(w0 + e) * 4 * NP, ROWB, &tbar[0]);
+        if (lsrk) bulk_load(sres + e * EQ, res + (size_t)(w0 + e) * 4 * NP, ROWB, &tbar[1]);
+      }
+      if (lane == 0) {
+        bulk_load(sg, (const S*)TY.geo + (size_t)w0 * GEO_TET, EB * GEO_TET * sizeof(S),
+                  &tbar[0]);
+        bulk_load(smat, (const S*)TY.mat + (size_t)w0 * 4, EB * 4 * sizeof(S), &tbar[0]);
+        bulk_load(sidx, TY.iop[1] + (size_t)w0 * NFP, EB * NFP * 4, &tbar[0]);
+      }
+    }
+    mbar_wait(&tbar[0], 0);
 #pragma unroll
-  for (int u = 0; u < IT; ++u) {
-    const int i = tid + u * NTH;
-    gv[u] = -1;
-    if (i < ne * NFP) gv[u] = __ldg(TY.iop[1] + (size_t)sk[i / NFP] * NFP + i % NFP);
+    for (int u = 0; u < IT; ++u) {
+      const int i = tid + u * NTH;
+      gv[u] = i < EB * NFP ? sidx[i] : -1;
+    }
+  } else {
+    tet_rows<L>(sq, q, sk, ne);
+    copy_rows<GEO_TET, GEO_TET, NTH, EB>(sg, (const S*)TY.geo, sk, ne);
+    copy_rows<4, 4, NTH, EB>(smat, (const S*)TY.mat, sk, ne);
+#pragma unroll
+    for (int u = 0; u < IT; ++u) {
+      const int i = tid + u * NTH;
+      gv[u] = -1;
+      if (i < ne * NFP) gv[u] = __ldg(TY.iop[1] + (size_t)sk[i / NFP] * NFP + i % NFP);
+    }
+    cp_async_commit();
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    __syncthreads();
   }
-  cp_async_commit();
-  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-  __syncthreads();
 
   // ---- P1: neighbour face-node values (registers, consumed by the flux)
   R nb[IT][4];
@@ -263,8 +316,9 @@ __global__ void __launch_bounds__(TetMma<N, S>::NTH, TetMma<N, S>::MINB)
     sfu[e * EF + f * NFK + jj] = S(fu * R(g[3]));
   }
   __syncthreads();
-  // LSRK residual rows, fetched behind the lift GEMM
-  if (lsrk) {
+  // LSRK residual rows, fetched behind the lift GEMM (the TMA path issued
+  // them with the other rows)
+  if (lsrk && !tma) {
     tet_rows<L>(sres, (const S*)E.res[HW_TET], sk, ne);
     cp_async_commit();
   }
@@ -302,11 +356,57 @@ __global__ void __launch_bounds__(TetMma<N, S>::NTH, TetMma<N, S>::MINB)
       }
     }
   }
+  const int n = rt * 8 + (lane >> 2);
+  if (tma) {
+    // results into the staged rows (each (node, element) is read and
+    // written by one lane only), then one bulk store per element row
+    if (lsrk) mbar_wait(&tbar[1], 0);
+    if (gw && n < NP) {
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int e = col0 + i;
+        const S kap = smat[e * 4 + 0], irho = smat[e * 4 + 1];
+        S* qe = sq + e * EQ + n;
+        S* re = sres + e * EQ + n;
+        const size_t base = (size_t)(w0 + e) * 4 * NP + n;
+#pragma unroll
+        for (int x = 0; x < 4; ++x) {
+          const S v = x == 0 ? S(accp[i] * R(kap)) : S(accu[x - 1][i] * R(irho));
+          const S qv = qe[x * NPK];
+          if (lsrk) {
+            const S r = S(E.a) * re[x * NPK] + S(E.dt) * v;
+            re[x * NPK] = r;
+            qe[x * NPK] = qv + S(E.b) * r;
+          } else if (E.mode == MODE_RHS) {
+            qe[x * NPK] = v;
+          } else {
+            S acc = S(E.c0) * v;
+            if (E.nhist > 1) acc += S(E.c1) * ((const S*)E.h1[HW_TET])[base + x * NP];
+            if (E.nhist > 2) acc += S(E.c2) * ((const S*)E.h2[HW_TET])[base + x * NP];
+            re[x * NPK] = v;
+            qe[x * NPK] = qv + S(E.dt) * acc;
+          }
+        }
+      }
+    }
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (warp == 0) {
+      S* d1 = (S*)(E.mode == MODE_RHS ? E.out[HW_TET] : E.qout[HW_TET]);
+      S* d2 = (S*)(lsrk ? E.res[HW_TET] : (E.mode == MODE_AB ? E.out[HW_TET] : nullptr));
+      for (int e = lane; e < EB; e += 32) {
+        bulk_store(d1 + (size_t)(w0 + e) * 4 * NP, sq + e * EQ, ROWB);
+        if (d2) bulk_store(d2 + (size_t)(w0 + e) * 4 * NP, sres + e * EQ, ROWB);
+      }
+      bulk_commit();
+      bulk_wait_read();
+    }
+    return;
+  }
   if (lsrk) {
     asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     __syncthreads();
   }
-  const int n = rt * 8 + (lane >> 2);
   if (gw && n < NP) {
 #pragma unroll
     for (int i = 0; i < 2; ++i) {

@@ -148,10 +148,18 @@ def test_polynomial_preservation(N, form, native_lib):
     exact derivative (-div u, -grad p) of the polynomial (1e-11)."""
     d = _disc("hybrid:3", N, form)
     fields, rhs = _poly(N)
-    got = d.compute_rhs(d.project(fields, 0.0))
+    st = d.project(fields, 0.0)
+    got = d.compute_rhs(st)
+    assert rel_err(got, oracle.compute_rhs(d, st)) < 1e-12
     exp = d.project(rhs, 0.0)
     for t in d.types:
         ids = _interior(d, t)
+        # SEM integrates quad faces with the (N+1)-point GLL rule (exact to
+        # degree 2N-1); the skew LSC wedge's average flux on them is degree
+        # 2N, so the reference itself does not preserve polynomials there
+        # (its RHS = the oracle's, asserted above)
+        if form == "SEM" and t == "wedge":
+            continue
         if len(ids):
             scale = np.abs(exp[t][ids]).max()
             assert np.abs(got[t][ids] - exp[t][ids]).max() <= 1e-11 * max(scale, 1.0), t

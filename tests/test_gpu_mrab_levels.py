@@ -55,8 +55,9 @@ def test_mrab_levels_match_reference(tag, N, form, n_levels, native_lib):
 @pytest.mark.parametrize("tag,N,form,n_levels", [CASES[0], CASES[3]])
 def test_mrab_levels_energy(tag, N, form, n_levels, native_lib):
     """Per-macro-step discrete energy (device hw_energy through the live
-    callback state) equals the reference's and never increases
-    (cavity run at CFL 0.5)."""
+    callback state) equals the reference's and never increases once every
+    level has its AB3 history (cavity run at CFL 0.5; the
+    AB1/AB2 warm-up macro step raises it, in the reference too)."""
     from paper_1507_02557_b200.timeint import mrab_run
     d, st0, plan = _setup(tag, N, form, n_levels)
     st = d.to_device(st0)
@@ -67,8 +68,8 @@ def test_mrab_levels_energy(tag, N, form, n_levels, native_lib):
     ref = G[f"{tag}/energy"]
     np.testing.assert_allclose(en, ref, rtol=1e-10)
     e0 = float(G[f"{tag}/energy0"])
-    seq = np.concatenate([[e0], en])
-    assert np.all(np.diff(seq) <= 1e-10 * e0)
+    assert np.all(np.diff(en) <= 1e-10 * e0)
+    assert np.all(np.diff(ref) <= 1e-10 * e0)
 
 
 def test_mrab_step_counting(native_lib):
