@@ -129,6 +129,13 @@ __device__ __forceinline__ void tet_rows(S* dst, const S* src, const int* sk, in
   }
 }
 
+// MMA column c of a column tile holds element pi(c) of its 8: swapping the
+// elements 4<->5 and 6<->7 makes the accumulator layout (lane holds columns
+// 2(lane&3) + {0,1}) touch four different bank groups in the epilogue
+// (elements {0,2,5,7} and {1,3,4,6} instead of {0,2,4,6}); B-fragment loads
+// stay conflict-free under any column permutation.
+__device__ __forceinline__ int tet_col_elem(int c) { return c ^ ((c >> 2) & 1); }
+
 // SK: skew form (forms_override testing hook) as a compile-time variant so
 // the production strong-form kernel carries none of its code
 template <int N, typename S, bool SK = false>
@@ -261,7 +268,7 @@ __global__ void __launch_bounds__(TetMma<N, S>::NTH, TetMma<N, S>::MINB)
 
   // ---- P2: volume GEMMs on DMMA
   const int rt = warp / L::CT, ct = warp - rt * L::CT;
-  const int bk = lane & 3, bcol = ct * 8 + (lane >> 2);
+  const int bk = lane & 3, bcol = ct * 8 + tet_col_elem(lane >> 2);
   constexpr bool skew = SK;
   R dp[3][2] = {{0, 0}, {0, 0}, {0, 0}}, dv[2] = {0, 0};
   const bool gw = warp < L::W;   // GEMM warp
@@ -324,12 +331,14 @@ __global__ void __launch_bounds__(TetMma<N, S>::NTH, TetMma<N, S>::MINB)
   }
 
   // ---- P4: lift on DMMA, combine, epilogue
-  const int col0 = ct * 8 + (lane & 3) * 2;
+  int ecol[2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) ecol[i] = ct * 8 + tet_col_elem((lane & 3) * 2 + i);
   R accp[2] = {skew ? dv[0] : -dv[0], skew ? dv[1] : -dv[1]};
   R accu[3][2];
 #pragma unroll
   for (int i = 0; i < 2; ++i) {
-    const S* G = sg + (col0 + i) * GEO_TET;
+    const S* G = sg + ecol[i] * GEO_TET;
 #pragma unroll
     for (int x = 0; x < 3; ++x)
       accu[x][i] = -(R(G[x]) * dp[0][i] + R(G[3 + x]) * dp[1][i] + R(G[6 + x]) * dp[2][i]);
@@ -349,7 +358,7 @@ __global__ void __launch_bounds__(TetMma<N, S>::NTH, TetMma<N, S>::MINB)
       }
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
-        const S* g = sg + (col0 + i) * GEO_TET + 9 + FS * f;
+        const S* g = sg + ecol[i] * GEO_TET + 9 + FS * f;
         accu[0][i] += R(g[0]) * tu[i];
         accu[1][i] += R(g[1]) * tu[i];
         accu[2][i] += R(g[2]) * tu[i];
@@ -364,7 +373,7 @@ __global__ void __launch_bounds__(TetMma<N, S>::NTH, TetMma<N, S>::MINB)
     if (gw && n < NP) {
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
-        const int e = col0 + i;
+        const int e = ecol[i];
         const S kap = smat[e * 4 + 0], irho = smat[e * 4 + 1];
         S* qe = sq + e * EQ + n;
         S* re = sres + e * EQ + n;
@@ -410,7 +419,7 @@ __global__ void __launch_bounds__(TetMma<N, S>::NTH, TetMma<N, S>::MINB)
   if (gw && n < NP) {
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
-      const int e = col0 + i;
+      const int e = ecol[i];
       if (e >= ne) continue;
       const R kap = smat[e * 4 + 0], irho = smat[e * 4 + 1];
       const size_t base = (size_t)sk[e] * 4 * NP + n;
