@@ -871,19 +871,46 @@ __global__ void HW_HEX_BOUNDS hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi E,
   }
   if (tid < 24) spc[tid] = __ldg(TY.iop[3] + tid);
   if (tid < ne) sk[tid] = list ? list[w0 + tid] : (int)(w0 + tid);
+  // TMA bulk copies of the element rows: every hex row (state, residual,
+  // traces, record, material) is a multiple of 16 bytes, so each element
+  // (of a subset list too) is one copy per array.  Group 0: volume inputs;
+  // group 1: own traces (GL) and the LSRK residual, waited for by the flux.
+  __shared__ __align__(8) uint64_t tbar[2];
+  const bool lsrk = E.mode == MODE_LSRK;
+  if (tid == 0) {
+    mbar_init(&tbar[0], 1);
+    mbar_init(&tbar[1], 1);
+    mbar_fence_init();
+  }
   __syncthreads();
-  // group 1 (volume inputs): state rows, records, links
-  copy_rows16<4 * NP, 4 * NP, NT, EPB>(sq, (const R*)Q.p[HW_HEX], sk, ne);
-  copy_rows16<GEO_HEX, GEO_HEX, NT, EPB>(sg, (const R*)TY.geo, sk, ne);   // 72 words
-  copy_rows<4, 4, NT, EPB>(smat, (const R*)TY.mat, sk, ne);
+  constexpr unsigned ROWB = 4 * NP * sizeof(R), TRB = 4 * NFP * sizeof(R);
+  static_assert(ROWB % 16 == 0 && TRB % 16 == 0 && (GEO_HEX * sizeof(R)) % 16 == 0 &&
+                    (L::SRES * sizeof(R)) % 16 == 0 && (L::STR * sizeof(R)) % 16 == 0 &&
+                    (L::SG * sizeof(R)) % 16 == 0 && (L::SMAT * sizeof(R)) % 16 == 0,
+                "hex rows / smem offsets must be 16-byte multiples for the bulk copies");
+  if (tid < 32) {
+    if (tid == 0) {
+      mbar_expect_tx(&tbar[0], ne * (ROWB + (GEO_HEX + 4) * sizeof(R)));
+      mbar_expect_tx(&tbar[1], ne * ((sem ? 0u : TRB) + (lsrk ? ROWB : 0u)));
+    }
+    __syncwarp();
+    for (int e = tid; e < ne; e += 32) {
+      const size_t k = (size_t)sk[e];
+      bulk_load(sq + e * 4 * NP, (const R*)Q.p[HW_HEX] + k * 4 * NP, ROWB, &tbar[0]);
+      bulk_load(sg + e * GEO_HEX, (const R*)TY.geo + k * GEO_HEX, GEO_HEX * sizeof(R),
+                &tbar[0]);
+      bulk_load(smat + e * 4, (const R*)TY.mat + k * 4, 4 * sizeof(R), &tbar[0]);
+      if (!sem)
+        bulk_load(sm + L::STR + e * 4 * NFP, (const R*)M.tr_in[HW_HEX] + k * 4 * NFP, TRB,
+                  &tbar[1]);
+      if (lsrk)
+        bulk_load(sm + L::SRES + e * 4 * NP, (const R*)E.res[HW_HEX] + k * 4 * NP, ROWB,
+                  &tbar[1]);
+    }
+  }
   for (int i = tid; i < ne * 6; i += NT)
     snc[i] = __ldg(TY.nbr_code + (size_t)sk[i / 6] * 6 + i % 6);
-  cp_async_commit();
-  // group 2 (flux / epilogue inputs): own traces (GL), LSRK residual, and the
-  // neighbour values at my face points through the host gather index
-  if (!sem) copy_rows16<4 * NFP, 4 * NFP, NT, EPB>(sm + L::STR, (const R*)M.tr_in[HW_HEX], sk, ne);
-  if (E.mode == MODE_LSRK)
-    copy_rows16<4 * NP, 4 * NP, NT, EPB>(sm + L::SRES, (const R*)E.res[HW_HEX], sk, ne);
+  // the neighbour values at my face points through the host gather index
   {
     constexpr int IT = (EPB * NFP + NT - 1) / NT;
     int gv[IT];
@@ -915,8 +942,8 @@ __global__ void HW_HEX_BOUNDS hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi E,
     }
   }
   cp_async_commit();
-  asm volatile("cp.async.wait_group 1;\n" ::: "memory");
-  __syncthreads();
+  mbar_wait(&tbar[0], 0);
+  __syncthreads();     // snc
 
   // skew form (forms_override testing hook, hybridwave/dg.py:392-398): the
   // pressure term is sum_c D^T (w3 J v_c), v_c = sum_x G[c][x] u_x, formed
@@ -1001,6 +1028,7 @@ __global__ void HW_HEX_BOUNDS hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi E,
   }
 
   cp_async_wait_all();
+  mbar_wait(&tbar[1], 0);
   __syncthreads();
 
   const R pen = R(M.penalty_scale);
@@ -1106,18 +1134,34 @@ __global__ void HW_HEX_BOUNDS hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi E,
     const R kap = smat[e * 4 + 0], irho = smat[e * 4 + 1];
     const size_t base = (size_t)sk[e] * 4 * NP + n;
     R* qe = sq + e * 4 * NP + n;
-    const R* re = sm + L::SRES + e * 4 * NP + n;
+    R* re = sm + L::SRES + e * 4 * NP + n;
+    // results into the staged rows (q_out over q; the residual / rhs / new
+    // slope over the residual row), written back by bulk stores below
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       const R v = acc[s][c] * (c == 0 ? kap : irho);
-      qe[c * NP] = epilogue_q<R>(E, HW_HEX, base + c * NP, v, qe[c * NP], re[c * NP]);
+      const R qv = qe[c * NP];
+      if (lsrk) {
+        const R r = R(E.a) * re[c * NP] + R(E.dt) * v;
+        re[c * NP] = r;
+        qe[c * NP] = qv + R(E.b) * r;
+      } else if (E.mode == MODE_RHS) {
+        re[c * NP] = v;
+      } else {
+        R a = R(E.c0) * v;
+        if (E.nhist > 1) a += R(E.c1) * ((const R*)E.h1[HW_HEX])[base + c * NP];
+        if (E.nhist > 2) a += R(E.c2) * ((const R*)E.h2[HW_HEX])[base + c * NP];
+        re[c * NP] = v;
+        qe[c * NP] = qv + R(E.dt) * a;
+      }
     }
   }
-  if (!sem && E.mode != MODE_RHS && M.tr_out[HW_HEX] != nullptr) {
+  const bool pub = !sem && E.mode != MODE_RHS && M.tr_out[HW_HEX] != nullptr;
+  if (pub) {
     __syncthreads();
     // GL hex traces of the new state: one thread per (element, axis, line)
-    // reads the line once and interpolates to both end faces of the axis
-    R* tro = (R*)M.tr_out[HW_HEX];
+    // reads the line once and interpolates to both end faces of the axis;
+    // into the (dead) own-trace rows, bulk-stored with the state rows
     for (int it = tid; it < ne * 3 * NFQ; it += NT) {
       const int e = it / (3 * NFQ), r = it - e * 3 * NFQ;
       const int a = r / NFQ, uv = r - a * NFQ, u = uv / N1, v = uv - u * N1;
@@ -1137,7 +1181,7 @@ __global__ void HW_HEX_BOUNDS hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi E,
           t1[c] += w1 * x;
         }
       }
-      R* o = tro + (size_t)sk[e] * 4 * NFP;
+      R* o = sm + L::STR + e * 4 * NFP;
 #pragma unroll
       for (int end = 0; end < 2; ++end) {
         const int f = 2 * a + end;
@@ -1147,6 +1191,20 @@ __global__ void HW_HEX_BOUNDS hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi E,
         for (int c = 0; c < 4; ++c) o[c * NFP + f * NFQ + pt] = end ? t1[c] : t0[c];
       }
     }
+  }
+  fence_proxy_async_smem();
+  __syncthreads();
+  if (tid < 32) {
+    R* dq = E.mode == MODE_RHS ? nullptr : (R*)E.qout[HW_HEX];
+    R* dr = (R*)(lsrk ? E.res[HW_HEX] : E.out[HW_HEX]);
+    for (int e = tid; e < ne; e += 32) {
+      const size_t k = (size_t)sk[e];
+      bulk_store(dr + k * 4 * NP, sm + L::SRES + e * 4 * NP, ROWB);
+      if (dq) bulk_store(dq + k * 4 * NP, sq + e * 4 * NP, ROWB);
+      if (pub) bulk_store((R*)M.tr_out[HW_HEX] + k * 4 * NFP, sm + L::STR + e * 4 * NFP, TRB);
+    }
+    bulk_commit();
+    bulk_wait_read();
   }
 }
 

@@ -8,8 +8,14 @@ Per element type (K elements):
   nbr_elem/code    (K, nfaces) int32: neighbour index and packed
                    type | face << 2 | orientation << 5 | boundary bit
   operators        constant matrices (device_operators), a few KB-100 KB
-No per-point geometry and no face-trace buffer are stored: neighbour
-traces are evaluated from the neighbour's state inside the kernels.
+  face gather index per element: the source offset of every face point's
+                   neighbour value, in this element's point order
+  face traces      (K, 4, Nfp) ping-pong buffers for the publishing types
+                   (wedge, pyramid, GL hex): each stage writes the traces of
+                   its output state; tets and SEM hexes are read by their
+                   neighbours straight from the state (selection traces)
+Per-point geometry exists only where the geometry is non-affine (pyramid
+base faces, cubature wedges); affine elements carry per-face records.
 """
 
 import numpy as np
