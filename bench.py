@@ -1,22 +1,25 @@
 #!/usr/bin/env python
 """Benchmark: LSRK-45 steps of the DG acoustic RHS + update on B200.
 
-Headline workload (BASELINE.json metric "GDOF·stage/s per LSRK step",
-configs[2]): the reference's structured hybrid cube hybrid:38 (14,440 hex,
-25,992 wedge, 7,220 pyramid, 158,840 tet = 206,492 elements), N=3, GL,
-fp64, cavity-mode initial data projected on the host, dt from the
-reference's local timestep rule (CFL 0.5).  One step = 5 RHS stages, each
-one fused kernel launch per element type; the timed loop replays a CUDA
-graph of one step.
+Default workload (BASELINE.json configs[3], the configuration the metric's
+1/2/4/8-GPU series is quoted on): the hex-dominant hybrid cube hexdom:120
+(1,584,000 hex, 115,200 wedge, 72,000 pyramid, 460,800 tet = 2,232,000
+elements, 907 M DOF), N=4, GL, fp64, cavity-mode initial data projected on
+the host, dt from the reference's local timestep rule (CFL 0.5).  The SAME
+mesh at every GPU count (strong scaling): N=1 runs the whole mesh on one
+B200, N>1 element-partitions it (x-slabs).  One step = 5 RHS stages, each
+one fused kernel launch per element type; on one GPU the timed loop replays
+a CUDA graph of one step.  ``--mesh hybrid:38 --order 3`` is configs[2]
+(the reference's own hybrid cube), ``--mesh tet:20`` configs[1].
 
   python bench.py [--gpus N --steps K --warmup W] [--impl reference]
-                  [--mesh hybrid:38 --order 3 --form GL --dtype f64]
+                  [--mesh hexdom:120 --order 4 --form GL --dtype f64]
 
-Multi-GPU (torchrun, N > 1): the mesh is extended along x to N slabs and
-element-partitioned (one slab per rank, the single-GPU workload each: weak
-scaling); every LSRK stage exchanges the partition-boundary element states
-with NCCL batched P2P while the interior elements compute
+Multi-GPU (torchrun, N > 1): every LSRK stage exchanges the shared-face
+values of the partition-boundary elements (face nodes or published face
+traces) with NCCL batched P2P while the interior elements compute
 (paper_1507_02557_b200/parallel.py); timing is the max over ranks.
+hybrid:n meshes are instead extended along x to n*N cells (weak scaling).
 """
 
 import argparse
@@ -44,8 +47,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=40)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--mesh", default="hybrid:38")
-    ap.add_argument("--order", type=int, default=3)
+    ap.add_argument("--mesh", default="hexdom:120")
+    ap.add_argument("--order", type=int, default=4)
     ap.add_argument("--form", default="GL", choices=["GL", "SEM"])
     ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
     ap.add_argument("--cpu-mesh", default=None, help="reference-arm sample mesh")
@@ -92,12 +95,26 @@ def n_dof(disc):
 
 def cpu_sample_mesh(args):
     """Bounded sample of the workload for the CPU oracle: the same band
-    layout, order and formulation on a coarser cube (per-DOF rate)."""
+    layout, order and formulation on a coarser cube (per-DOF rate):
+    hexdom:14 (4 hex / 4 wedge / 1 pyramid / 5 tet layers of 14 x 14 cells)
+    for configs[3], hybrid:20 for configs[2]."""
     if args.cpu_mesh:
         return args.cpu_mesh
     kind, n = args.mesh.split(":")
     n = int(n)
-    return f"{kind}:{min(n, 10)}"
+    cap = {"hexdom": 14, "hybrid": 20, "tet": 20, "hex": 12, "graded": 12}.get(kind, 10)
+    return f"{kind}:{min(n, cap)}"
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
 
 
 def run_cpu_oracle(args, steps, warmup):
@@ -122,8 +139,20 @@ def run_cpu_oracle(args, steps, warmup):
     value = d.n_dof * 5 * steps / el / 1e9
     cores = int(os.environ.get("OPENBLAS_NUM_THREADS", os.cpu_count() or 1))
     sample = (f"{spec} N={args.order} {args.form} fp64 ({sum(d.n_elems.values())} elements, "
-              f"{d.n_dof} DOF), {steps} LSRK steps (5 oracle RHS each)")
+              f"{d.n_dof} DOF), {steps} LSRK steps (5 oracle RHS each); "
+              f"host CPU: {cpu_model()}, {os.cpu_count()} logical cores")
     return value, el / steps, sample, cores
+
+
+def scaling_of(spec):
+    """hybrid:n is extended along x with the GPU count (weak); every other
+    mesh is the same at every GPU count (strong)."""
+    return "weak" if spec.split(":")[0] == "hybrid" else "strong"
+
+
+def workload_label(args):
+    return (f"{args.mesh} N={args.order} {args.form} LSRK-45 ({config_index(args.mesh)})"
+            + (f", jitter {args.jitter}" if args.jitter else ""))
 
 
 def reference_arm(args):
@@ -135,12 +164,12 @@ def reference_arm(args):
     value, sps, sample, cores = run_cpu_oracle(args, steps, warm)
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
             "n_gpus": args.gpus, "steps": steps, "warmup": warm, "ms_per_step": sps * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": scaling_of(args.mesh), "vs_baseline": None,
+            "dtype": "f64",
             "data": "synthetic (cavity eigenmode projected on the mesh)",
-            "config": {"workload": f"{args.mesh} N={args.order} {args.form} LSRK-45",
-                       "sample": sample},
+            "config": {"workload": workload_label(args), "sample": sample},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                             "sample": sample},
+                             "sample": sample, "cpu_model": cpu_model()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -388,18 +417,17 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, sps, sample, cores = run_cpu_oracle(args, 3, 1)
-        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample}
+        v, sps, sample, cores = run_cpu_oracle(args, 2, 0)
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample,
+               "cpu_model": cpu_model()}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "higher_is_better": True, "scaling": scaling_of(args.mesh), "vs_baseline": None,
                 "dtype": args.dtype,
-                "data": "synthetic (cavity eigenmode projected on the mesh), per-rank replica",
-                "config": {"workload": f"{args.mesh} N={args.order} {args.form} LSRK-45 "
-                                       f"({config_index(args.mesh)})" +
-                                       (f", jitter {args.jitter}" if args.jitter else ""),
+                "data": "synthetic (cavity eigenmode projected on the mesh)",
+                "config": {"workload": workload_label(args),
                            "elements": {t: disc.n_elems[t] for t in disc.types},
                            "n_dof_per_rank": disc.n_dof, "dt": dt,
                            "l2_policy": "inputs larger than L2 (state+res+q_out "
@@ -573,21 +601,22 @@ def partitioned(args, world, rank, local, dev, dtype, s_bytes):
     d2h = sum(v.numel() * v.element_size() for v in h_out.values())
     assert all(torch.isfinite(ps.S.q[t_]).all() for t_ in dl.types), "state diverged"
     value = total_dof * 5 * args.steps / (ms * 1e-3) / 1e9
-    halo = sum(int(b - a) * 4 * dl.ops[t_].Np * s_bytes
-               for per_t in part.recv.values() for t_, (a, b) in per_t.items())
+    halo = ps.halo_bytes
+    halo_full = sum(int(b - a) * 4 * dl.ops[t_].Np * s_bytes
+                    for per_t in part.recv.values() for t_, (a, b) in per_t.items())
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
                 "higher_is_better": True, "scaling": "weak" if weak else "strong",
                 "vs_baseline": None, "dtype": args.dtype,
                 "data": "synthetic (cavity eigenmode projected on the mesh)",
-                "config": {"workload": f"{args.mesh} N={args.order} {args.form} LSRK-45, "
-                                       f"x-extended x{world}, x-slab partition" if weak else
-                                       f"{args.mesh} N={args.order} {args.form} LSRK-45, "
-                                       "x-slab partition",
+                "config": {"workload": workload_label(args),
+                           "partition": (f"x-extended x{world}, x-slab" if weak else
+                                         f"x-slab x{world}"),
                            "n_dof_total": int(total_dof), "dt": dt, "setup_s": setup_s,
                            "halo_bytes_per_stage_rank0": halo,
-                           "parallelism": f"element partition x{world}, NCCL halo",
+                           "halo_bytes_if_whole_ghost_states_rank0": halo_full,
+                           "parallelism": f"element partition x{world}, NCCL face halo",
                            "cuda_graph": False,
                            "l2_policy": "inputs larger than L2"},
                 "gpu_launches": launches,

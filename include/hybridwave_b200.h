@@ -141,6 +141,19 @@ int hw_hist_push(const hw_mesh_t* mesh, hw_fields_t* h0, hw_fields_t* h1,
 int hw_halo_pack(const hw_mesh_t* mesh, int elem_type, const void* q,
                  const int32_t* idx, int64_t n, void* sendbuf, void* stream);
 
+/* Face-level halo exchange of partitioned runs (no reference counterpart:
+ * the reference has no distributed path).  A
+ * partition-boundary element's neighbour across the cut is a ghost whose
+ * only data the kernels read is the shared face: its face nodes (tet, SEM
+ * hex state) or its published face traces (wedge, pyramid, GL hex).
+ * gather: buf[c*n + i] = src[off[i] + c*stride];  scatter: dst[off[i] +
+ * c*stride] = buf[c*n + i]  (c = 0..3 fields; off = flat element-row
+ * offsets of field 0, stride = Np for states, Nfp for trace buffers). */
+int hw_halo_gather(const hw_mesh_t* mesh, const void* src, int64_t stride,
+                   const int64_t* off, int64_t n, void* buf, void* stream);
+int hw_halo_scatter(const hw_mesh_t* mesh, const void* buf, int64_t stride,
+                    const int64_t* off, int64_t n, void* dst, void* stream);
+
 /* Discrete energy U^T M U with material weights (p^2 / kappa + rho |u|^2)
  * per element type (discrete_energy, hybridwave/dg.py:655-674).  out is a
  * DEVICE pointer to HW_NTYPES doubles: zeroed on `stream`, then one sum

@@ -501,6 +501,30 @@ __global__ void pack_kernel(const R* __restrict__ q, const int32_t* __restrict__
   }
 }
 
+// face-level halo: buf[c * n + i] = src[off[i] + c * stride] (gather) and
+// dst[off[i] + c * stride] = buf[c * n + i] (scatter), c = 0..3 fields
+template <typename R>
+__global__ void halo_gather_kernel(const R* __restrict__ src, int64_t stride,
+                                   const int64_t* __restrict__ off, int64_t n,
+                                   R* __restrict__ buf) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < 4 * n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = i / n, j = i - c * n;
+    buf[i] = src[off[j] + c * stride];
+  }
+}
+
+template <typename R>
+__global__ void halo_scatter_kernel(const R* __restrict__ buf, int64_t stride,
+                                    const int64_t* __restrict__ off, int64_t n,
+                                    R* __restrict__ dst) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < 4 * n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = i / n, j = i - c * n;
+    dst[off[j] + c * stride] = buf[i];
+  }
+}
+
 static int np_of(int t, int N) {
   switch (t) {
     case HW_HEX: return (N + 1) * (N + 1) * (N + 1);
@@ -715,6 +739,38 @@ int hw_halo_pack(const hw_mesh_t* mesh, int elem_type, const void* q, const int3
   else
     pack_kernel<float><<<g, 256, 0, st>>>((const float*)q, idx, n, chunk, (float*)sendbuf);
   return check_launch("pack_kernel");
+}
+
+int hw_halo_gather(const hw_mesh_t* mesh, const void* src, int64_t stride, const int64_t* off,
+                   int64_t n, void* buf, void* stream) {
+  HW_DEVICE_GUARD(mesh);
+  if (n <= 0) return 0;
+  if (!src || !off || !buf) return fail("hw_halo_gather: null pointer");
+  const unsigned g = grid_for(4 * n);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (mesh->dtype == HW_F64)
+    halo_gather_kernel<double><<<g, 256, 0, st>>>((const double*)src, stride, off, n,
+                                                  (double*)buf);
+  else
+    halo_gather_kernel<float><<<g, 256, 0, st>>>((const float*)src, stride, off, n,
+                                                 (float*)buf);
+  return check_launch("halo_gather_kernel");
+}
+
+int hw_halo_scatter(const hw_mesh_t* mesh, const void* buf, int64_t stride, const int64_t* off,
+                    int64_t n, void* dst, void* stream) {
+  HW_DEVICE_GUARD(mesh);
+  if (n <= 0) return 0;
+  if (!dst || !off || !buf) return fail("hw_halo_scatter: null pointer");
+  const unsigned g = grid_for(4 * n);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (mesh->dtype == HW_F64)
+    halo_scatter_kernel<double><<<g, 256, 0, st>>>((const double*)buf, stride, off, n,
+                                                   (double*)dst);
+  else
+    halo_scatter_kernel<float><<<g, 256, 0, st>>>((const float*)buf, stride, off, n,
+                                                  (float*)dst);
+  return check_launch("halo_scatter_kernel");
 }
 
 int hw_energy(const hw_mesh_t* mesh, const hw_fields_t* q, double* out, void* stream) {

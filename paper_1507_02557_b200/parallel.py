@@ -1,14 +1,19 @@
 """Element-partitioned LSRK-45 across GPUs (one process per GPU) with a
-per-stage halo exchange of partition-boundary element states.
+per-stage face-level halo exchange.
 
-Per stage, on every rank:
-  1. pack the owned elements other ranks hold as ghosts (hw_halo_pack);
-  2. start the exchange: NCCL send/recv (torch.distributed, one P2P group per
-     stage) straight into the contiguous ghost ranges of q_in;
+A ghost element is read by my boundary elements only through the face it
+shares with them: its face nodes (tet, SEM hex: selection traces of the
+state) or its published face traces (wedge, pyramid, GL hex).  So only
+those face values travel (hex N=4: 4 x 25 values per cut face instead of
+the 4 x 125 of a whole element state).  Per stage, on every rank:
+  1. gather the shared-face values of my owned elements the peers touch
+     (hw_halo_gather: face nodes of q_in, or my input-trace rows);
+  2. start the exchange: NCCL send/recv (torch.distributed, one batched P2P
+     group per stage) into per-peer receive buffers;
   3. run the fused stage kernels on the owned *interior* elements (they read
      no ghost) while the exchange is in flight;
-  4. wait, form the ghosts' face traces (hw_traces on the ghost subset), run
-     the owned *boundary* elements.
+  4. wait, scatter the received face values into the ghosts' state rows /
+     input-trace rows (hw_halo_scatter), run the owned *boundary* elements.
 The arithmetic per element is the single-GPU kernels' (the same kernels,
 on subsets), so partitioned runs reproduce single-GPU results to rounding
 (tests/test_gpu_parity.py::test_partitioned_lsrk_loopback).
@@ -34,7 +39,10 @@ def make_parts(mesh, nparts, method="xslab", N=3, ranks=None):
 
 
 class NCCLTransport:
-    """Halo exchange over torch.distributed (NCCL on GPUs, gloo on CPU)."""
+    """Halo exchange over torch.distributed (NCCL on GPUs, gloo on CPU):
+    ``ps.send_buffers()`` / ``ps.recv_buffers(q)`` list (peer, tensor) in
+    the canonical (peer, element type) order both sides derive from the
+    global partition, so the batched P2P operations pair up."""
 
     def __init__(self, group=None):
         import torch.distributed as dist
@@ -43,13 +51,9 @@ class NCCLTransport:
 
     def start(self, ps, q):
         d = self.dist
-        ops = []
-        for peer, per_t in ps.sendbuf.items():
-            for t, buf in per_t.items():
-                ops.append(d.P2POp(d.isend, buf, peer, group=self.group))
-        for peer, per_t in ps.part.recv.items():
-            for t, (a, b) in per_t.items():
-                ops.append(d.P2POp(d.irecv, q[t][a:b], peer, group=self.group))
+        ops = [d.P2POp(d.isend, buf, peer, group=self.group) for peer, buf in ps.send_buffers()]
+        ops += [d.P2POp(d.irecv, buf, peer, group=self.group)
+                for peer, buf in ps.recv_buffers(q)]
         return d.batch_isend_irecv(ops) if ops else []
 
     def wait(self, handle):
@@ -58,23 +62,45 @@ class NCCLTransport:
 
 
 class LoopbackTransport:
-    """In-process exchange between PartSteppers sharing one GPU (tests):
-    ghost rows are copied from the owning part's current input state."""
+    """In-process exchange between the parts of one partition sharing one
+    GPU (tests): each receiver pulls its halo from the owning part."""
 
     def __init__(self):
         self.steppers = {}
 
     def start(self, ps, q):
-        for peer, per_t in ps.part.recv.items():
-            other = self.steppers[peer]
-            src = other.halo_source()
-            for t, (a, b) in per_t.items():
-                src_idx = other.send_idx[ps.part.rank][t]
-                q[t][a:b].copy_(src[t][src_idx.long()])
+        for peer in ps.part.recv:
+            ps.receive_from(self.steppers[peer], q)
         return None
 
     def wait(self, handle):
         return None
+
+
+def face_halo_offsets(t, dops, N, sem):
+    """Per face of type t: (offsets of the face's values within one element
+    row of the halo source, field stride kind).  Tet and SEM hex faces are
+    read from the state (face nodes), the publishing types from their trace
+    rows (device face-point order)."""
+    fo = np.asarray(dops["face_offsets"])
+    nf = len(fo) - 1
+    if t == "tet":
+        nfn = len(dops["face_nodes"]) // 4
+        fn = np.asarray(dops["face_nodes"]).reshape(4, nfn)
+        return [fn[f].astype(np.int64) for f in range(4)], "state"
+    if t == "hex" and sem:
+        tab = np.asarray(dops["face_tab"]).reshape(-1, 3)
+        return [(tab[fo[f]:fo[f + 1], 0] + np.where(tab[fo[f]:fo[f + 1], 2] != 0, N, 0)
+                 * tab[fo[f]:fo[f + 1], 1]).astype(np.int64) for f in range(nf)], "state"
+    return [np.arange(fo[f], fo[f + 1], dtype=np.int64) for f in range(nf)], "trace"
+
+
+def flat_face_offsets(pairs, local, row):
+    """Flat field-0 offsets of the (element, face) pairs' values: element *
+    row + the face's offsets within the row (row = 4 * Np or 4 * Nfp)."""
+    if len(pairs) == 0:
+        return np.zeros(0, dtype=np.int64)
+    return np.concatenate([int(k) * row + local[int(f)] for k, f in pairs])
 
 
 class PartStepper:
@@ -101,60 +127,104 @@ class PartStepper:
             return out
         self._keep = [lists("interior"), lists("boundary"), lists("ghost")]
         self.sub_interior, self.sub_boundary, self.sub_ghost = (nat.subset(x) for x in self._keep)
-        self.send_idx = {peer: {t: torch.as_tensor(idx, dtype=torch.int32, device=dev)
-                                for t, idx in per_t.items()}
-                         for peer, per_t in part.send.items()}
-        self.sendbuf = {peer: {t: torch.empty((len(idx), 4, d.ops[t].Np), dtype=dtype, device=dev)
-                               for t, idx in per_t.items()}
-                        for peer, per_t in part.send.items()}
+        # face-level halo: flat offsets of the shared faces' values in the
+        # halo source (state rows or trace rows) on both sides
+        pack = dm_pack = d.device_mesh.pack
+        sem = d.formulation.kind == "SEM"
+        self.kind, self.row, self.fstride = {}, {}, {}
+        local = {}
+        for t in d.types:
+            local[t], self.kind[t] = face_halo_offsets(t, dm_pack["types"][t]["dops"], N, sem)
+            nfp = pack["types"][t]["nfp"]
+            Np = d.ops[t].Np
+            self.fstride[t] = Np if self.kind[t] == "state" else nfp
+            self.row[t] = 4 * self.fstride[t]
+        as_dev = lambda a: torch.as_tensor(a, dtype=torch.int64, device=dev)
+        self.send_off = {peer: {t: as_dev(flat_face_offsets(pr, local[t], self.row[t]))
+                                for t, pr in per_t.items()}
+                         for peer, per_t in part.send_faces.items()}
+        self.recv_off = {peer: {t: as_dev(flat_face_offsets(pr, local[t], self.row[t]))
+                                for t, pr in per_t.items()}
+                         for peer, per_t in part.recv_faces.items()}
+        self.sendbuf = {peer: {t: torch.empty(4 * o.numel(), dtype=dtype, device=dev)
+                               for t, o in per_t.items()}
+                        for peer, per_t in self.send_off.items()}
+        self.recvbuf = {peer: {t: torch.empty(4 * o.numel(), dtype=dtype, device=dev)
+                               for t, o in per_t.items()}
+                        for peer, per_t in self.recv_off.items()}
         if isinstance(transport, LoopbackTransport):
             transport.steppers[part.rank] = self
         self.n_dof_owned = sum(part.n_owned[t] * 4 * d.ops[t].Np for t in d.types)
+        self.halo_bytes = sum(b.numel() * b.element_size()
+                              for per_t in self.recvbuf.values() for b in per_t.values())
 
-    def halo_source(self):
-        """The state whose partition-boundary rows the peers receive."""
-        return self.S.q
+    def _source(self, t, tr_set):
+        return (self.S.q[t] if self.kind[t] == "state"
+                else self.disc.device_mesh.traces[tr_set][TYPE_ID[t]])
+
+    def send_buffers(self):
+        return [(peer, self.sendbuf[peer][t]) for peer in sorted(self.sendbuf)
+                for t in self.disc.types if t in self.sendbuf[peer]]
+
+    def recv_buffers(self, q):
+        return [(peer, self.recvbuf[peer][t]) for peer in sorted(self.recvbuf)
+                for t in self.disc.types if t in self.recvbuf[peer]]
+
+    def receive_from(self, other, q):
+        """Loopback: the owning part gathers my halo from its current input."""
+        other._pack(only=self.part.rank)
+        for t, buf in self.recvbuf[other.part.rank].items():
+            buf.copy_(other.sendbuf[self.part.rank][t])
 
     def launches_per_stage(self):
-        """Kernel launches one stage issues (bench gpu_launches): halo packs,
-        interior and boundary stage kernels per present type, ghost traces
-        per publishing type with ghosts."""
+        """Kernel launches one stage issues (bench gpu_launches): halo
+        gathers and scatters, interior and boundary stage kernels per
+        present type."""
         d, p = self.disc, self.part
-        n = sum(len(per_t) for per_t in self.send_idx.values())
+        n = sum(len(per_t) for per_t in self.send_off.values())
+        n += sum(len(per_t) for per_t in self.recv_off.values())
         n += sum(1 for t in d.types if p.n_interior[t] > 0)
         n += sum(1 for t in d.types if p.n_owned[t] > p.n_interior[t])
-        sem = d.formulation.kind == "SEM"
-        pub = ("wedge", "pyramid") if sem else ("hex", "wedge", "pyramid")
-        n += sum(1 for t in d.types if t in pub and d.n_elems[t] > p.n_owned[t])
         return n
 
-    def _pack(self, q):
+    def _pack(self, only=None):
+        """Gather the shared-face values of this stage's input (state q_in,
+        input trace set) for the peers (only: one peer)."""
         L, st = nat.lib(), self.disc.stream_ptr()
         dm = self.disc.device_mesh
-        for peer, per_t in self.send_idx.items():
-            for t, idx in per_t.items():
-                nat.check(L.hw_halo_pack(dm.struct, TYPE_ID[t], q[t].data_ptr(), idx.data_ptr(),
-                                         idx.numel(), self.sendbuf[peer][t].data_ptr(), st))
+        for peer, per_t in self.send_off.items():
+            if only is not None and peer != only:
+                continue
+            for t, off in per_t.items():
+                src = self._source(t, self.S.tr)
+                nat.check(L.hw_halo_gather(dm.struct, src.data_ptr(), self.fstride[t],
+                                           off.data_ptr(), off.numel(),
+                                           self.sendbuf[peer][t].data_ptr(), st))
 
     def begin(self):
-        """Pack and start the exchange of this stage's input states."""
-        self._pack(self.S.q)
+        """Gather and start the exchange of this stage's shared-face values."""
+        if not isinstance(self.transport, LoopbackTransport):
+            self._pack()
         self._handle = self.transport.start(self, self.S.q)
 
     def finish(self, a, b, h):
-        """Interior elements (overlapping the exchange), then the ghosts'
-        traces and the boundary elements."""
+        """Interior elements (overlapping the exchange), then the received
+        face values into the ghosts and the boundary elements."""
         S, d = self.S, self.disc
         L, st, dm = nat.lib(), d.stream_ptr(), d.device_mesh
         F = S._f
         handle, self._handle = self._handle, None
+        tin = S.tr                      # input trace set of this stage
         S._stage_traces()
         nat.check(L.hw_lsrk_stage(dm.struct, F(S.q), F(S.q2), F(S.res), a, b, h,
                                   self.sub_interior, st))
         self.transport.wait(handle)
-        # ghost traces into the current input trace set
-        tin = 1 - S.tr
-        nat.check(L.hw_traces(dm.struct, F(S.q), nat.fields(dm.traces[tin]), self.sub_ghost, st))
+        for peer, per_t in self.recv_off.items():
+            for t, off in per_t.items():
+                dst = self._source(t, tin)
+                nat.check(L.hw_halo_scatter(dm.struct, self.recvbuf[peer][t].data_ptr(),
+                                            self.fstride[t], off.data_ptr(), off.numel(),
+                                            dst.data_ptr(), st))
         nat.check(L.hw_lsrk_stage(dm.struct, F(S.q), F(S.q2), F(S.res), a, b, h,
                                   self.sub_boundary, st))
 
@@ -227,6 +297,21 @@ class PartMRAB:
 
     def halo_source(self):
         return self.eff
+
+    def send_buffers(self):
+        return [(peer, self.sendbuf[peer][t]) for peer in sorted(self.sendbuf)
+                for t in self.disc.types if t in self.sendbuf[peer]]
+
+    def recv_buffers(self, q):
+        return [(peer, q[t][a:b]) for peer in sorted(self.part.recv)
+                for t in self.disc.types if t in self.part.recv[peer]
+                for a, b in [self.part.recv[peer][t]]]
+
+    def receive_from(self, other, q):
+        """Loopback: ghost rows copied from the owner's effective state."""
+        src = other.halo_source()
+        for t, (a, b) in self.part.recv[other.part.rank].items():
+            q[t][a:b].copy_(src[t][other.send_idx[self.part.rank][t].long()])
 
     def _build_subsets(self):
         d, part, L = self.disc, self.part, self.L

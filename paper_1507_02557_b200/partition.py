@@ -83,6 +83,11 @@ class LocalPart:
     global_ids: dict                   # t -> (K_local,) global element index
     send: dict = field(default_factory=dict)   # peer -> t -> local indices (owned), in order
     recv: dict = field(default_factory=dict)   # peer -> t -> (start, stop) local ghost range
+    # face-level halo: peer -> t -> (n, 2) (local element, face) pairs, the
+    # owned faces a peer's elements touch (send) / the ghost faces my owned
+    # elements touch (recv), both in global (element, face) order
+    send_faces: dict = field(default_factory=dict)
+    recv_faces: dict = field(default_factory=dict)
 
     @property
     def types(self):
@@ -94,8 +99,10 @@ def build_local_parts(mesh, rank_of, ranks=None):
     others are None — a distributed run builds only its own)."""
     nparts = int(max(int(v.max(initial=0)) for v in rank_of.values())) + 1
     types = mesh.elem_types
-    # (type of needed element, element, needing rank) over every cut face
+    # (type of needed element, element, needing rank) over every cut face,
+    # and the same with the needed element's face
     pairs = {t: [] for t in types}
+    fpairs = {t: [] for t in types}
     has_off = {t: np.zeros(len(mesh.blocks[t]), dtype=bool) for t in types}
     for t in types:
         nbr = mesh.nbr[t]
@@ -106,14 +113,18 @@ def build_local_parts(mesh, rank_of, ranks=None):
                 if not sel.any():
                     continue
                 k2 = nbr[sel, f, 1]
+                f2 = nbr[sel, f, 2]
                 rm = r_me[sel]
                 diff = rank_of[t2][k2] != rm
                 has_off[t][np.flatnonzero(sel)[diff]] = True
                 pairs[t2].append(np.column_stack([k2[diff], rm[diff]]))
-    need = {}
+                fpairs[t2].append(np.column_stack([k2[diff], f2[diff], rm[diff]]))
+    need, need_f = {}, {}
     for t in types:
         a = np.vstack(pairs[t]) if pairs[t] else np.zeros((0, 2), dtype=np.int64)
         need[t] = np.unique(a, axis=0)          # rows (element, needing rank), sorted by element
+        a = np.vstack(fpairs[t]) if fpairs[t] else np.zeros((0, 3), dtype=np.int64)
+        need_f[t] = np.unique(a, axis=0)        # rows (element, face, needing rank)
     parts = []
     for r in range(nparts):
         if ranks is not None and r not in ranks:
@@ -158,4 +169,22 @@ def build_local_parts(mesh, rank_of, ranks=None):
             for sr in np.unique(mine[:, 1]):
                 ks = np.sort(mine[mine[:, 1] == sr, 0])
                 part.send.setdefault(int(sr), {})[t] = lookup[ks]
+            # face-level lists: sent (owned element, face) pairs, and the
+            # received ghost (element, face) pairs in the same global order
+            nf = need_f[t]
+            mine = nf[rank_of[t][nf[:, 0]] == r]
+            for sr in np.unique(mine[:, 2]):
+                rows = mine[mine[:, 2] == sr]
+                part.send_faces.setdefault(int(sr), {})[t] = np.column_stack(
+                    [lookup[rows[:, 0]], rows[:, 1]])
+            theirs = nf[nf[:, 2] == r]
+            if len(theirs):
+                glookup = np.full(len(mesh.blocks[t]), -1, dtype=np.int64)
+                gl = part.global_ids[t]
+                glookup[gl[part.n_owned[t]:]] = np.arange(part.n_owned[t], len(gl))
+                src = rank_of[t][theirs[:, 0]]
+                for sr in np.unique(src):
+                    rows = theirs[src == sr]
+                    part.recv_faces.setdefault(int(sr), {})[t] = np.column_stack(
+                        [glookup[rows[:, 0]], rows[:, 1]])
     return parts

@@ -67,13 +67,17 @@ def _hex_metric(X, r, s, t):
 _HEX_FV = [(0, 4, 7, 3), (1, 2, 6, 5), (0, 1, 5, 4), (2, 3, 7, 6), (0, 3, 2, 1), (4, 5, 6, 7)]
 
 
-def rhs(pack, disc, state):
-    """dU/dtau of every type from the packed layout (fp64)."""
+def rhs(pack, disc, state, traces=None):
+    """dU/dtau of every type from the packed layout (fp64).  traces: optional
+    dict t -> (K, 4, Nfp) replacing the traces formed from the state (the
+    partitioned path delivers ghost traces through the face halo)."""
     N = disc.N
     sem = disc.formulation.kind == "SEM"
     d = _dims(N)
     q = {t: np.asarray(state[t], dtype=float) for t in disc.types}
-    traces = {t: own_traces(pack, t, q[t], N, sem) for t in disc.types}
+    own = {t: own_traces(pack, t, q[t], N, sem) for t in disc.types}
+    traces = {t: (traces[t] if traces is not None and t in traces else own[t])
+              for t in disc.types}
     out = {}
     for t in disc.types:
         P = pack["types"][t]
