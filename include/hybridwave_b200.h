@@ -83,6 +83,11 @@ typedef struct {
   void* tr_in[HW_NTYPES];
   void* tr_out[HW_NTYPES];
   hw_type_t t[HW_NTYPES];
+  /* Optional forcing term of dp/dtau per type, state layout (K, 4, Np),
+   * field 0 read (NULL: no forcing): hw_rhs / hw_lsrk_stage / hw_ab_step
+   * add it to the pressure RHS in their epilogue, so the published traces
+   * of the new state include it.  Filled by hw_forcing (assign = 1). */
+  const void* frc[HW_NTYPES];
 } hw_mesh_t;
 
 /* per-type buffers, NULL for absent types */
@@ -140,6 +145,22 @@ int hw_hist_push(const hw_mesh_t* mesh, hw_fields_t* h0, hw_fields_t* h1,
  * element, copy its (4, Np) state into the contiguous send buffer. */
 int hw_halo_pack(const hw_mesh_t* mesh, int elem_type, const void* q,
                  const int32_t* idx, int64_t n, void* sendbuf, void* stream);
+
+/* Forcing residual of the pressure equation, integrated on the device
+ * (replaces Discretization._forcing_residual + its mass inverse and kappa,
+ * hybridwave/dg.py:497-515, 479-490).  f: (K, nq) fp64 values of the forcing
+ * at the type's cubature points (evaluated by the caller, on the device or
+ * copied in); B: (Np, nq) = [invM_ref] V^T diag(w); scale: (K, nq) = J
+ * (sqrt(J) for wedges) at the cubature points; nodefac: (K, Np) per-node
+ * mass inverse (1/(w3 J) hex, 1/J tet and pyramid, 1 wedge).  Adds alpha*F
+ * to the p field of out1 and beta*F to that of out2 (NULL: none): the RHS
+ * (alpha 1), or an LSRK stage's residual (h) and new state (b h), or an AB
+ * step's new slope (1) and new state (dt c0).  assign = 1: out1 = alpha*F
+ * (p field; out2 unused) — the forcing buffer of hw_mesh_t.frc. */
+int hw_forcing(const hw_mesh_t* mesh, int elem_type, const double* f,
+               const double* B, const double* scale, const double* nodefac,
+               int nq, double alpha, void* out1, double beta, void* out2,
+               int assign, void* stream);
 
 /* Face-level halo exchange of partitioned runs (no reference counterpart:
  * the reference has no distributed path).  A

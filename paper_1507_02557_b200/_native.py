@@ -31,7 +31,7 @@ class HWMesh(ctypes.Structure):
                 ("device", c_int32), ("penalty_scale", c_double),
                 ("perm_tri", c_void_p), ("perm_quad", c_void_p),
                 ("tr_in", c_void_p * 4), ("tr_out", c_void_p * 4),
-                ("t", HWType * 4)]
+                ("t", HWType * 4), ("frc", c_void_p * 4)]
 
 
 class HWFields(ctypes.Structure):
@@ -74,6 +74,9 @@ def lib():
         L.hw_halo_pack.argtypes = [P(HWMesh), c_int, c_void_p, c_void_p, c_int64,
                                    c_void_p, c_void_p]
         L.hw_energy.argtypes = [P(HWMesh), P(HWFields), c_void_p, c_void_p]
+        L.hw_forcing.argtypes = [P(HWMesh), c_int, c_void_p, c_void_p, c_void_p, c_void_p,
+                                 c_int, c_double, c_void_p, c_double, c_void_p, c_int,
+                                 c_void_p]
         L.hw_halo_gather.argtypes = [P(HWMesh), c_void_p, c_int64, c_void_p, c_int64,
                                      c_void_p, c_void_p]
         L.hw_halo_scatter.argtypes = [P(HWMesh), c_void_p, c_int64, c_void_p, c_int64,
@@ -81,7 +84,7 @@ def lib():
         L.hw_last_error.restype = ctypes.c_char_p
         for name in ("hw_rhs", "hw_traces", "hw_lsrk_stage", "hw_ab_step", "hw_axpy3",
                      "hw_hist_push", "hw_halo_pack", "hw_halo_gather", "hw_halo_scatter",
-                     "hw_energy", "hw_version", "hw_supported_orders"):
+                     "hw_forcing", "hw_energy", "hw_version", "hw_supported_orders"):
             getattr(L, name).restype = c_int
         L.hw_launch_count.restype = ctypes.c_longlong
         L.hw_launch_count.argtypes = []
@@ -90,7 +93,8 @@ def lib():
 
 
 EXPORTED_SYMBOLS = ("hw_rhs", "hw_traces", "hw_lsrk_stage", "hw_ab_step", "hw_axpy3", "hw_hist_push",
-                    "hw_halo_pack", "hw_halo_gather", "hw_halo_scatter", "hw_energy", "hw_last_error", "hw_version",
+                    "hw_halo_pack", "hw_halo_gather", "hw_halo_scatter", "hw_forcing", "hw_energy",
+                    "hw_last_error", "hw_version",
                     "hw_supported_orders", "hw_launch_count")
 
 

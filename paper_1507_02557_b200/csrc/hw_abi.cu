@@ -501,6 +501,37 @@ __global__ void pack_kernel(const R* __restrict__ q, const int32_t* __restrict__
   }
 }
 
+// Forcing residual of the pressure equation (hybridwave/dg.py:508-515 with
+// the mass inverse of dg.py:479-490 and kappa): one thread per (element,
+// node),
+//   F[k][n] = kappa_k nodefac[k][n] sum_q B[n][q] f[k][q] scale[k][q],
+// then out1[k][0][n] += alpha F, out2[k][0][n] += beta F (optional).
+template <typename R>
+__global__ void forcing_kernel(const double* __restrict__ f, const double* __restrict__ B,
+                               const double* __restrict__ scale,
+                               const double* __restrict__ nodefac, const R* __restrict__ mat,
+                               int64_t K, int np, int nq, double alpha, R* __restrict__ out1,
+                               double beta, R* __restrict__ out2, int assign) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < K * np;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = i / np;
+    const int n = (int)(i - k * np);
+    const double* fk = f + k * nq;
+    const double* sk = scale + k * nq;
+    const double* b = B + (size_t)n * nq;
+    double acc = 0.0;
+    for (int qd = 0; qd < nq; ++qd) acc += b[qd] * (fk[qd] * sk[qd]);
+    const double F = (double)mat[k * 4] * nodefac[i] * acc;
+    const size_t o = (size_t)k * 4 * np + n;
+    if (assign) {
+      out1[o] = R(alpha * F);
+    } else {
+      out1[o] = R((double)out1[o] + alpha * F);
+      if (out2) out2[o] = R((double)out2[o] + beta * F);
+    }
+  }
+}
+
 // face-level halo: buf[c * n + i] = src[off[i] + c * stride] (gather) and
 // dst[off[i] + c * stride] = buf[c * n + i] (scatter), c = 0..3 fields
 template <typename R>
@@ -618,6 +649,7 @@ int hw_rhs(const hw_mesh_t* mesh, const hw_fields_t* q, hw_fields_t* rhs,
   }
   Epi E;
   memset(&E, 0, sizeof(E));
+  for (int t = 0; t < HW_NTYPES; ++t) E.frc[t] = mesh->frc[t];
   E.mode = MODE_RHS;
   for (int t = 0; t < HW_NTYPES; ++t) E.out[t] = rhs->p[t];
   return run_rhs(mesh, q, E, subset, stream);
@@ -630,6 +662,7 @@ int hw_lsrk_stage(const hw_mesh_t* mesh, const hw_fields_t* q_in, hw_fields_t* q
   if (!q_out || !res) return fail("null q_out/res");
   Epi E;
   memset(&E, 0, sizeof(E));
+  for (int t = 0; t < HW_NTYPES; ++t) E.frc[t] = mesh->frc[t];
   E.mode = MODE_LSRK;
   E.a = a;
   E.b = b;
@@ -650,6 +683,7 @@ int hw_ab_step(const hw_mesh_t* mesh, const hw_fields_t* q_in, hw_fields_t* q_ou
   if (n_hist < 1 || n_hist > 3) return fail("history depth must be 1..3");
   Epi E;
   memset(&E, 0, sizeof(E));
+  for (int t = 0; t < HW_NTYPES; ++t) E.frc[t] = mesh->frc[t];
   E.mode = MODE_AB;
   E.nhist = n_hist;
   E.c0 = c0;
@@ -771,6 +805,30 @@ int hw_halo_scatter(const hw_mesh_t* mesh, const void* buf, int64_t stride, cons
     halo_scatter_kernel<float><<<g, 256, 0, st>>>((const float*)buf, stride, off, n,
                                                   (float*)dst);
   return check_launch("halo_scatter_kernel");
+}
+
+int hw_forcing(const hw_mesh_t* mesh, int elem_type, const double* f, const double* B,
+               const double* scale, const double* nodefac, int nq, double alpha, void* out1,
+               double beta, void* out2, int assign, void* stream) {
+  HW_DEVICE_GUARD(mesh);
+  if (elem_type < 0 || elem_type >= HW_NTYPES) return fail("bad element type");
+  const int64_t K = mesh->t[elem_type].K;
+  if (K <= 0) return 0;
+  if (!f || !B || !scale || !nodefac || !out1 || nq <= 0) return fail("hw_forcing: bad arguments");
+  const int np = np_of(elem_type, mesh->N);
+  const unsigned g = grid_for(K * np);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (mesh->dtype == HW_F64)
+    forcing_kernel<double><<<g, 256, 0, st>>>(f, B, scale, nodefac,
+                                              (const double*)mesh->t[elem_type].mat, K, np, nq,
+                                              alpha, (double*)out1, beta, (double*)out2,
+                                              assign);
+  else
+    forcing_kernel<float><<<g, 256, 0, st>>>(f, B, scale, nodefac,
+                                             (const float*)mesh->t[elem_type].mat, K, np, nq,
+                                             alpha, (float*)out1, beta, (float*)out2,
+                                             assign);
+  return check_launch("forcing_kernel");
 }
 
 int hw_energy(const hw_mesh_t* mesh, const hw_fields_t* q, double* out, void* stream) {

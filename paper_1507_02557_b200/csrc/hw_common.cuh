@@ -49,7 +49,14 @@ struct Epi {
   void* qout[HW_NTYPES];       // advanced state
   const void* h1[HW_NTYPES];
   const void* h2[HW_NTYPES];
+  const void* frc[HW_NTYPES];  // forcing term of dp/dtau (state layout), or NULL
 };
+
+// forcing term of dp/dtau at the field-0 index `base` (0 without forcing)
+template <typename S>
+__device__ __forceinline__ S frc_at(const Epi& E, int t, size_t base) {
+  return E.frc[t] ? ((const S*)E.frc[t])[base] : S(0);
+}
 
 template <int N>
 __device__ __forceinline__ int face_offset(int t, int f) {

@@ -433,7 +433,9 @@ __device__ __forceinline__ void dense_mma_body(const hw_mesh_t& M, const hw_fiel
       S* qe = sq + e * EQ + n;
       const S* re = sres + e * EQ + n;
       auto out_p = [&]() {
-        qe[0] = epilogue_q<S>(E, T, base, S(accp[i] * R(smat[e * 4 + 0])), qe[0], re[0]);
+        qe[0] = epilogue_q<S>(E, T, base,
+                              S(accp[i] * R(smat[e * 4 + 0])) + frc_at<S>(E, T, base), qe[0],
+                              re[0]);
       };
       auto out_u = [&]() {
         const R irho = R(smat[e * 4 + 1]);

@@ -380,7 +380,8 @@ __global__ void __launch_bounds__(TetMma<N, S>::NTH, TetMma<N, S>::MINB)
         const size_t base = (size_t)(w0 + e) * 4 * NP + n;
 #pragma unroll
         for (int x = 0; x < 4; ++x) {
-          const S v = x == 0 ? S(accp[i] * R(kap)) : S(accu[x - 1][i] * R(irho));
+          const S v = x == 0 ? S(accp[i] * R(kap)) + frc_at<S>(E, HW_TET, base)
+                             : S(accu[x - 1][i] * R(irho));
           const S qv = qe[x * NPK];
           if (lsrk) {
             const S r = S(E.a) * re[x * NPK] + S(E.dt) * v;
@@ -425,7 +426,8 @@ __global__ void __launch_bounds__(TetMma<N, S>::NTH, TetMma<N, S>::MINB)
       const size_t base = (size_t)sk[e] * 4 * NP + n;
       const S* qe = sq + e * EQ + n;
       const S* re = sres + e * EQ + n;
-      epilogue_s<S>(E, HW_TET, base, S(accp[i] * kap), qe[0], re[0]);
+      epilogue_s<S>(E, HW_TET, base, S(accp[i] * kap) + frc_at<S>(E, HW_TET, base), qe[0],
+                    re[0]);
 #pragma unroll
       for (int x = 0; x < 3; ++x)
         epilogue_s<S>(E, HW_TET, base + (1 + x) * NP, S(accu[x][i] * irho), qe[(1 + x) * NPK],

@@ -165,6 +165,7 @@ class Discretization:
     def rhs_device(self, q, out=None, subset=None):
         """Device RHS: q, out dicts of CUDA tensors (no host copies)."""
         dm = self.device_mesh
+        self.clear_forcing()          # compute_rhs adds the forcing itself
         dm.set_traces(0, None)        # hw_rhs fills trace set 0 with q's traces
         out = out if out is not None else self.empty_state()
         sub = nat.subset(subset) if subset is not None else None
@@ -304,16 +305,86 @@ class Discretization:
             self._cub[key] = (rule.weights, self._basis_values(t, rule.collapsed), x, J)
         return self._cub[key]
 
-    def _add_forcing(self, out, time):
-        for t in self.types:
+    def _forcing_ops(self, t):
+        """Device operands of hw_forcing for type t, built once: B = [invM_ref]
+        V^T diag(w) (Np, nq), scale = J (sqrt(J) wedge) at the cubature
+        points (K, nq), the per-node mass inverse (K, Np), and the cubature
+        points themselves for device-evaluated forcing (hybridwave/dg.py:
+        177-188, 479-490, 508-515)."""
+        cache = self.__dict__.setdefault("_frc_ops", {})
+        if t not in cache:
             w, V, x, J = self._cubature(t, "cub")
-            f = np.asarray(self.forcing(x, time))
+            B = V.T * w[None, :]
+            if t == "tet":
+                B = self.ops[t].invM_ref @ B
             scale = np.sqrt(J) if t == "wedge" else J
-            R = np.zeros((self.n_elems[t], FIELDS, self.ops[t].Np))
-            R[:, 0] = (f * scale * w[None, :]) @ V
-            dm = self.apply_mass_inverse(t, R)
-            dm[:, 0] *= self.mesh.materials[t][:, 1][:, None]
-            out[t] += torch.as_tensor(dm, dtype=self.dtype, device=out[t].device)
+            d, Np = self.data[t], self.ops[t].Np
+            if t == "hex":
+                nodefac = 1.0 / (d.w3[None, :] * d.J)
+            elif t == "tet":
+                nodefac = np.repeat(1.0 / d.J[:, :1], Np, axis=1)
+            elif t == "wedge":
+                nodefac = np.ones((self.n_elems[t], Np))
+            else:
+                nodefac = 1.0 / d.J
+            dev = lambda a: torch.as_tensor(np.ascontiguousarray(a), dtype=torch.float64,
+                                            device=self.device)
+            cache[t] = {"B": dev(B), "scale": dev(scale), "nodefac": dev(nodefac),
+                        "x": x, "x_dev": None, "nq": int(B.shape[1])}
+        return cache[t]
+
+    def forcing_values(self, t, time):
+        """The forcing callback at type t's cubature points as a (K, nq) fp64
+        CUDA tensor.  A callback with ``on_device = True`` is called with the
+        points as a CUDA tensor (no host work); otherwise with numpy points,
+        as in the reference, and the values are copied to the device."""
+        op = self._forcing_ops(t)
+        if getattr(self.forcing, "on_device", False):
+            if op["x_dev"] is None:
+                op["x_dev"] = torch.as_tensor(op["x"], dtype=torch.float64, device=self.device)
+            f = self.forcing(op["x_dev"], time)
+            return torch.as_tensor(f, dtype=torch.float64, device=self.device).contiguous()
+        f = np.ascontiguousarray(np.asarray(self.forcing(op["x"], time), dtype=np.float64))
+        return torch.as_tensor(f).to(self.device, non_blocking=False)
+
+    def forcing_buffer(self):
+        if getattr(self, "_frc_buf", None) is None:
+            self._frc_buf = self.zeros_state()
+        return self._frc_buf
+
+    def set_forcing(self, time):
+        """Fill the forcing buffer with kappa M^-1 (forcing integral) at `time`
+        (hw_forcing) and point the mesh's frc slots at it: the next
+        hw_rhs / hw_lsrk_stage / hw_ab_step add it to dp/dtau in their
+        epilogues.  Returns the buffer dict."""
+        dm, L, st = self.device_mesh, nat.lib(), self.stream_ptr()
+        buf = self.forcing_buffer()
+        keep = []
+        for t in self.types:
+            op = self._forcing_ops(t)
+            f = self.forcing_values(t, time)
+            keep.append(f)
+            nat.check(L.hw_forcing(dm.struct, TYPE_ID[t], f.data_ptr(), op["B"].data_ptr(),
+                                   op["scale"].data_ptr(), op["nodefac"].data_ptr(), op["nq"],
+                                   1.0, buf[t].data_ptr(), 0.0, None, 1, st))
+            dm.struct.frc[TYPE_ID[t]] = buf[t].data_ptr()
+        self._frc_keep = keep           # alive until the kernels ran
+        return buf
+
+    def clear_forcing(self):
+        if self._dev is not None:
+            for i in range(4):
+                self._dev.struct.frc[i] = None
+
+    def _add_forcing(self, out, time):
+        """out (device dict) += the forcing term at `time`, on the device."""
+        dm, L, st = self.device_mesh, nat.lib(), self.stream_ptr()
+        for t in self.types:
+            op = self._forcing_ops(t)
+            f = self.forcing_values(t, time)
+            nat.check(L.hw_forcing(dm.struct, TYPE_ID[t], f.data_ptr(), op["B"].data_ptr(),
+                                   op["scale"].data_ptr(), op["nodefac"].data_ptr(), op["nq"],
+                                   1.0, out[t].data_ptr(), 0.0, None, 0, st))
 
     def project(self, fields_fn, time=0.0):
         """L2 projection of callable fields (dg.py:521-548); host numpy."""
@@ -346,19 +417,41 @@ class Discretization:
         return vals
 
     def l2_error(self, state, exact_fn, time=0.0):
-        """Over-integrated L2 errors {p, u, total} (dg.py:558-572)."""
-        tot = {"p": 0.0, "u": 0.0}
+        """Over-integrated L2 errors {p, u, total} (hybridwave/dg.py:558-572),
+        on the device: the state is evaluated at the degree-(N+2) cubature
+        points by a matmul with the stored basis values, the exact solution
+        is evaluated there (on the device when ``exact_fn.on_device``), and
+        the weighted squares are reduced with one host read at the end.
+        Host arrays or CUDA tensors in."""
+        dev = self.device
+        num_p = torch.zeros((), dtype=torch.float64, device=dev)
+        num_u = torch.zeros((), dtype=torch.float64, device=dev)
         for t in self.types:
             w, V, x, J = self._cubature(t, "over")
-            num = self.eval_at(t, state[t])
-            ex = np.moveaxis(np.asarray(exact_fn(x, time)), -1, 1)
-            d2 = (num - ex) ** 2
-            wJ = w[None, :] * J
-            tot["p"] += float(np.sum(d2[:, 0] * wJ))
-            tot["u"] += float(np.sum(d2[:, 1:] * wJ[:, None, :]))
-        out = {k: np.sqrt(v) for k, v in tot.items()}
-        out["total"] = np.sqrt(tot["p"] + tot["u"])
-        return out
+            c = self.__dict__.setdefault("_l2_ops", {})
+            if t not in c:
+                Vd = torch.as_tensor(V, dtype=torch.float64, device=dev)
+                wJ = torch.as_tensor(w[None, :] * J, dtype=torch.float64, device=dev)
+                isj = (torch.as_tensor(1.0 / np.sqrt(J), dtype=torch.float64, device=dev)
+                       if t == "wedge" else None)
+                c[t] = (Vd, wJ, isj)
+            Vd, wJ, isj = c[t]
+            s_ = state[t]
+            s_ = (s_ if isinstance(s_, torch.Tensor)
+                  else torch.as_tensor(np.asarray(s_))).to(dev, torch.float64)
+            vals = s_ @ Vd.T                                     # (K, 4, nq)
+            if isj is not None:
+                vals = vals * isj[:, None, :]
+            if getattr(exact_fn, "on_device", False):
+                ex = exact_fn(torch.as_tensor(x, dtype=torch.float64, device=dev), time)
+            else:
+                ex = torch.as_tensor(np.asarray(exact_fn(x, time)), dtype=torch.float64)
+            ex = ex.to(dev).movedim(-1, 1)
+            d2 = (vals - ex) ** 2
+            num_p = num_p + (d2[:, 0] * wJ).sum()
+            num_u = num_u + (d2[:, 1:] * wJ[:, None, :]).sum()
+        p_, u_ = (float(v) for v in torch.stack([num_p, num_u]).cpu())
+        return {"p": np.sqrt(p_), "u": np.sqrt(u_), "total": np.sqrt(p_ + u_)}
 
     def state_to_vector(self, state):
         return np.concatenate([_host(state[t]).ravel() for t in self.types])

@@ -72,59 +72,7 @@ def _export(disc, q, host, out=None):
 
 def _no_forcing(disc):
     if disc.forcing is not None:
-        raise NotImplementedError("the fused device time loops do not take a forcing "
-                                  "callback; use compute_rhs + ab3_step")
-
-
-def _forced_rhs(disc, q, time):
-    """Device RHS plus the forcing residual (host callback at the cubature
-    points, hybridwave/dg.py:497-515), device dict."""
-    out = disc.rhs_device(q)
-    disc._add_forcing(out, time)
-    return out
-
-
-def _single_rate_forced(disc, state, dt, T_final, callback, out):
-    """single_rate_run with a forcing callback: unfused RHS (hw_rhs) + host
-    forcing + the AB3 update, in the reference's operation order."""
-    host = _is_host(state)
-    q = disc.to_device(state)
-    hist = []
-    time = 0.0
-    while time < T_final - 1e-14:
-        h = min(dt, T_final - time)
-        hist.insert(0, _forced_rhs(disc, q, time))
-        del hist[3:]
-        c = ab_coefficients(len(hist), h / dt)
-        new = {}
-        for t in disc.types:
-            acc = q[t].clone()
-            for ci, f in zip(c, hist):
-                acc += dt * float(ci) * f[t]
-            new[t] = acc
-        q = new
-        time += h
-        if callback is not None:
-            callback(time, _view(disc, q, host))
-    return _export(disc, q, host, out)
-
-
-def _lsrk_forced(disc, state, dt, T_final, callback, out):
-    host = _is_host(state)
-    q = disc.to_device(state)
-    res = disc.zeros_state()
-    time = 0.0
-    while time < T_final - 1e-14:
-        h = min(dt, T_final - time)
-        for a, b, c in zip(LSRK_A, LSRK_B, LSRK_C):
-            k = _forced_rhs(disc, q, time + c * h)
-            for t in disc.types:
-                res[t] = a * res[t] + h * k[t]
-                q[t] = q[t] + b * res[t]
-        time += h
-        if callback is not None:
-            callback(time, _view(disc, q, host))
-    return _export(disc, q, host, out)
+        raise NotImplementedError("lsrk_step takes no forcing callback; use lsrk_run")
 
 
 class Stepper:
@@ -155,25 +103,38 @@ class Stepper:
     def _f(self, s):
         return nat.fields(self.disc.slots(s))
 
-    def lsrk_step(self, h):
+    def lsrk_step(self, h, time=0.0):
+        """One LSRK(4,5) step from `time`.  With a forcing callback, each
+        stage's forcing term (at time + c_i h) is integrated on the device
+        (hw_forcing) and added in the stage kernel's epilogue."""
         L = nat.lib()
         st = self.disc.stream_ptr()
-        for a, b in zip(LSRK_A, LSRK_B):
+        forced = self.disc.forcing is not None
+        for a, b, c in zip(LSRK_A, LSRK_B, LSRK_C):
+            if forced:
+                self.disc.set_forcing(time + c * h)
             self._stage_traces()
             nat.check(L.hw_lsrk_stage(self.dm.struct, self._f(self.q), self._f(self.q2),
                                       self._f(self.res), a, b, h, None, st))
             self.q, self.q2 = self.q2, self.q
+        if forced:
+            self.disc.clear_forcing()
 
-    def ab_step(self, dt, theta=1.0):
+    def ab_step(self, dt, theta=1.0, time=0.0):
         nh = min(self.n_steps + 1, 3)
         c = ab_coefficients(nh, theta)
         c = list(c) + [0.0] * (3 - len(c))
         new = self.hist[2]
+        forced = self.disc.forcing is not None
+        if forced:
+            self.disc.set_forcing(time)
         self._stage_traces()
         nat.check(nat.lib().hw_ab_step(self.dm.struct, self._f(self.q), self._f(self.q2),
                                        self._f(new), self._f(self.hist[0]),
                                        self._f(self.hist[1]), nh, c[0], c[1], c[2], dt, None,
                                        self.disc.stream_ptr()))
+        if forced:
+            self.disc.clear_forcing()
         self.hist = [new, self.hist[0], self.hist[1]]
         self.q, self.q2 = self.q2, self.q
         self.n_steps += 1
@@ -194,16 +155,14 @@ def single_rate_run(disc, state, dt, T_final, callback=None, out=None, callback_
     """AB3 to T_final; the last step lands through the fractional
     coefficients (hybridwave/timeint.py:57-72).  out: optional host arrays
     the final state is written into; callback_every: call back every k-th
-    step (and after the last).  With a forcing callback the step is the
-    fused RHS + device forcing + update."""
-    if disc.forcing is not None:
-        return _single_rate_forced(disc, state, dt, T_final, callback, out)
+    step (and after the last).  A forcing callback is integrated on the
+    device each step and added in the fused kernel's epilogue."""
     host = _is_host(state)
     S = Stepper(disc, state, "ab")
     time, n = 0.0, 0
     while time < T_final - 1e-14:
         h = min(dt, T_final - time)
-        S.ab_step(dt, theta=h / dt)
+        S.ab_step(dt, theta=h / dt, time=time)
         time += h
         n += 1
         if _want_callback(callback, callback_every, n, time, T_final):
@@ -233,14 +192,12 @@ def lsrk_step(disc, q, res, dt, q_tmp=None):
 def lsrk_run(disc, state, dt, T_final, callback=None, out=None, callback_every=1):
     """Low-storage RK(4,5) to T_final with the single_rate_run signature;
     the last step is shortened to land on T_final."""
-    if disc.forcing is not None:
-        return _lsrk_forced(disc, state, dt, T_final, callback, out)
     host = _is_host(state)
     S = Stepper(disc, state, "lsrk")
     time, n = 0.0, 0
     while time < T_final - 1e-14:
         h = min(dt, T_final - time)
-        S.lsrk_step(h)
+        S.lsrk_step(h, time=time)
         time += h
         n += 1
         if _want_callback(callback, callback_every, n, time, T_final):

@@ -210,3 +210,45 @@ def test_second_device(native_lib):
     with torch.cuda.device(0):
         r = d.compute_rhs(st)
     assert rel_err(r, oracle.compute_rhs(d, st)) < 1e-12
+
+
+def _host_l2(d, state, exact_fn, time):
+    """hybridwave/dg.py:558-572 in numpy (the check for the device version)."""
+    tot = {"p": 0.0, "u": 0.0}
+    for t in d.types:
+        w, V, x, J = d._cubature(t, "over")
+        num = np.asarray(state[t]) @ V.T
+        if t == "wedge":
+            num = num / np.sqrt(J)[:, None, :]
+        ex = np.moveaxis(np.asarray(exact_fn(x, time)), -1, 1)
+        d2 = (num - ex) ** 2
+        wJ = w[None, :] * J
+        tot["p"] += float(np.sum(d2[:, 0] * wJ))
+        tot["u"] += float(np.sum(d2[:, 1:] * wJ[:, None, :]))
+    return {"p": np.sqrt(tot["p"]), "u": np.sqrt(tot["u"]),
+            "total": np.sqrt(tot["p"] + tot["u"])}
+
+
+def test_l2_error_on_device(native_lib):
+    """Device l2_error (host or device exact solution) = the host formula."""
+    import math
+    from paper_1507_02557_b200.app import cavity_fields
+    from paper_1507_02557_b200.timeint import lsrk_run
+    d = _disc("hybrid:3", 3, "GL")
+    st = d.project(cavity_fields, 0.0)
+    q = lsrk_run(d, d.to_device(st), 1e-3, 5e-3)
+    host = {t: v.cpu().numpy() for t, v in q.items()}
+    ref = _host_l2(d, host, cavity_fields, 5e-3)
+
+    def cav_dev(x, tau):
+        w = math.sqrt(3.0) * math.pi
+        s = [torch.sin(math.pi * x[..., i]) for i in range(3)]
+        c = [torch.cos(math.pi * x[..., i]) for i in range(3)]
+        g = -math.pi * math.sin(w * tau) / w
+        return torch.stack([s[0] * s[1] * s[2] * math.cos(w * tau), g * c[0] * s[1] * s[2],
+                            g * s[0] * c[1] * s[2], g * s[0] * s[1] * c[2]], dim=-1)
+    cav_dev.on_device = True
+    for got in (d.l2_error(q, cavity_fields, 5e-3), d.l2_error(q, cav_dev, 5e-3),
+                d.l2_error(host, cavity_fields, 5e-3)):
+        for k in ("p", "u", "total"):
+            assert abs(got[k] - ref[k]) <= 1e-12 * ref[k], (k, got[k], ref[k])
