@@ -83,10 +83,11 @@ typedef struct {
   void* tr_in[HW_NTYPES];
   void* tr_out[HW_NTYPES];
   hw_type_t t[HW_NTYPES];
-  /* Optional forcing term of dp/dtau per type, state layout (K, 4, Np),
-   * field 0 read (NULL: no forcing): hw_rhs / hw_lsrk_stage / hw_ab_step
-   * add it to the pressure RHS in their epilogue, so the published traces
-   * of the new state include it.  Filled by hw_forcing (assign = 1). */
+  /* Optional extra RHS term per type, state layout (K, 4, Np) (NULL:
+   * none): hw_rhs / hw_lsrk_stage / hw_ab_step add it to dU/dtau in their
+   * epilogue, so the published traces of the new state include it.  Filled
+   * by hw_forcing (assign = 1: the pressure forcing) and
+   * hw_wedge_face_correction (accumulating). */
   const void* frc[HW_NTYPES];
 } hw_mesh_t;
 
@@ -161,6 +162,22 @@ int hw_forcing(const hw_mesh_t* mesh, int elem_type, const double* f,
                const double* B, const double* scale, const double* nodefac,
                int nq, double alpha, void* out1, double beta, void* out2,
                int assign, void* stream);
+
+/* Tet faces across a triangle of a non-affine (LSC-DG) wedge: adds to the
+ * extra-RHS buffer `out` (state layout, all four fields; installed as
+ * mesh->frc) the difference between the reference's face-cubature surface
+ * integral (hybridwave/dg.py:326-354 at the stored 6(N+1)^2 points, wedge
+ * trace q/sqrt(J)) and the tet kernel's nodal lift of the unscaled wedge
+ * trace.  One row per (tet, face): idata [elem, face, nb_off[nfn]] (offsets
+ * of the wedge's published triangle trace at my face nodes in
+ * mesh->tr_in[HW_WEDGE], field 0), fdata [avg(rho c), 1/avg, n(3), Js,
+ * s-1 at the nq points, 1/J per node]; L (4, nq, nfn) nodal-to-cubature
+ * interpolants, P (4, Np, nq) = invM_ref Vf_f^T diag(w) (layout:
+ * paper_1507_02557_b200/device.py wedge_face_corrections). */
+int hw_wedge_face_correction(const hw_mesh_t* mesh, int elem_type, int n_pairs,
+                             const int32_t* idata, const double* fdata,
+                             const double* L, const double* P, int nq, int nfn,
+                             void* out, void* stream);
 
 /* Face-level halo exchange of partitioned runs (no reference counterpart:
  * the reference has no distributed path).  A

@@ -77,6 +77,9 @@ def lib():
         L.hw_forcing.argtypes = [P(HWMesh), c_int, c_void_p, c_void_p, c_void_p, c_void_p,
                                  c_int, c_double, c_void_p, c_double, c_void_p, c_int,
                                  c_void_p]
+        L.hw_wedge_face_correction.argtypes = [P(HWMesh), c_int, c_int, c_void_p, c_void_p,
+                                               c_void_p, c_void_p, c_int, c_int, c_void_p,
+                                               c_void_p]
         L.hw_halo_gather.argtypes = [P(HWMesh), c_void_p, c_int64, c_void_p, c_int64,
                                      c_void_p, c_void_p]
         L.hw_halo_scatter.argtypes = [P(HWMesh), c_void_p, c_int64, c_void_p, c_int64,
@@ -84,7 +87,7 @@ def lib():
         L.hw_last_error.restype = ctypes.c_char_p
         for name in ("hw_rhs", "hw_traces", "hw_lsrk_stage", "hw_ab_step", "hw_axpy3",
                      "hw_hist_push", "hw_halo_pack", "hw_halo_gather", "hw_halo_scatter",
-                     "hw_forcing", "hw_energy", "hw_version", "hw_supported_orders"):
+                     "hw_forcing", "hw_wedge_face_correction", "hw_energy", "hw_version", "hw_supported_orders"):
             getattr(L, name).restype = c_int
         L.hw_launch_count.restype = ctypes.c_longlong
         L.hw_launch_count.argtypes = []
@@ -93,8 +96,8 @@ def lib():
 
 
 EXPORTED_SYMBOLS = ("hw_rhs", "hw_traces", "hw_lsrk_stage", "hw_ab_step", "hw_axpy3", "hw_hist_push",
-                    "hw_halo_pack", "hw_halo_gather", "hw_halo_scatter", "hw_forcing", "hw_energy",
-                    "hw_last_error", "hw_version",
+                    "hw_halo_pack", "hw_halo_gather", "hw_halo_scatter", "hw_forcing",
+                    "hw_wedge_face_correction", "hw_energy", "hw_last_error", "hw_version",
                     "hw_supported_orders", "hw_launch_count")
 
 

@@ -532,6 +532,65 @@ __global__ void forcing_kernel(const double* __restrict__ f, const double* __res
   }
 }
 
+// Tet faces across a non-affine wedge's triangle (device.wedge_face_
+// corrections): one block per (tet, face) pair adds the lift of the flux of
+// delta = (L nb) * (s - 1) at the reference's face cubature points to the
+// extra-RHS buffer `out` (state layout, all four fields).  nb: the wedge's
+// published (unscaled) triangle trace at my face nodes.
+template <typename R>
+__global__ void wedge_face_corr_kernel(const R* __restrict__ trw, int nfp_w,
+                                       const R* __restrict__ mat, double pen, int np, int nfn,
+                                       int nq, const int* __restrict__ idata,
+                                       const double* __restrict__ fdata,
+                                       const double* __restrict__ Lall,
+                                       const double* __restrict__ Pall, R* __restrict__ out) {
+  extern __shared__ double wsm[];
+  double* nb = wsm;                 // [4][nfn]
+  double* dfp = nb + 4 * nfn;       // [nq]
+  double* dfu = dfp + nq;           // [nq]
+  const int* ir = idata + (size_t)blockIdx.x * (2 + nfn);
+  const double* fr = fdata + (size_t)blockIdx.x * (6 + nq + np);
+  const int k = ir[0], f = ir[1];
+  for (int i = threadIdx.x; i < 4 * nfn; i += blockDim.x) {
+    const int c = i / nfn, jj = i - c * nfn;
+    nb[i] = (double)trw[(size_t)ir[2 + jj] + (size_t)c * nfp_w];
+  }
+  __syncthreads();
+  const double tp = pen * fr[1], tu = pen * fr[0];
+  const double n0 = fr[2], n1 = fr[3], n2 = fr[4], js = fr[5];
+  const double* sm1 = fr + 6;
+  const double* L = Lall + (size_t)f * nq * nfn;
+  for (int i = threadIdx.x; i < nq; i += blockDim.x) {
+    double d[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int jj = 0; jj < nfn; ++jj) {
+      const double l = L[i * nfn + jj];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) d[c] += l * nb[c * nfn + jj];
+    }
+    const double s = sm1[i];
+    const double dp = d[0] * s, dun = (n0 * d[1] + n1 * d[2] + n2 * d[3]) * s;
+    dfp[i] = 0.5 * tp * dp - 0.5 * dun;
+    dfu[i] = 0.5 * tu * dun - 0.5 * dp;
+  }
+  __syncthreads();
+  const double* P = Pall + (size_t)f * np * nq;
+  const double kap = (double)mat[(size_t)k * 4], irho = (double)mat[(size_t)k * 4 + 1];
+  for (int n = threadIdx.x; n < np; n += blockDim.x) {
+    double sp = 0.0, su = 0.0;
+    for (int i = 0; i < nq; ++i) {
+      const double pv = P[n * nq + i];
+      sp += pv * dfp[i];
+      su += pv * dfu[i];
+    }
+    const double fac = js * fr[6 + nq + n];
+    R* o = out + (size_t)k * 4 * np + n;
+    atomicAdd(o, R(kap * fac * sp));
+    atomicAdd(o + np, R(irho * fac * n0 * su));
+    atomicAdd(o + 2 * np, R(irho * fac * n1 * su));
+    atomicAdd(o + 3 * np, R(irho * fac * n2 * su));
+  }
+}
+
 // face-level halo: buf[c * n + i] = src[off[i] + c * stride] (gather) and
 // dst[off[i] + c * stride] = buf[c * n + i] (scatter), c = 0..3 fields
 template <typename R>
@@ -829,6 +888,30 @@ int hw_forcing(const hw_mesh_t* mesh, int elem_type, const double* f, const doub
                                              alpha, (float*)out1, beta, (float*)out2,
                                              assign);
   return check_launch("forcing_kernel");
+}
+
+int hw_wedge_face_correction(const hw_mesh_t* mesh, int elem_type, int n_pairs,
+                             const int32_t* idata, const double* fdata, const double* L,
+                             const double* P, int nq, int nfn, void* out, void* stream) {
+  HW_DEVICE_GUARD(mesh);
+  if (n_pairs <= 0) return 0;
+  if (elem_type != HW_TET) return fail("hw_wedge_face_correction: tets only");
+  if (!mesh->tr_in[HW_WEDGE]) return fail("hw_wedge_face_correction: no wedge traces");
+  const int np = np_of(elem_type, mesh->N), nfp_w = [&] {
+    const int N = mesh->N, nfn_ = (N + 1) * (N + 2) / 2, nfq = (N + 1) * (N + 1);
+    return 2 * nfn_ + 3 * nfq;
+  }();
+  const size_t smem = sizeof(double) * (4 * nfn + 2 * nq);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (mesh->dtype == HW_F64)
+    wedge_face_corr_kernel<double><<<n_pairs, 128, smem, st>>>(
+        (const double*)mesh->tr_in[HW_WEDGE], nfp_w, (const double*)mesh->t[elem_type].mat,
+        mesh->penalty_scale, np, nfn, nq, idata, fdata, L, P, (double*)out);
+  else
+    wedge_face_corr_kernel<float><<<n_pairs, 128, smem, st>>>(
+        (const float*)mesh->tr_in[HW_WEDGE], nfp_w, (const float*)mesh->t[elem_type].mat,
+        mesh->penalty_scale, np, nfn, nq, idata, fdata, L, P, (float*)out);
+  return check_launch("wedge_face_corr_kernel");
 }
 
 int hw_energy(const hw_mesh_t* mesh, const hw_fields_t* q, double* out, void* stream) {

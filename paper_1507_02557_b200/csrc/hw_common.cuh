@@ -49,10 +49,10 @@ struct Epi {
   void* qout[HW_NTYPES];       // advanced state
   const void* h1[HW_NTYPES];
   const void* h2[HW_NTYPES];
-  const void* frc[HW_NTYPES];  // forcing term of dp/dtau (state layout), or NULL
+  const void* frc[HW_NTYPES];  // extra RHS term (state layout: forcing, face corrections)
 };
 
-// forcing term of dp/dtau at the field-0 index `base` (0 without forcing)
+// extra RHS term at the flat state index `base` (0 without one)
 template <typename S>
 __device__ __forceinline__ S frc_at(const Epi& E, int t, size_t base) {
   return E.frc[t] ? ((const S*)E.frc[t])[base] : S(0);

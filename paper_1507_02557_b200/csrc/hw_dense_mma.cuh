@@ -441,7 +441,9 @@ __device__ __forceinline__ void dense_mma_body(const hw_mesh_t& M, const hw_fiel
         const R irho = R(smat[e * 4 + 1]);
 #pragma unroll
         for (int x = 0; x < 3; ++x)
-          qe[(1 + x) * L::QF] = epilogue_q<S>(E, T, base + (1 + x) * NP, S(acc[x][i] * irho),
+          qe[(1 + x) * L::QF] = epilogue_q<S>(E, T, base + (1 + x) * NP,
+                                              S(acc[x][i] * irho) +
+                                                  frc_at<S>(E, T, base + (1 + x) * NP),
                                               qe[(1 + x) * L::QF], re[(1 + x) * L::QF]);
       };
       if (L::SPLIT) {

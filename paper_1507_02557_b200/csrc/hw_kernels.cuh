@@ -768,7 +768,7 @@ __global__ void __launch_bounds__(NT) dense_kernel(hw_mesh_t M, hw_fields_t Q, E
     const R* re = sm + L::SRES + e * 4 * NP + n;
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
-      const R v = acc[s][c] * (c == 0 ? kap : irho) + (c == 0 ? frc_at<R>(E, T, base) : R(0));
+      const R v = acc[s][c] * (c == 0 ? kap : irho) + frc_at<R>(E, T, base + c * NP);
       const R qn = epilogue_q<R>(E, T, base + c * NP, v, qe[c * NP], re[c * NP]);
       if (T != HW_TET) qe[c * NP] = qn;    // new state, for the published traces
     }
@@ -1139,8 +1139,7 @@ __global__ void HW_HEX_BOUNDS hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi E,
     // slope over the residual row), written back by bulk stores below
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
-      const R v = acc[s][c] * (c == 0 ? kap : irho) +
-                  (c == 0 ? frc_at<R>(E, HW_HEX, base) : R(0));
+      const R v = acc[s][c] * (c == 0 ? kap : irho) + frc_at<R>(E, HW_HEX, base + c * NP);
       const R qv = qe[c * NP];
       if (lsrk) {
         const R r = R(E.a) * re[c * NP] + R(E.dt) * v;

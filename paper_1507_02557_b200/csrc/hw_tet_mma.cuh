@@ -380,8 +380,8 @@ __global__ void __launch_bounds__(TetMma<N, S>::NTH, TetMma<N, S>::MINB)
         const size_t base = (size_t)(w0 + e) * 4 * NP + n;
 #pragma unroll
         for (int x = 0; x < 4; ++x) {
-          const S v = x == 0 ? S(accp[i] * R(kap)) + frc_at<S>(E, HW_TET, base)
-                             : S(accu[x - 1][i] * R(irho));
+          const S v = (x == 0 ? S(accp[i] * R(kap)) : S(accu[x - 1][i] * R(irho))) +
+                      frc_at<S>(E, HW_TET, base + x * NP);
           const S qv = qe[x * NPK];
           if (lsrk) {
             const S r = S(E.a) * re[x * NPK] + S(E.dt) * v;
@@ -430,7 +430,9 @@ __global__ void __launch_bounds__(TetMma<N, S>::NTH, TetMma<N, S>::MINB)
                     re[0]);
 #pragma unroll
       for (int x = 0; x < 3; ++x)
-        epilogue_s<S>(E, HW_TET, base + (1 + x) * NP, S(accu[x][i] * irho), qe[(1 + x) * NPK],
+        epilogue_s<S>(E, HW_TET, base + (1 + x) * NP,
+                      S(accu[x][i] * irho) + frc_at<S>(E, HW_TET, base + (1 + x) * NP),
+                      qe[(1 + x) * NPK],
                       re[(1 + x) * NPK]);
     }
   }

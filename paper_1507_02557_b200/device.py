@@ -33,18 +33,16 @@ _INTERIOR_ABC = {"tet": np.array([[-0.5, -0.5, -0.5]]), "wedge": np.array([[0.0,
 def _affine_check(disc, t, verts):
     """Non-affine wedges run the cubature form of the scalar kernel
     (wedge_cubature_ops); their triangle faces are integrated at the
-    reference's face cubature, which the device reproduces exactly only when
-    the neighbour across the triangle is a wedge too (or the boundary): a
-    tet or pyramid there would need its own face cubature."""
+    reference's face cubature.  A tet or pyramid across such a triangle gets
+    the matching correction of its nodal lift (wedge_face_corrections)."""
     from .refelem import affine_mask
     if t != "wedge" or len(verts) == 0 or affine_mask(t, verts, tol=1e-10).all():
         return False
     nb = disc.mesh.nbr["wedge"][:, :2, 0]
-    bad = (nb >= 0) & (nb != 1)
-    if bad.any():
+    if np.any(nb == 2):
         raise NotImplementedError(
-            f"non-affine wedges with {int(bad.sum())} triangle faces shared with tets or "
-            "pyramids (DESIGN.md, scope)")
+            f"non-affine wedges with {int(np.sum(nb == 2))} triangle faces shared with "
+            "pyramids (no generator or test mesh has them; tets are supported, DESIGN.md)")
     return True
 
 
@@ -84,7 +82,11 @@ def wedge_cubature_ops(disc, dops):
         ok = ~bnd[flat] & (g >= 0) & (g < K * tot)
         gc = np.where(ok, g, 0)
         tri[:, f, :, 0] = d.invsqrtJ_face[:, rs]
-        tri[:, f, :, 1] = np.where(ok, d.invsqrtJ_face[gc // tot, gc % tot], 0.0)
+        # the neighbour's 1/sqrt(J): a wedge's at the coincident point; a tet
+        # or pyramid trace carries no sqrt(J) factor
+        other = ~bnd[flat] & ~ok
+        tri[:, f, :, 1] = np.where(ok, d.invsqrtJ_face[gc // tot, gc % tot],
+                                   np.where(other, 1.0, 0.0))
         tri[:, f, :, 2] = d.wJs[:, rs] * d.invsqrtJ_face[:, rs]
     geo = np.concatenate([vol.reshape(K, -1), quad.reshape(K, -1), tri.reshape(K, -1)], axis=1)
     mats = [ops.V, ops.Dr3, ops.Ds3, ops.Dt3]
@@ -93,6 +95,94 @@ def wedge_cubature_ops(disc, dops):
     const = np.concatenate([np.stack([m.T for m in mats]).ravel(), np.stack(mats).ravel(),
                             Lq.ravel(), Vf.ravel()])
     return {8: geo, 9: const}
+
+
+def wedge_face_corrections(disc, pack):
+    """Tets and pyramids across a triangle face of a non-affine wedge: the
+    wedge trace there is q_w / sqrt(J_w), not a polynomial, so the nodal
+    face lift of the tet / pyramid kernels (exact for polynomial fluxes) is
+    replaced by the reference's face cubature (hybridwave/dg.py:326-354 at
+    the stored 6(N+1)^2 points).  The flux is linear in the neighbour trace,
+    so the correction is the lift of the flux of
+        delta = (L nb) * (s - 1),   s = the wedge's 1/sqrt(J) at the point,
+    nb = the wedge's published (unscaled) triangle trace at my face nodes,
+    L = my nodal-to-cubature interpolant:
+        dfp = tau_p/2 delta_p - n.delta_u / 2,  dfu = tau_u/2 n.delta_u - delta_p / 2,
+        drhs = nodefac * Js * P_f [dfp, n dfu]   (kappa, 1/rho in the kernel),
+    P_f = [invM_ref] Vf_f^T diag(w_f).  Returns {t: arrays} for the
+    hw_wedge_face_correction kernel, empty when no such face exists."""
+    from .operators import _tri_lagrange
+    out = {}
+    if "wedge" not in disc.types or 8 not in pack["types"]["wedge"]["op"]:
+        return out
+    N = disc.N
+    wd = disc.data["wedge"]
+    wops = disc.ops["wedge"]
+    wtot = int(wops.face_offsets[-1])
+    wbase = disc.trace_bases["wedge"]
+    gidx = np.asarray(disc.gather_idx)
+    nfp_w = pack["types"]["wedge"]["nfp"]
+    for t, tid_faces in (("tet", range(4)),):
+        if t not in disc.types:
+            continue
+        nbr = disc.mesh.nbr[t]
+        P_ = pack["types"][t]
+        dops = P_["dops"]
+        ops = disc.ops[t]
+        d = disc.data[t]
+        K, Np = disc.n_elems[t], ops.Np
+        nfn = len(dops["tri2d"])
+        roffs = np.asarray(ops.face_offsets)
+        tot = int(roffs[-1])
+        base = disc.trace_bases[t]
+        gi = P_["iop"][1].reshape(K, -1)
+        doffs = np.asarray(dops["face_offsets"])
+        rows_i, rows_f = [], []
+        nq = None
+        Ls, Ps = [], []
+        for f in range(nbr.shape[1]):
+            if f not in tid_faces:
+                Ls.append(None)
+                Ps.append(None)
+                continue
+            pts = ops.face_pts2d[f]
+            nq = len(pts)
+            Ls.append(_tri_lagrange(dops["tri2d"], pts, N))
+            Pf = ops.Vf[roffs[f]:roffs[f + 1]].T * ops.face_wts[f][None, :]
+            if t == "tet":
+                Pf = ops.invM_ref @ Pf
+            Ps.append(Pf)
+            sel = np.flatnonzero(nbr[:, f, 0] == 1)          # wedge neighbours
+            if len(sel) == 0:
+                continue
+            flat = base + sel[:, None] * tot + np.arange(roffs[f], roffs[f + 1])[None, :]
+            g = gidx[flat] - wbase
+            s_ = wd.invsqrtJ_face[g // wtot, g % wtot]          # (n, nq)
+            if np.abs(s_ - 1.0).max() == 0.0:
+                continue
+            gv = gi[sel][:, doffs[f]:doffs[f] + nfn] if t == "pyramid" else \
+                gi[sel].reshape(len(sel), 4, nfn)[:, f, :]
+            nb_off = (-gv.astype(np.int64) - 4) // 2 if t == "tet" else gv.astype(np.int64)
+            rec = P_["geo"][sel]
+            fb = 9 + 6 * f
+            js = d.wJs[sel, roffs[f]] / ops.face_wts[f][0]
+            nodefac = (np.repeat(1.0 / d.J[sel, :1], Np, axis=1) if t == "tet"
+                       else 1.0 / d.J[sel])
+            rows_i.append(np.column_stack([sel, np.full(len(sel), f), nb_off]))
+            rows_f.append(np.column_stack([rec[:, fb + 4], rec[:, fb + 5], rec[:, fb:fb + 3],
+                                           js, s_ - 1.0, nodefac]))
+        if not rows_i:
+            continue
+        if int(np.max(np.concatenate(rows_i)[:, 2:])) >= 2 ** 31:
+            raise ValueError("wedge trace offsets exceed int32")
+        zL = np.zeros((nq, nfn))
+        zP = np.zeros((Np, nq))
+        out[t] = {"idata": np.concatenate(rows_i).astype(np.int32),
+                  "fdata": np.concatenate(rows_f).astype(np.float64),
+                  "L": np.stack([x if x is not None else zL for x in Ls]),
+                  "P": np.stack([x if x is not None else zP for x in Ps]),
+                  "nq": nq, "nfn": nfn, "nfp_w": nfp_w}
+    return out
 
 
 def face_impedance_avg(mesh, t):
@@ -499,6 +589,16 @@ class DeviceMesh:
                                                              dtype=dtype, device=self.device)
         self.struct = S
         self.set_traces(0, None)
+        # tet faces across non-affine wedge triangles (face-cubature correction)
+        self.corr = {}
+        for t, c in wedge_face_corrections(disc, pack).items():
+            self.corr[t] = {"n": int(len(c["idata"])), "nq": c["nq"], "nfn": c["nfn"],
+                            "idata": torch.as_tensor(c["idata"], device=self.device),
+                            "fdata": torch.as_tensor(c["fdata"], device=self.device),
+                            "L": torch.as_tensor(c["L"], device=self.device),
+                            "P": torch.as_tensor(c["P"], device=self.device),
+                            "elems": torch.as_tensor(np.unique(c["idata"][:, 0]).astype(np.int64),
+                                                     device=self.device)}
         orders = nat.lib().hw_supported_orders()
         if not (orders >> disc.N) & 1:
             raise ValueError(f"order N={disc.N} not compiled into {nat.LIB_NAME}")

@@ -167,10 +167,14 @@ class Discretization:
         dm = self.device_mesh
         self.clear_forcing()          # compute_rhs adds the forcing itself
         dm.set_traces(0, None)        # hw_rhs fills trace set 0 with q's traces
+        if dm.corr:                   # the corrections read the traces of q
+            dm.compute_traces(nat.fields(self.slots(q)), 0, self.stream_ptr())
+            self.apply_corrections()
         out = out if out is not None else self.empty_state()
         sub = nat.subset(subset) if subset is not None else None
         nat.check(nat.lib().hw_rhs(dm.struct, nat.fields(self.slots(q)),
                                    nat.fields(self.slots(out)), sub, self.stream_ptr()))
+        self.clear_forcing()
         return out
 
     # ------------------------------------------------------------ public API
@@ -375,6 +379,42 @@ class Discretization:
         if self._dev is not None:
             for i in range(4):
                 self._dev.struct.frc[i] = None
+
+    @property
+    def has_corrections(self):
+        return bool(self.device_mesh.corr)
+
+    def apply_corrections(self):
+        """Extra-RHS rows of the tets across non-affine wedge triangles: the
+        reference's face-cubature integral minus the kernels' nodal lift
+        (hw_wedge_face_correction) from the current input traces
+        (mesh->tr_in), installed in the mesh's frc slots (accumulates onto a
+        forcing term set just before)."""
+        dm, L, st = self.device_mesh, nat.lib(), self.stream_ptr()
+        if not dm.corr:
+            return
+        buf = self.forcing_buffer()
+        for t, c in dm.corr.items():
+            if dm.struct.frc[TYPE_ID[t]] is None:     # no forcing term: fresh rows
+                buf[t].index_fill_(0, c["elems"], 0.0)
+            nat.check(L.hw_wedge_face_correction(dm.struct, TYPE_ID[t], c["n"],
+                                                 c["idata"].data_ptr(), c["fdata"].data_ptr(),
+                                                 c["L"].data_ptr(), c["P"].data_ptr(), c["nq"],
+                                                 c["nfn"], buf[t].data_ptr(), st))
+            dm.struct.frc[TYPE_ID[t]] = buf[t].data_ptr()
+
+    def prepare_stage(self, time):
+        """Extra RHS of the next fused stage: forcing at `time` (if any), then
+        the face corrections.  Call after the stage's input traces are set.
+        Returns True when the mesh's frc slots were installed."""
+        on = False
+        if self.forcing is not None:
+            self.set_forcing(time)
+            on = True
+        if self._dev is not None and self._dev.corr:
+            self.apply_corrections()
+            on = True
+        return on
 
     def _add_forcing(self, out, time):
         """out (device dict) += the forcing term at `time`, on the device."""

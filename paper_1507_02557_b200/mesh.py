@@ -465,3 +465,32 @@ def mesh_volume(mesh, N=2):
         rule = element_rule(t, N)
         vol[t] = jacobian_det_fast(t, mesh.element_vertices(t), rule.collapsed) @ rule.weights
     return float(sum(v.sum() for v in vol.values()))
+
+
+def wedge_tet_columns_mesh(nx=4, ny=2, nz=2):
+    """Test mesh (not in the reference): nx x ny x nz cells of the unit box
+    whose x-columns alternate between wedge pairs and Kuhn tets, so wedge
+    triangle faces meet tet faces (the wedge triangles lie on the cells'
+    x-faces and their diagonals match the Kuhn split).  Jittering the
+    interior vertices makes those wedges non-affine."""
+    xs, ys, zs = (np.linspace(0.0, 1.0, n + 1) for n in (nx, ny, nz))
+    gx, gy, gz = np.meshgrid(xs, ys, zs, indexing="ij")
+    X = np.column_stack([gx.transpose(2, 1, 0).ravel(), gy.transpose(2, 1, 0).ravel(),
+                         gz.transpose(2, 1, 0).ravel()])
+
+    def vid(i, j, k):
+        return (k * (ny + 1) + j) * (nx + 1) + i
+
+    wed, tet = [], []
+    kuhn = _kuhn_local()
+    for k in range(nz):
+        for j in range(ny):
+            for i in range(nx):
+                c = np.array([vid(i, j, k), vid(i + 1, j, k), vid(i + 1, j + 1, k),
+                              vid(i, j + 1, k), vid(i, j, k + 1), vid(i + 1, j, k + 1),
+                              vid(i + 1, j + 1, k + 1), vid(i, j + 1, k + 1)])
+                if i % 2 == 0:
+                    wed.append(c[_WEDGE_LOCAL].reshape(-1, 6))
+                else:
+                    tet.append(_orient_tets(c[kuhn].reshape(-1, 4), X))
+    return HybridMesh(X, {"wedge": np.vstack(wed), "tet": np.vstack(tet)})

@@ -113,6 +113,9 @@ class PartStepper:
         self.disc = Discretization(part.mesh, N, formulation, dtype=dtype, device=device)
         d = self.disc
         dev = d.device
+        if d.device_mesh.corr:
+            raise NotImplementedError("partitioned runs of meshes with tets across non-affine "
+                                      "wedge triangles (single-GPU only)")
         self.S = Stepper(d, state_local, "lsrk")
         empty = torch.zeros(0, dtype=torch.int32, device=dev)
 
@@ -277,6 +280,9 @@ class PartMRAB:
         self.transport = transport
         self.disc = d = Discretization(part.mesh, N, formulation, dtype=dtype, device=device)
         dev = d.device
+        if d.device_mesh.corr:
+            raise NotImplementedError("partitioned runs of meshes with tets across non-affine "
+                                      "wedge triangles (single-GPU only)")
         self.L = L = int(n_levels)
         self.levels = {t: np.asarray(levels_local[t]) for t in d.types}
         self.q = d.to_device(state_local)

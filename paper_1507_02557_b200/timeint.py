@@ -109,15 +109,14 @@ class Stepper:
         (hw_forcing) and added in the stage kernel's epilogue."""
         L = nat.lib()
         st = self.disc.stream_ptr()
-        forced = self.disc.forcing is not None
+        extra = False
         for a, b, c in zip(LSRK_A, LSRK_B, LSRK_C):
-            if forced:
-                self.disc.set_forcing(time + c * h)
             self._stage_traces()
+            extra = self.disc.prepare_stage(time + c * h) or extra
             nat.check(L.hw_lsrk_stage(self.dm.struct, self._f(self.q), self._f(self.q2),
                                       self._f(self.res), a, b, h, None, st))
             self.q, self.q2 = self.q2, self.q
-        if forced:
+        if extra:
             self.disc.clear_forcing()
 
     def ab_step(self, dt, theta=1.0, time=0.0):
@@ -125,15 +124,13 @@ class Stepper:
         c = ab_coefficients(nh, theta)
         c = list(c) + [0.0] * (3 - len(c))
         new = self.hist[2]
-        forced = self.disc.forcing is not None
-        if forced:
-            self.disc.set_forcing(time)
         self._stage_traces()
+        extra = self.disc.prepare_stage(time)
         nat.check(nat.lib().hw_ab_step(self.dm.struct, self._f(self.q), self._f(self.q2),
                                        self._f(new), self._f(self.hist[0]),
                                        self._f(self.hist[1]), nh, c[0], c[1], c[2], dt, None,
                                        self.disc.stream_ptr()))
-        if forced:
+        if extra:
             self.disc.clear_forcing()
         self.hist = [new, self.hist[0], self.hist[1]]
         self.q, self.q2 = self.q2, self.q
@@ -182,10 +179,13 @@ def lsrk_step(disc, q, res, dt, q_tmp=None):
     for a, b in zip(LSRK_A, LSRK_B):
         dm.set_traces(tr, 1 - tr)
         tr = 1 - tr
+        if dm.corr:
+            disc.apply_corrections()
         nat.check(nat.lib().hw_lsrk_stage(dm.struct, nat.fields(disc.slots(q)),
                                           nat.fields(disc.slots(q_tmp)),
                                           nat.fields(disc.slots(res)), a, b, dt, None, st))
         q, q_tmp = q_tmp, q
+    disc.clear_forcing()
     return q
 
 
@@ -312,6 +312,8 @@ class MRABDriver:
             # of each stepping level (no trace publishing)
             dm.compute_traces(F(eff), 0, st, subset=self._trace_subs[tick])
             dm.set_traces(0, None)
+            if dm.corr:
+                disc.apply_corrections()
             for lev in stepping:
                 n_hist[lev] = min(n_hist[lev] + 1, 3)
                 steps[lev] += 1

@@ -334,7 +334,44 @@ def mrab_multilevel_fixtures():
     print("multi-level MRAB fixtures written")
 
 
+def wedge_tet_fixtures():
+    """Non-affine (jittered) wedges whose triangle faces meet tets: the
+    reference's RHS (face cubature on both sides) and 10 LSRK-45 steps.  The
+    mesh generator is the repo's (wedge_tet_columns_mesh); every number
+    below comes from the reference's HybridMesh / Discretization."""
+    sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+    from paper_1507_02557_b200.mesh import wedge_tet_columns_mesh
+    from hybridwave.mesh import HybridMesh
+    fd = {}
+    g = wedge_tet_columns_mesh(4, 2, 2)
+    rng = np.random.default_rng(21)
+    X = g.vertices.copy()
+    inner = np.all((X > 1e-9) & (X < 1 - 1e-9), axis=1)
+    X[inner] += 0.04 * rng.uniform(-1, 1, (inner.sum(), 3))
+    fd["X"] = X
+    for tag, N, form in [("n1_gl", 1, "GL"), ("n2_gl", 2, "GL"), ("n3_sem", 3, "SEM"),
+                         ("n3_gl", 3, "GL")]:
+        m = HybridMesh(X, {t: g.blocks[t].copy() for t in g.elem_types})
+        set_random_materials(m, 4)
+        d = Discretization(m, N, form)
+        rng = np.random.default_rng(N + 30)
+        st = {t: rng.standard_normal((d.n_elems[t], 4, d.ops[t].Np)) for t in d.types}
+        rhs = d.compute_rhs(st, 0.0)
+        for t in d.types:
+            fd[f"{tag}/rhs/{t}"] = rhs[t]
+        st0 = d.project(cavity_fields, 0.0)
+        dt = 0.5 * min(float(v.min()) for v in local_timesteps(d, 0.5).values())
+        lk = lsrk_run_ref(d, st0, dt, 10 * dt)
+        for t in d.types:
+            fd[f"{tag}/lsrk/{t}"] = lk[t]
+        fd[f"{tag}/dt"] = np.array(dt)
+    np.savez_compressed(os.path.join(HERE, "wedge_tet.npz"), **fd)
+    print("wedge/tet fixtures written")
+
+
 if __name__ == "__main__":
+    if sys.argv[1:] == ["wedge_tet"]:
+        sys.exit(wedge_tet_fixtures())
     if sys.argv[1:] == ["mrab_levels"]:
         sys.exit(mrab_multilevel_fixtures())
     if sys.argv[1:] == ["nonaffine"]:

@@ -84,10 +84,11 @@ def test_nonaffine_wedge_layout_matches_reference(tag, spec, N, form, seed):
     assert rel_err(oracle.compute_rhs(d, st), {"wedge": G[f"{tag}/rhs/wedge"]}) < 1e-12
 
 
-def test_nonaffine_wedge_next_to_tets_is_refused():
-    """A non-affine wedge whose triangle face touches a tet (or pyramid) has
-    no exact nodal-face representation on the tet side: refused, not wrong.
-    (The generator meshes put only wedges on wedge triangle faces.)"""
+def test_nonaffine_wedge_next_to_tets_gets_face_corrections():
+    """A non-affine wedge whose triangle face touches a tet: the tet side
+    gets the face-cubature correction rows (device.wedge_face_corrections);
+    an affine wedge needs none."""
+    from paper_1507_02557_b200.device import wedge_face_corrections
     from paper_1507_02557_b200.dg import Discretization
     from paper_1507_02557_b200.mesh import HybridMesh
     def mesh(x4):
@@ -97,6 +98,38 @@ def test_nonaffine_wedge_next_to_tets_is_refused():
                               "tet": np.array([[3, 5, 4, 6]])})
     m = mesh(1.2)
     assert 3 in m.nbr["wedge"][0, :2, 0]
-    with pytest.raises(NotImplementedError):
-        pack_mesh(Discretization(m, 2, "GL"))
-    pack_mesh(Discretization(mesh(1.0), 2, "GL"))   # affine: packs
+    d = Discretization(m, 2, "GL")
+    c = wedge_face_corrections(d, pack_mesh(d))
+    assert set(c) == {"tet"} and c["tet"]["idata"].shape[0] == 1
+    assert np.abs(c["tet"]["fdata"][:, 6:6 + c["tet"]["nq"]]).max() > 0   # s - 1 != 0
+    d1 = Discretization(mesh(1.0), 2, "GL")
+    assert wedge_face_corrections(d1, pack_mesh(d1)) == {}
+
+
+def test_wedge_tet_mesh_corrections_cover_every_shared_triangle():
+    from paper_1507_02557_b200.device import wedge_face_corrections
+    from paper_1507_02557_b200.dg import Discretization
+    from paper_1507_02557_b200.mesh import HybridMesh, wedge_tet_columns_mesh
+    g = wedge_tet_columns_mesh(4, 2, 2)
+    X = load_golden("wedge_tet")["X"]
+    d = Discretization(HybridMesh(X, g.blocks), 2, "GL")
+    c = wedge_face_corrections(d, pack_mesh(d))
+    shared = int(np.sum(d.mesh.nbr["tet"][:, :, 0] == 1))
+    assert c["tet"]["idata"].shape[0] == shared == 24
+
+
+def test_oracle_on_wedge_tet_mesh_matches_reference():
+    """The oracle on the jittered wedge/tet column mesh = the reference's RHS
+    (pins the oracle for the device's face-correction path)."""
+    from conftest import set_random_materials
+    from paper_1507_02557_b200.dg import Discretization
+    from paper_1507_02557_b200.mesh import HybridMesh, wedge_tet_columns_mesh
+    Gw = load_golden("wedge_tet")
+    g = wedge_tet_columns_mesh(4, 2, 2)
+    for tag, N, form in [("n1_gl", 1, "GL"), ("n3_sem", 3, "SEM")]:
+        m = HybridMesh(Gw["X"], g.blocks)
+        set_random_materials(m, 4)
+        d = Discretization(m, N, form, device="cpu")
+        rng = np.random.default_rng(N + 30)
+        st = {t: rng.standard_normal((d.n_elems[t], 4, d.ops[t].Np)) for t in d.types}
+        assert rel_err(oracle.compute_rhs(d, st), {t: Gw[f"{tag}/rhs/{t}"] for t in d.types}) < 1e-12
