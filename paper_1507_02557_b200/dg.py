@@ -384,7 +384,7 @@ class Discretization:
     def has_corrections(self):
         return bool(self.device_mesh.corr)
 
-    def apply_corrections(self):
+    def apply_corrections(self, after_forcing=False):
         """Extra-RHS rows of the tets across non-affine wedge triangles: the
         reference's face-cubature integral minus the kernels' nodal lift
         (hw_wedge_face_correction) from the current input traces
@@ -395,7 +395,7 @@ class Discretization:
             return
         buf = self.forcing_buffer()
         for t, c in dm.corr.items():
-            if dm.struct.frc[TYPE_ID[t]] is None:     # no forcing term: fresh rows
+            if not after_forcing:        # rows hold the last stage's values
                 buf[t].index_fill_(0, c["elems"], 0.0)
             nat.check(L.hw_wedge_face_correction(dm.struct, TYPE_ID[t], c["n"],
                                                  c["idata"].data_ptr(), c["fdata"].data_ptr(),
@@ -408,11 +408,12 @@ class Discretization:
         the face corrections.  Call after the stage's input traces are set.
         Returns True when the mesh's frc slots were installed."""
         on = False
+        self.clear_forcing()
         if self.forcing is not None:
             self.set_forcing(time)
             on = True
         if self._dev is not None and self._dev.corr:
-            self.apply_corrections()
+            self.apply_corrections(after_forcing=self.forcing is not None)
             on = True
         return on
 
