@@ -63,10 +63,8 @@ typedef struct {
   const void* op[10];
   const int32_t* iop[4];
   int32_t form;              /* HW_FORM_STRONG or HW_FORM_SKEW            */
-  int32_t flags;             /* HW_TYPE_ALL_AFFINE: every element affine  */
+  int32_t pad_;
 } hw_type_t;
-
-#define HW_TYPE_ALL_AFFINE 1
 
 typedef struct {
   int32_t N;

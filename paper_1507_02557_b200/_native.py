@@ -17,14 +17,13 @@ HW_F64, HW_F32 = 0, 1
 HW_FORM_STRONG, HW_FORM_SKEW = 0, 1
 HW_GL, HW_SEM = 0, 1
 HW_NBR_BOUNDARY = 0x200
-HW_TYPE_ALL_AFFINE = 1
 
 
 class HWType(ctypes.Structure):
     _fields_ = [("K", c_int64), ("geo", c_void_p), ("mat", c_void_p),
                 ("nbr_elem", c_void_p), ("nbr_code", c_void_p),
                 ("op", c_void_p * 10), ("iop", c_void_p * 4),
-                ("form", c_int32), ("flags", c_int32)]
+                ("form", c_int32), ("pad_", c_int32)]
 
 
 class HWMesh(ctypes.Structure):

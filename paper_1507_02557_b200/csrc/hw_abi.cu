@@ -92,17 +92,6 @@ struct DeviceGuard {
   DeviceGuard device_guard_(M);                                   \
   if (!device_guard_.ok) return fail("cannot make the mesh's device current")
 
-// HW_HEX_MMA=0 selects the scalar sum-factorised hex kernel for affine
-// meshes too (A/B checks); default: the DMMA tiles
-static bool hex_mma_on() {
-  static int v = -1;
-  if (v < 0) {
-    const char* s = getenv("HW_HEX_MMA");
-    v = (s && s[0] == '0') ? 0 : 1;
-  }
-  return v == 1;
-}
-
 static void subset_of(const hw_subset_t* sub, int t, int64_t K, const int32_t** list,
                       int64_t* n) {
   *list = nullptr;
@@ -327,14 +316,6 @@ static int launch_rhs_all(const hw_mesh_t& M, const hw_fields_t& Q, const Epi& E
         if (M.t[HW_HEX].form == HW_FORM_SKEW) {
           if ((rc = set_smem(hex_kernel<N, R, true>, L::BYTES))) return rc;
           hex_kernel<N, R, true><<<grid, HW_HEX_NT, L::BYTES, st>>>(M, Q, E, list, n);
-        } else if (hex_mma_on() && (M.t[HW_HEX].flags & HW_TYPE_ALL_AFFINE) &&
-                   4 * L::NP <= L::STG) {
-          // affine hexes: DMMA volume / lift tiles (the node sums need the
-          // staging area: N <= 5)
-          if constexpr (4 * L::NP <= L::STG) {
-            if ((rc = set_smem(hex_kernel<N, R, false, true>, L::BYTES))) return rc;
-            hex_kernel<N, R, false, true><<<grid, HW_HEX_NT, L::BYTES, st>>>(M, Q, E, list, n);
-          }
         } else {
           if ((rc = set_smem(hex_kernel<N, R, false>, L::BYTES))) return rc;
           hex_kernel<N, R, false><<<grid, HW_HEX_NT, L::BYTES, st>>>(M, Q, E, list, n);

@@ -834,16 +834,7 @@ __device__ __forceinline__ R hex_metric(const R* X, R r, R s, R t, R G[9]) {
 #else
 #define HW_HEX_BOUNDS __launch_bounds__(HW_HEX_NT)
 #endif
-// SK: skew form (testing hook).  MMA: every hex of the mesh is affine and
-// the form strong: the volume derivatives and the surface lift run as
-// tensor-core (DMMA) tiles, per direction c of the tensor grid
-//   DU_f,c = D (N1 x N1) . U_f viewed as (index along c) x (the other two),
-//   LIFT_f,c = [ve_0 ve_1] (N1 x 2) . [F_f,2c ; F_f,2c+1] (2 x face points),
-// combined with the constant metric in registers and accumulated per node
-// in shared memory (one direction after the other); the per-node loop then
-// only runs the update.  Shared-memory loads per node drop from the
-// 3 (N+1) x 4 of the scalar sum-factorised loop to a few B fragments.
-template <int N, typename R, bool SK = false, bool MMA = false>
+template <int N, typename R, bool SK = false>   // SK: skew form (testing hook)
 __global__ void HW_HEX_BOUNDS hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi E,
                                                  const int32_t* __restrict__ list,
                                                  int64_t nwork) {
@@ -990,7 +981,7 @@ __global__ void HW_HEX_BOUNDS hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi E,
 #pragma unroll
     for (int c = 0; c < 4; ++c) acc[s][c] = R(0);
     minv[s] = R(0);
-    if (!MMA && e < ne) {
+    if (e < ne) {
       const int ii = n / (N1 * N1), jj = (n / N1) % N1, kk = n % N1;
       R d[4][3];
 #pragma unroll
@@ -1110,100 +1101,17 @@ __global__ void HW_HEX_BOUNDS hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi E,
   }
   __syncthreads();
 
-  R* sacc = sm + L::SST;      // MMA path: [e][field][node] (staged values are dead)
-  if constexpr (MMA) {
-    static_assert(4 * NP <= L::STG, "MMA hex path keeps the node sums in the staging area");
-    constexpr int NN = N1 * N1, CT = (NN + 7) / 8, KS = (N1 + 3) / 4, NWH = NT / 32;
-    const int lane = tid & 31, warp = tid >> 5;
-    const int ar = lane >> 2, ak = lane & 3;
-    double aD[KS];
-#pragma unroll
-    for (int ks = 0; ks < KS; ++ks) {
-      const int k = ks * 4 + ak;
-      aD[ks] = (ar < N1 && k < N1) ? double(sD[ar * N1 + k]) : 0.0;
-    }
-    // lift rows: A[row][k = end] = ve[end][row] (GL) or the end selection (SEM)
-    const double aL = (ar < N1 && ak < 2)
-                          ? (sem ? (ar == (ak ? N : 0) ? 1.0 : 0.0) : double(sve[ak * N1 + ar]))
-                          : 0.0;
-    auto node = [](int dir, int l, int a, int b) {
-      return dir == 0 ? (l * N1 + a) * N1 + b : (dir == 1 ? (a * N1 + l) * N1 + b
-                                                          : (a * N1 + b) * N1 + l);
-    };
-#pragma unroll 1
-    for (int dir = 0; dir < 3; ++dir) {
-      for (int task = warp; task < ne * CT; task += NWH) {
-        const int e = task / CT, ct = task - e * CT;
-        const R* u = sq + e * 4 * NP;
-        const R* fl = sf + e * 4 * NFP;
-        const int bcol = ct * 8 + ar;                 // B fragment column of this lane
-        const bool bv = bcol < NN;
-        const int ba = bv ? bcol / N1 : 0, bb = bv ? bcol - ba * N1 : 0;
-        double dv[4][2], lv[4][2];
-#pragma unroll
-        for (int f = 0; f < 4; ++f) dv[f][0] = dv[f][1] = lv[f][0] = lv[f][1] = 0.0;
-#pragma unroll
-        for (int ks = 0; ks < KS; ++ks) {
-          const int l = ks * 4 + ak;
-          const bool ok = bv && l < N1;
-          const int nd = ok ? node(dir, l, ba, bb) : 0;
-#pragma unroll
-          for (int f = 0; f < 4; ++f)
-            dmma884(dv[f][0], dv[f][1], aD[ks], ok ? double(u[f * NP + nd]) : 0.0);
-        }
-        {   // lift: faces 2 dir (end 0) and 2 dir + 1 (end 1)
-          const int fc = 2 * dir + (ak & 1);
-          const int* cf = spc + 4 * fc;
-          const int i0 = dir == 0 ? 0 : ba, i1 = dir == 0 ? ba : (dir == 1 ? 0 : bb),
-                    i2 = dir == 2 ? 0 : bb;
-          const int pt = cf[0] * i0 + cf[1] * i1 + cf[2] * i2 + cf[3];
-          const bool ok = bv && ak < 2;
-#pragma unroll
-          for (int f = 0; f < 4; ++f)
-            dmma884(lv[f][0], lv[f][1], aL, ok ? double(fl[f * NFP + fc * NFQ + pt]) : 0.0);
-        }
-        const R* Xe = sg + e * GEO_HEX;
-        const double iJ = Xe[HX_IJ];
-        const double g0 = Xe[HX_G + 3 * dir], g1 = Xe[HX_G + 3 * dir + 1],
-                     g2 = Xe[HX_G + 3 * dir + 2];
-        R* ae = sacc + e * 4 * NP;
-#pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          const int col = ct * 8 + ak * 2 + i;
-          if (ar >= N1 || col >= NN) continue;
-          const int ca = col / N1, cb = col - ca * N1;
-          const int n = node(dir, ar, ca, cb);
-          const int ii = n / NN, jj = (n / N1) % N1, kk = n % N1;
-          const double mi = double(siw1[ii]) * siw1[jj] * siw1[kk] * iJ;
-          const double out[4] = {-(g0 * dv[1][i] + g1 * dv[2][i] + g2 * dv[3][i]) + mi * lv[0][i],
-                            -g0 * dv[0][i] + mi * lv[1][i], -g1 * dv[0][i] + mi * lv[2][i],
-                            -g2 * dv[0][i] + mi * lv[3][i]};
-#pragma unroll
-          for (int f = 0; f < 4; ++f) {
-            if (dir == 0) ae[f * NP + n] = R(out[f]);
-            else ae[f * NP + n] = R(double(ae[f * NP + n]) + out[f]);
-          }
-        }
-      }
-      __syncthreads();
-    }
-  }
-
 #pragma unroll
   for (int s = 0; s < S; ++s) {
     const int i = tid + s * NT;
     const int e = i / NP, n = i - e * NP;
     if (e >= ne) continue;
-    if constexpr (MMA) {
-#pragma unroll
-      for (int c = 0; c < 4; ++c) acc[s][c] = sacc[(e * 4 + c) * NP + n];
-    }
     const int idx[3] = {n / (N1 * N1), (n / N1) % N1, n % N1};
     const R* fl = sf + e * NFP * 4;
     R lift[4] = {R(0), R(0), R(0), R(0)};
     // (hex: fl is [field][face point])
 #pragma unroll
-    for (int f = 0; f < (MMA ? 0 : 6); ++f) {
+    for (int f = 0; f < 6; ++f) {
       const int axis = f >> 1, end = f & 1;
       const int l = idx[axis];
       R w;

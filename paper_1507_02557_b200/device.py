@@ -569,8 +569,6 @@ class DeviceMesh:
             T = S.t[TYPE_ID[t]]
             T.K = P["K"]
             T.form = nat.HW_FORM_SKEW if P["form"] == "skew" else nat.HW_FORM_STRONG
-            if t == "hex" and np.all(np.asarray(P["geo"])[:, 36] != 0):   # HX_AFF word
-                T.flags |= nat.HW_TYPE_ALL_AFFINE
             T.geo = self._put(P["geo"])
             T.mat = self._put(P["mat"])
             T.nbr_elem = self._put(P["nbr_elem"], torch.int32)
