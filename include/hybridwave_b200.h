@@ -199,6 +199,12 @@ int hw_halo_scatter(const hw_mesh_t* mesh, const void* buf, int64_t stride,
 int hw_energy(const hw_mesh_t* mesh, const hw_fields_t* q, double* out,
               void* stream);
 
+/* One-time per-mesh setup on the mesh's device (synchronous; call once
+ * after filling hw_mesh_t, before the first launch and outside any CUDA
+ * graph capture): uploads the order/formulation constant tables the
+ * kernels read from constant memory (hex node -> face-point map). */
+int hw_prepare(const hw_mesh_t* mesh);
+
 const char* hw_last_error(void);
 int hw_version(void);
 /* kernel launches this library has issued so far (all devices, all

@@ -80,6 +80,7 @@ def lib():
         L.hw_wedge_face_correction.argtypes = [P(HWMesh), c_int, c_int, c_void_p, c_void_p,
                                                c_void_p, c_void_p, c_int, c_int, c_void_p,
                                                c_void_p]
+        L.hw_prepare.argtypes = [P(HWMesh)]
         L.hw_halo_gather.argtypes = [P(HWMesh), c_void_p, c_int64, c_void_p, c_int64,
                                      c_void_p, c_void_p]
         L.hw_halo_scatter.argtypes = [P(HWMesh), c_void_p, c_int64, c_void_p, c_int64,
@@ -87,7 +88,7 @@ def lib():
         L.hw_last_error.restype = ctypes.c_char_p
         for name in ("hw_rhs", "hw_traces", "hw_lsrk_stage", "hw_ab_step", "hw_axpy3",
                      "hw_hist_push", "hw_halo_pack", "hw_halo_gather", "hw_halo_scatter",
-                     "hw_forcing", "hw_wedge_face_correction", "hw_energy", "hw_version", "hw_supported_orders"):
+                     "hw_forcing", "hw_wedge_face_correction", "hw_prepare", "hw_energy", "hw_version", "hw_supported_orders"):
             getattr(L, name).restype = c_int
         L.hw_launch_count.restype = ctypes.c_longlong
         L.hw_launch_count.argtypes = []
@@ -97,7 +98,7 @@ def lib():
 
 EXPORTED_SYMBOLS = ("hw_rhs", "hw_traces", "hw_lsrk_stage", "hw_ab_step", "hw_axpy3", "hw_hist_push",
                     "hw_halo_pack", "hw_halo_gather", "hw_halo_scatter", "hw_forcing",
-                    "hw_wedge_face_correction", "hw_energy", "hw_last_error", "hw_version",
+                    "hw_wedge_face_correction", "hw_prepare", "hw_energy", "hw_last_error", "hw_version",
                     "hw_supported_orders", "hw_launch_count")
 
 

@@ -914,6 +914,20 @@ int hw_wedge_face_correction(const hw_mesh_t* mesh, int elem_type, int n_pairs,
   return check_launch("wedge_face_corr_kernel");
 }
 
+int hw_prepare(const hw_mesh_t* mesh) {
+  HW_DEVICE_GUARD(mesh);
+  if (!mesh) return fail("null mesh");
+  if (mesh->N < 1 || mesh->N > 7) return fail("polynomial order out of range");
+  if (mesh->t[HW_HEX].K > 0) {
+    if (!mesh->t[HW_HEX].iop[3]) return fail("hex face-point table missing");
+    const size_t off = sizeof(int) * 24 * ((size_t)mesh->formulation * 8 + mesh->N);
+    cudaError_t e = cudaMemcpyToSymbol(c_hex_spc, mesh->t[HW_HEX].iop[3], 24 * sizeof(int),
+                                       off, cudaMemcpyDeviceToDevice);
+    if (e != cudaSuccess) return fail(cudaGetErrorString(e));
+  }
+  return 0;
+}
+
 int hw_energy(const hw_mesh_t* mesh, const hw_fields_t* q, double* out, void* stream) {
   HW_DEVICE_GUARD(mesh);
   if (!out) return fail("hw_energy: out is null");

@@ -823,6 +823,13 @@ __device__ __forceinline__ R hex_metric(const R* X, R r, R s, R t, R G[9]) {
   return J;
 }
 
+// node (i, j, k) -> face point c . (i, j, k, 1) of each hex face, per
+// formulation and order, in constant memory (hw_prepare uploads the mesh's
+// iop[3]): the face index is a compile-time constant of the unrolled lift
+// and publish loops, so the coefficients are uniform constant-bank reads
+// instead of shared-memory loads (24 per node).
+__constant__ int c_hex_spc[2][8][6][4];
+
 #ifndef HW_HEX_NT
 #define HW_HEX_NT 128
 #endif
@@ -869,7 +876,7 @@ __global__ void HW_HEX_BOUNDS hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi E,
     siw1[tid] = R(1) / sw1[tid];
     sx[tid] = ldg((const R*)TY.op[4] + tid);
   }
-  if (tid < 24) spc[tid] = __ldg(TY.iop[3] + tid);
+  (void)spc;
   if (tid < ne) sk[tid] = list ? list[w0 + tid] : (int)(w0 + tid);
   // TMA bulk copies of the element rows: every hex row (state, residual,
   // traces, record, material) is a multiple of 16 bytes, so each element
@@ -1121,7 +1128,7 @@ __global__ void HW_HEX_BOUNDS hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi E,
       } else {
         w = sve[end * N1 + l];
       }
-      const int* cf = spc + 4 * f;
+      const int* cf = c_hex_spc[M.formulation][N][f];
       const int pt = cf[0] * idx[0] + cf[1] * idx[1] + cf[2] * idx[2] + cf[3];
       const R* o = fl + f * NFQ + pt;
 #pragma unroll
@@ -1185,7 +1192,7 @@ __global__ void HW_HEX_BOUNDS hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi E,
 #pragma unroll
       for (int end = 0; end < 2; ++end) {
         const int f = 2 * a + end;
-        const int* cf = spc + 4 * f;
+        const int* cf = c_hex_spc[M.formulation][N][f];
         const int pt = cf[0] * ii + cf[1] * jj + cf[2] * kk + cf[3];
 #pragma unroll
         for (int c = 0; c < 4; ++c) o[c * NFP + f * NFQ + pt] = end ? t1[c] : t0[c];

@@ -602,6 +602,7 @@ class DeviceMesh:
         orders = nat.lib().hw_supported_orders()
         if not (orders >> disc.N) & 1:
             raise ValueError(f"order N={disc.N} not compiled into {nat.LIB_NAME}")
+        nat.check(nat.lib().hw_prepare(self.struct))
 
     def set_traces(self, tin, tout):
         """Point the struct's tr_in / tr_out at trace buffer sets (0/1/None)."""

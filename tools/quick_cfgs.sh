@@ -1,7 +1,9 @@
 #!/bin/bash
-# per-type kernel us for a few configurations: tools/quick_cfgs.sh TAG
+# per-type kernel us for the BASELINE configurations: tools/quick_cfgs.sh TAG
 tag=$1
-for args in "--dtype f32" "--mesh tet:20" "--mesh tet:20 --dtype f32" "--mesh hexdom:120 --order 4"; do
+for args in "--mesh hybrid:38 --order 3" "--mesh hybrid:38 --order 3 --dtype f32" \
+            "--mesh tet:20 --order 3" "--mesh tet:20 --order 3 --dtype f32" \
+            "--mesh hexdom:120 --order 4 --dtype f32"; do
   python bench.py --no-cpu-baseline --steps 20 $args > gpurun_out/q.log 2>&1
   python - "$args" <<'PY'
 import json, sys
