@@ -62,6 +62,9 @@ def parse():
     ap.add_argument("--levels", type=int, default=3)
     ap.add_argument("--partitioned", action="store_true",
                     help="use the element-partitioned path even on one rank")
+    ap.add_argument("--no-extra", action="store_true",
+                    help="skip the other BASELINE configurations measured alongside the "
+                         "default single-GPU line (other_configs)")
     return ap.parse_args()
 
 
@@ -247,6 +250,42 @@ def alg_bytes_per_elem(t, Np, s, N, gl=True):
     pub = t in ("wedge", "pyramid") or (t == "hex" and gl)
     tr = 2 * 4 * face_points(t, N) * s if pub else 0
     return 4 * 4 * Np * s + GEO_WORDS[t] * s + 4 * s + links + tr
+
+
+# the other BASELINE configurations, measured by the default N=1 run in
+# separate processes (each its own JSON line, summarised in other_configs)
+EXTRA_CONFIGS = [
+    ("configs[2] hybrid:38 N=3 GL fp64 LSRK-45", ["--mesh", "hybrid:38", "--order", "3"]),
+    ("configs[2] hybrid:38 N=3 GL fp32 LSRK-45",
+     ["--mesh", "hybrid:38", "--order", "3", "--dtype", "f32"]),
+    ("configs[1] tet:20 N=3 GL fp64 LSRK-45", ["--mesh", "tet:20", "--order", "3"]),
+    ("configs[4] graded:24 N=3 GL fp64 MRAB-AB3, 3 levels",
+     ["--mesh", "graded:24", "--order", "3", "--scheme", "mrab", "--levels", "3"]),
+]
+
+
+def other_configs(args):
+    import subprocess
+    out = {}
+    for label, extra in EXTRA_CONFIGS:
+        cmd = [sys.executable, os.path.abspath(__file__), "--no-cpu-baseline", "--no-extra",
+               "--steps", str(min(args.steps, 20)), "--warmup", str(args.warmup)] + extra
+        try:
+            p = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+            line = json.loads([x for x in p.stdout.splitlines() if x.startswith("{")][-1])
+        except Exception as e:  # pragma: no cover - reported, not fatal
+            out[label] = {"error": f"{type(e).__name__}: {str(e)[:200]}"}
+            continue
+        roof = line.get("roofline") or {}
+        out[label] = {"value": line["value"], "unit": line["unit"],
+                      "ms_per_step": line["ms_per_step"], "steps": line["steps"],
+                      "e2e": (line.get("e2e") or {}).get("value"),
+                      "gpu_launches": line.get("gpu_launches"),
+                      "roofline_frac": roof.get("frac"), "roofline_kernel": roof.get("kernel"),
+                      "per_type_us": {t: v["us_per_launch"]
+                                      for t, v in (roof.get("per_type") or {}).items()},
+                      "config": line["config"].get("workload")}
+    return out
 
 
 def main():
@@ -442,6 +481,8 @@ def main():
                         "steps": e2e_steps,
                         "api": "timeint.lsrk_run(disc, host_state, dt, T, out=host_out): pinned numpy in/out"},
                 "cpu_baseline": cpu}
+        if world == 1 and not args.no_extra and args.scheme == "lsrk":
+            line["other_configs"] = other_configs(args)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

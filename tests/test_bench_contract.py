@@ -46,7 +46,7 @@ def test_reference_arm_other_ranks_silent():
 @pytest.mark.gpu
 def test_product_arm_line():
     (line,) = run_bench(["--mesh", "hybrid:8", "--order", "3", "--steps", "3", "--warmup", "3",
-                         "--no-cpu-baseline"])
+                         "--no-cpu-baseline", "--no-extra"])
     assert BASE_KEYS <= set(line)
     assert line["n_gpus"] == 1 and line["warmup"] >= 3 and line["steps"] == 3
     assert line["value"] > 0 and line["dtype"] == "f64"
@@ -81,3 +81,23 @@ def test_partitioned_line_one_rank():
     assert BASE_KEYS <= set(line)
     assert line["value"] > 0 and line["gpu_launches"] == 3 * 5 * 4
     assert line["e2e"]["value"] > 0
+
+
+@pytest.mark.gpu
+def test_other_configs_summary():
+    """The default single-GPU line carries the other BASELINE configurations
+    (run as subprocesses with --no-extra), each with its value and workload."""
+    import bench
+    from types import SimpleNamespace
+    saved = bench.EXTRA_CONFIGS
+    bench.EXTRA_CONFIGS = [("small", ["--mesh", "hybrid:4", "--order", "2"]),
+                           ("small mrab", ["--mesh", "graded:6", "--order", "2",
+                                           "--scheme", "mrab"])]
+    try:
+        out = bench.other_configs(SimpleNamespace(steps=3, warmup=3))
+    finally:
+        bench.EXTRA_CONFIGS = saved
+    assert set(out) == {"small", "small mrab"}
+    for v in out.values():
+        assert "error" not in v, v
+        assert v["value"] > 0 and v["config"]

@@ -5,7 +5,7 @@ tag=$1; shift
 mkdir -p gpurun_out
 python -m pytest tests -m gpu -q -x -rf > gpurun_out/tests_$tag.txt 2>&1
 tail -3 gpurun_out/tests_$tag.txt
-python bench.py --no-cpu-baseline "$@" > gpurun_out/bench_$tag.json 2> gpurun_out/bench_$tag.err
+python bench.py --no-cpu-baseline --no-extra "$@" > gpurun_out/bench_$tag.json 2> gpurun_out/bench_$tag.err
 python - "$tag" <<'PY'
 import json, sys
 tag = sys.argv[1]

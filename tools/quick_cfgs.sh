@@ -4,7 +4,7 @@ tag=$1
 for args in "--mesh hybrid:38 --order 3" "--mesh hybrid:38 --order 3 --dtype f32" \
             "--mesh tet:20 --order 3" "--mesh tet:20 --order 3 --dtype f32" \
             "--mesh hexdom:120 --order 4 --dtype f32"; do
-  python bench.py --no-cpu-baseline --steps 20 $args > gpurun_out/q.log 2>&1
+  python bench.py --no-cpu-baseline --no-extra --steps 20 $args > gpurun_out/q.log 2>&1
   python - "$args" <<'PY'
 import json, sys
 try:
