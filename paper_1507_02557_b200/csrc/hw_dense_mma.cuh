@@ -88,7 +88,7 @@ struct DMma {
 #define HW_DENSE_MINB 3
 #endif
 #ifndef HW_DENSE_MINB32
-#define HW_DENSE_MINB32 4
+#define HW_DENSE_MINB32 5
 #endif
   static constexpr int MINB = sizeof(S) == 8 ? HW_DENSE_MINB : HW_DENSE_MINB32;
   static constexpr int BIG_MINB = (65536 / (NTH * 64)) > 1 ? 65536 / (NTH * 64) : 1;
