@@ -19,10 +19,6 @@ struct Dims {
   static constexpr int NP_PYR = (N + 1) * (N + 2) * (2 * N + 3) / 6;
   static constexpr int NQ_WEDGE = N1 * N1 * N1;
   static constexpr int NFP_HEX = 6 * NFQ;
-  // hex trace-buffer rows pad each face to an even point count, so a face's
-  // values are 16-byte aligned 16-byte multiples (bulk-copied by neighbours)
-  static constexpr int NFQP = NFQ + (NFQ & 1);
-  static constexpr int NFPT_HEX = 6 * NFQP;
   static constexpr int NFP_TET = 4 * NFN;
   static constexpr int NFP_WEDGE = 2 * NFN + 3 * NFQ;
   static constexpr int NFP_PYR = NFQ + 4 * NFN;
@@ -66,7 +62,7 @@ template <int N>
 __device__ __forceinline__ int face_offset(int t, int f) {
   using D = Dims<N>;
   switch (t) {
-    case HW_HEX: return f * D::NFQP;   // trace-buffer row offset (padded faces)
+    case HW_HEX: return f * D::NFQ;
     case HW_TET: return f * D::NFN;
     case HW_WEDGE: return f < 2 ? f * D::NFN : 2 * D::NFN + (f - 2) * D::NFQ;
     default: return f == 0 ? 0 : D::NFQ + (f - 1) * D::NFN;  // pyramid
@@ -217,17 +213,6 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
                "r"(bytes)
                : "memory");
-}
-
-// add expected bytes without arriving (several issuing lanes, one arrive)
-__device__ __forceinline__ void mbar_expect_only(uint64_t* bar, unsigned bytes) {
-  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
 
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {

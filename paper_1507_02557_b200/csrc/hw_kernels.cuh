@@ -30,8 +30,6 @@ template <int N>
 struct TT<N, HW_TET> {
   using D = Dims<N>;
   static constexpr int NP = D::NP_TET, NF = 4, NFP = D::NFP_TET, GEO = GEO_TET, GF = 9;
-  static constexpr int NFPT = NFP;
-  __host__ __device__ static constexpr int tpos(int j) { return j; }
   __host__ __device__ static constexpr bool tri(int) { return true; }
   __host__ __device__ static constexpr int off(int f) { return f * D::NFN; }
   __host__ __device__ static constexpr int cnt(int) { return D::NFN; }
@@ -42,8 +40,6 @@ template <int N>
 struct TT<N, HW_WEDGE> {
   using D = Dims<N>;
   static constexpr int NP = D::NP_WEDGE, NF = 5, NFP = D::NFP_WEDGE, GEO = GEO_WEDGE, GF = 10;
-  static constexpr int NFPT = NFP;
-  __host__ __device__ static constexpr int tpos(int j) { return j; }
   __host__ __device__ static constexpr bool tri(int f) { return f < 2; }
   __host__ __device__ static constexpr int off(int f) {
     return f < 2 ? f * D::NFN : 2 * D::NFN + (f - 2) * D::NFQ;
@@ -81,8 +77,6 @@ template <int N>
 struct TT<N, HW_PYRAMID> {
   using D = Dims<N>;
   static constexpr int NP = D::NP_PYR, NF = 5, NFP = D::NFP_PYR, GEO = GEO_PYR, GF = 9;
-  static constexpr int NFPT = NFP;
-  __host__ __device__ static constexpr int tpos(int j) { return j; }
   __host__ __device__ static constexpr bool tri(int f) { return f > 0; }
   __host__ __device__ static constexpr int off(int f) {
     return f == 0 ? 0 : D::NFQ + (f - 1) * D::NFN;
@@ -95,16 +89,10 @@ template <int N>
 struct TT<N, HW_HEX> {
   using D = Dims<N>;
   static constexpr int NP = D::NP_HEX, NF = 6, NFP = D::NFP_HEX, GEO = GEO_HEX, GF = 0;
-  static constexpr int NFPT = D::NFPT_HEX;      // trace-buffer row (padded faces)
-  __host__ __device__ static constexpr int tpos(int j) {
-    return (j / D::NFQ) * D::NFQP + j % D::NFQ;
-  }
   __host__ __device__ static constexpr bool tri(int) { return false; }
   __host__ __device__ static constexpr int off(int f) { return f * D::NFQ; }
   __host__ __device__ static constexpr int cnt(int) { return D::NFQ; }
-  // staged neighbour values [face][field][NFQP]: hex neighbours' published
-  // face blocks arrive whole (bulk copy, their point order)
-  __host__ __device__ static constexpr int stage(int) { return 4 * D::NFQP; }
+  __host__ __device__ static constexpr int stage(int) { return 4 * D::NFQ; }
 };
 
 template <int N, int T>
@@ -212,7 +200,7 @@ __device__ __forceinline__ bool publishes(int t, bool sem) {
 template <int N>
 __device__ __forceinline__ int nfp_of(int t) {
   using D = Dims<N>;
-  return t == HW_HEX ? D::NFPT_HEX : t == HW_TET ? D::NFP_TET
+  return t == HW_HEX ? D::NFP_HEX : t == HW_TET ? D::NFP_TET
                      : t == HW_WEDGE ? D::NFP_WEDGE : D::NFP_PYR;
 }
 
@@ -317,9 +305,8 @@ __device__ __forceinline__ void publish_traces(const hw_mesh_t& M, const R* sq, 
         a0 *= isj; a1 *= isj; a2 *= isj; a3 *= isj;
       }
     }
-    constexpr int NT_ = X::NFPT;   // trace-buffer row (hex: padded faces)
-    R* o = tr + (size_t)sk[e] * 4 * NT_ + X::tpos(j);
-    o[0] = a0; o[NT_] = a1; o[2 * NT_] = a2; o[3 * NT_] = a3;
+    R* o = tr + (size_t)sk[e] * 4 * NFP + j;
+    o[0] = a0; o[NFP] = a1; o[2 * NFP] = a2; o[3 * NFP] = a3;
   }
 }
 
@@ -340,7 +327,7 @@ struct Smem {
   static constexpr int SF = SV + ((T == HW_HEX) ? 0 : EPB * 3 * NP);
   static constexpr int SST = SF + EPB * NFP * FLUXW;
   static constexpr int STR = SST + EPB * STG;               // own traces (publishing types)
-  static constexpr int SG = STR + ((T == HW_TET) ? 0 : EPB * 4 * X::NFPT);
+  static constexpr int SG = STR + ((T == HW_TET) ? 0 : EPB * 4 * NFP);
   static constexpr int SMAT = SG + EPB * X::GEO;
   static constexpr int SOPS = SMAT + EPB * 4;   // hex: D1, x, w, Vend, 1/w
   static constexpr int TOTAL = SOPS + ((T == HW_HEX) ? (N + 1) * (N + 1) + 5 * (N + 1) : 0);
@@ -903,17 +890,16 @@ __global__ void HW_HEX_BOUNDS hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi E,
     mbar_fence_init();
   }
   __syncthreads();
-  constexpr int NFPT = Dims<N>::NFPT_HEX, NFQP = Dims<N>::NFQP;   // trace rows
-  constexpr unsigned ROWB = 4 * NP * sizeof(R), TRB = 4 * NFPT * sizeof(R);
+  constexpr unsigned ROWB = 4 * NP * sizeof(R), TRB = 4 * NFP * sizeof(R);
   static_assert(ROWB % 16 == 0 && TRB % 16 == 0 && (GEO_HEX * sizeof(R)) % 16 == 0 &&
                     (L::SRES * sizeof(R)) % 16 == 0 && (L::STR * sizeof(R)) % 16 == 0 &&
                     (L::SG * sizeof(R)) % 16 == 0 && (L::SMAT * sizeof(R)) % 16 == 0,
                 "hex rows / smem offsets must be 16-byte multiples for the bulk copies");
-  // staged neighbour values [e][face][field][NFQP]
-  constexpr int SFE = 24 * NFQP;
-  constexpr unsigned FB = NFQP * sizeof(R);        // one field of one face block
   if (tid < 32) {
-    if (tid == 0) mbar_expect_tx(&tbar[0], ne * (ROWB + (GEO_HEX + 4) * sizeof(R)));
+    if (tid == 0) {
+      mbar_expect_tx(&tbar[0], ne * (ROWB + (GEO_HEX + 4) * sizeof(R)));
+      mbar_expect_tx(&tbar[1], ne * ((sem ? 0u : TRB) + (lsrk ? ROWB : 0u)));
+    }
     __syncwarp();
     for (int e = tid; e < ne; e += 32) {
       const size_t k = (size_t)sk[e];
@@ -921,35 +907,17 @@ __global__ void HW_HEX_BOUNDS hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi E,
       bulk_load(sg + e * GEO_HEX, (const R*)TY.geo + k * GEO_HEX, GEO_HEX * sizeof(R),
                 &tbar[0]);
       bulk_load(smat + e * 4, (const R*)TY.mat + k * 4, 4 * sizeof(R), &tbar[0]);
-      mbar_expect_only(&tbar[1], (sem ? 0u : TRB) + (lsrk ? ROWB : 0u));
       if (!sem)
-        bulk_load(sm + L::STR + e * 4 * NFPT, (const R*)M.tr_in[HW_HEX] + k * 4 * NFPT, TRB,
+        bulk_load(sm + L::STR + e * 4 * NFP, (const R*)M.tr_in[HW_HEX] + k * 4 * NFP, TRB,
                   &tbar[1]);
       if (lsrk)
         bulk_load(sm + L::SRES + e * 4 * NP, (const R*)E.res[HW_HEX] + k * 4 * NP, ROWB,
                   &tbar[1]);
     }
-    // GL hex neighbours: their published face block (4 fields x NFQP), whole,
-    // in their point order; the flux applies the face permutation
-    if (!sem)
-      for (int pr = tid; pr < ne * 6; pr += 32) {
-        const int e = pr / 6, f = pr - e * 6;
-        const int code = __ldg(TY.nbr_code + (size_t)sk[e] * 6 + f);
-        if ((code & HW_NBR_BOUNDARY) || HW_NBR_TYPE(code) != HW_HEX) continue;
-        const size_t k2 = (size_t)__ldg(TY.nbr_elem + (size_t)sk[e] * 6 + f);
-        const R* src = (const R*)M.tr_in[HW_HEX] + k2 * 4 * NFPT + HW_NBR_FACE(code) * NFQP;
-        R* dst = sm + L::SST + e * SFE + f * 4 * NFQP;
-        mbar_expect_only(&tbar[1], 4 * FB);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) bulk_load(dst + c * NFQP, src + c * NFPT, FB, &tbar[1]);
-      }
-    __syncwarp();
-    if (tid == 0) mbar_arrive(&tbar[1]);
   }
   for (int i = tid; i < ne * 6; i += NT)
     snc[i] = __ldg(TY.nbr_code + (size_t)sk[i / 6] * 6 + i % 6);
-  // the other neighbour values at my face points through the host gather
-  // index (wedge / pyramid traces, SEM hex face nodes), in my point order
+  // the neighbour values at my face points through the host gather index
   {
     constexpr int IT = (EPB * NFP + NT - 1) / NT;
     int gv[IT];
@@ -965,7 +933,6 @@ __global__ void HW_HEX_BOUNDS hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi E,
       if (i >= ne * NFP || gv[u] < 0) continue;
       const int e = i / NFP, j = i - e * NFP;
       const int t2 = HW_NBR_TYPE(__ldg(TY.nbr_code + (size_t)sk[e] * 6 + j / NFQ));
-      if (!sem && t2 == HW_HEX) continue;        // bulk-copied face block
       const R* src;
       int stride;
       if (publishes(t2, sem)) {
@@ -976,10 +943,9 @@ __global__ void HW_HEX_BOUNDS hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi E,
         stride = NP;
       }
       src += gv[u];
-      const int f = j / NFQ;
-      R* dst = sm + L::SST + e * SFE + f * 4 * NFQP + (j - f * NFQ);
+      R* dst = sm + L::SST + e * 4 * NFP + j;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) cp_async(dst + c * NFQP, src + c * stride);
+      for (int c = 0; c < 4; ++c) cp_async(dst + c * NFP, src + c * stride);
     }
   }
   cp_async_commit();
@@ -1084,10 +1050,10 @@ __global__ void HW_HEX_BOUNDS hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi E,
       const int node = base + (end ? N : 0) * stride;
 #pragma unroll
       for (int c = 0; c < 4; ++c) own[c] = qe[c * NP + node];
-    } else {   // GL: published traces of the input state (padded face rows)
-      const R* te = sm + L::STR + e * 4 * NFPT + f * NFQP + jj;
+    } else {   // GL: published traces of the input state
+      const R* te = sm + L::STR + e * 4 * NFP + j;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) own[c] = te[c * NFPT];
+      for (int c = 0; c < 4; ++c) own[c] = te[c * NFP];
     }
     // face geometry at (xi, eta) = (x[a], x[b]) from the 4 face vertices
     const int a = jj / N1, b = jj - a * N1;
@@ -1127,11 +1093,9 @@ __global__ void HW_HEX_BOUNDS hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi E,
     R pp, up[3];
     if (code & HW_NBR_BOUNDARY) {
       pp = -own[0]; up[0] = um[0]; up[1] = um[1]; up[2] = um[2];
-    } else {   // staged neighbour values: a hex's face block in its point order
-      const int p = (!sem && HW_NBR_TYPE(code) == HW_HEX)
-                        ? __ldg(M.perm_quad + HW_NBR_PERM(code) * NFQ + jj) : jj;
-      const R* se = sm + L::SST + e * SFE + f * 4 * NFQP + p;
-      pp = se[0]; up[0] = se[NFQP]; up[1] = se[2 * NFQP]; up[2] = se[3 * NFQP];
+    } else {   // neighbour values staged in my point order
+      const R* se = sm + L::SST + e * 4 * NFP + j;
+      pp = se[0]; up[0] = se[NFP]; up[1] = se[2 * NFP]; up[2] = se[3 * NFP];
     }
     R tp, tu, fp, fu;
     penalties(Xv[HX_Z + 2 * f], Xv[HX_Z + 2 * f + 1], pen, tp, tu);
@@ -1224,14 +1188,14 @@ __global__ void HW_HEX_BOUNDS hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi E,
           t1[c] += w1 * x;
         }
       }
-      R* o = sm + L::STR + e * 4 * NFPT;
+      R* o = sm + L::STR + e * 4 * NFP;
 #pragma unroll
       for (int end = 0; end < 2; ++end) {
         const int f = 2 * a + end;
         const int* cf = c_hex_spc[M.formulation][N][f];
         const int pt = cf[0] * ii + cf[1] * jj + cf[2] * kk + cf[3];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) o[c * NFPT + f * NFQP + pt] = end ? t1[c] : t0[c];
+        for (int c = 0; c < 4; ++c) o[c * NFP + f * NFQ + pt] = end ? t1[c] : t0[c];
       }
     }
   }
@@ -1244,7 +1208,7 @@ __global__ void HW_HEX_BOUNDS hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi E,
       const size_t k = (size_t)sk[e];
       bulk_store(dr + k * 4 * NP, sm + L::SRES + e * 4 * NP, ROWB);
       if (dq) bulk_store(dq + k * 4 * NP, sq + e * 4 * NP, ROWB);
-      if (pub) bulk_store((R*)M.tr_out[HW_HEX] + k * 4 * NFPT, sm + L::STR + e * 4 * NFPT, TRB);
+      if (pub) bulk_store((R*)M.tr_out[HW_HEX] + k * 4 * NFP, sm + L::STR + e * 4 * NFP, TRB);
     }
     bulk_commit();
     bulk_wait_read();

@@ -349,7 +349,7 @@ def pack_mesh(disc):
                    **(wedge_cubature_ops(disc, dops) if naw else {})},
             "iop": _pack_iops(t, dops, disc.N, mesh, perm_tri, face_offsets, dops_all,
                               perm_quad, disc.formulation.kind == "SEM"),
-            "nfp": trace_layout(t, face_offsets[t], disc.N)[1],   # trace-buffer row
+            "nfp": int(dops["face_offsets"][-1]),
             "publishes": t in ("wedge", "pyramid") or (t == "hex"
                                                        and disc.formulation.kind == "GL")}
     pack["perm_tri"] = face_symmetry_perms("tri", dops_any["tri2d"])
@@ -491,18 +491,6 @@ def tet_gather_index(mesh, dops, perm_tri, face_offsets):
     return out.astype(np.int32)
 
 
-def trace_layout(t, face_offsets, N):
-    """(face offsets, row length) of type t's face-trace buffer rows: the
-    device face-point order, except that hex rows pad each face to an even
-    point count (16-byte aligned face blocks, Dims::NFQP in hw_common.cuh)."""
-    offs, nfp = face_offsets
-    if t != "hex":
-        return np.asarray(offs), int(nfp)
-    nfq = (N + 1) ** 2
-    nfqp = nfq + (nfq & 1)
-    return np.arange(7, dtype=np.int64) * nfqp, 6 * nfqp
-
-
 def face_gather_index(mesh, t, dops_all, perm_tri, perm_quad, face_offsets, N, sem):
     """(K, Nfp) int32 for the hex / wedge / pyramid kernels: for each of my face
     points (device order, hybridwave/dg.py:258-300 neighbour trace, already
@@ -528,7 +516,7 @@ def face_gather_index(mesh, t, dops_all, perm_tri, perm_quad, face_offsets, N, s
             k2, f2, pc = nbr[sel, f, 1], nbr[sel, f, 2], code[sel, f]
             p = perm[pc]                                   # (n, cnt) neighbour face point
             if t2 in ("wedge", "pyramid") or (t2 == "hex" and not sem):
-                offs2, nfp2 = trace_layout(t2, face_offsets[t2], N)
+                offs2, nfp2 = face_offsets[t2]
                 val = k2[:, None] * 4 * nfp2 + offs2[f2][:, None] + p
             elif t2 == "tet":
                 d2 = dops_all["tet"]

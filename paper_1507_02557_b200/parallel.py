@@ -92,10 +92,7 @@ def face_halo_offsets(t, dops, N, sem):
         tab = np.asarray(dops["face_tab"]).reshape(-1, 3)
         return [(tab[fo[f]:fo[f + 1], 0] + np.where(tab[fo[f]:fo[f + 1], 2] != 0, N, 0)
                  * tab[fo[f]:fo[f + 1], 1]).astype(np.int64) for f in range(nf)], "state"
-    from .device import trace_layout
-    to, _ = trace_layout(t, (fo, int(fo[-1])), N)          # hex rows: padded faces
-    return [np.arange(to[f], to[f] + (fo[f + 1] - fo[f]), dtype=np.int64)
-            for f in range(nf)], "trace"
+    return [np.arange(fo[f], fo[f + 1], dtype=np.int64) for f in range(nf)], "trace"
 
 
 def flat_face_offsets(pairs, local, row):

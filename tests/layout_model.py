@@ -28,19 +28,8 @@ def face_layout(t, N):
             + [("tri", d["NFQ"] + f * d["NFN"], d["NFN"]) for f in range(4)])
 
 
-def trace_offsets(t, N):
-    """Face offsets within a trace-buffer row: the device face-point order,
-    hex rows padded to an even point count per face (Dims::NFQP)."""
-    d = _dims(N)
-    if t == "hex":
-        nfqp = d["NFQ"] + (d["NFQ"] & 1)
-        return [f * nfqp for f in range(6)], 6 * nfqp
-    lay = face_layout(t, N)
-    return [o for _, o, _ in lay], lay[-1][1] + lay[-1][2]
-
-
 def own_traces(pack, t, q, N, sem):
-    """(K, 4, row) traces in the trace-buffer layout, as the kernels form them."""
+    """(K, 4, Nfp) traces at the device face points, as the kernels form them."""
     P = pack["types"][t]
     if t == "tet":
         return q[:, :, P["iop"][0]]
@@ -53,12 +42,7 @@ def own_traces(pack, t, q, N, sem):
         out = 0.0
         for l in range(N + 1):
             out = out + Vend[end, l][None, None, :] * q[:, :, base + l * stride]
-        offs, row = trace_offsets("hex", N)
-        nfq = (N + 1) ** 2
-        pad = np.zeros(out.shape[:2] + (row,))
-        for f in range(6):
-            pad[:, :, offs[f]:offs[f] + nfq] = out[:, :, f * nfq:(f + 1) * nfq]
-        return pad
+        return out
     ET = P["op"][5]                                    # (Np, Nfp)
     tr = q @ ET
     if t == "wedge":
@@ -142,8 +126,7 @@ def rhs(pack, disc, state, traces=None):
         flux = np.zeros((K, 4 if t == "hex" else 2, nfp))
         zm = mat[:, 2]
         for f, (ft, off, cnt) in enumerate(lay):
-            toff = trace_offsets(t, N)[0][f] if (t != "hex" or not sem) else off
-            own = traces[t][:, :, toff:toff + cnt]
+            own = traces[t][:, :, off:off + cnt]
             code = P["nbr_code"][:, f]
             k2 = P["nbr_elem"][:, f]
             oth = np.empty_like(own)
@@ -157,11 +140,8 @@ def rhs(pack, disc, state, traces=None):
                 f2 = (code[sel] >> 2) & 7
                 pc = (code[sel] >> 5) & 15
                 perm = (pack["perm_tri"] if ft == "tri" else pack["perm_quad"])[pc]   # (n, cnt)
-                if t2 == "hex" and sem:
-                    lay2 = [o for _, o, _ in face_layout(t2, N)]
-                else:
-                    lay2 = trace_offsets(t2, N)[0]
-                off2 = np.array([lay2[x] for x in f2])
+                lay2 = face_layout(t2, N)
+                off2 = np.array([lay2[x][1] for x in f2])
                 cols = off2[:, None] + perm
                 tr2 = traces[t2][k2[sel]]                                      # (n,4,nfp2)
                 oth[sel] = np.take_along_axis(tr2, np.repeat(cols[:, None, :], 4, axis=1), axis=2)
