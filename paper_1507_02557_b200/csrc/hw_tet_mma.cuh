@@ -82,7 +82,10 @@ struct TetMma {
   // (MINB 7); slower for fp32 N=3 (141 -> 148) and fp64 N=1,2,4,5.
   static constexpr int XW = (sizeof(S) == 8 && N == 3) ? HW_TET_XW : 0;
   static constexpr int NTH = 32 * (W + XW);
-  static constexpr bool VEC = (NPK == NP) && ((4 * NP * sizeof(S)) % 16 == 0);  // 16-byte rows
+  // q / res rows are contiguous in smem (field stride NP, as in HBM); the
+  // K padding of the p-field B fragments reads the next field's values,
+  // which the zero-padded A fragments cancel
+  static constexpr bool VEC = (4 * NP * sizeof(S)) % 16 == 0;  // 16-byte rows
   static constexpr int EQ = frag_stride<S>(4 * NPK);        // q / res element stride
   static constexpr int EV = frag_stride<S>(3 * NPK);        // v_c
   static constexpr int EF = frag_stride<S>(4 * NFK);        // fp / fu
@@ -100,7 +103,7 @@ struct TetMma {
   // smem (no K padding) and every copy a multiple of 16 bytes at 16-byte
   // aligned addresses; otherwise the cp.async path stages them
   static constexpr bool TMA_OK =
-      NPK == NP && (4 * NP * sizeof(S)) % 16 == 0 && (EQ * sizeof(S)) % 16 == 0 &&
+      (4 * NP * sizeof(S)) % 16 == 0 && (EQ * sizeof(S)) % 16 == 0 &&
       (SRES * sizeof(S)) % 16 == 0 && (SG * sizeof(S)) % 16 == 0 &&
       (SMAT * sizeof(S)) % 16 == 0 && (TOTAL * sizeof(S)) % 16 == 0 &&
       (E * GEO_TET * sizeof(S)) % 16 == 0 && (E * 4 * sizeof(S)) % 16 == 0 &&
@@ -114,7 +117,7 @@ struct TetMma {
   static constexpr int IT = (E * NFP + NTH - 1) / NTH;
 };
 
-// element rows (K, 4, NP) -> smem [e][field (stride NPK)][node]
+// element rows (K, 4, NP) -> smem [e][field (stride NP)][node]
 template <typename L, typename S>
 __device__ __forceinline__ void tet_rows(S* dst, const S* src, const int* sk, int ne) {
   constexpr int NP = L::NP, NPK = L::NPK;
@@ -124,7 +127,7 @@ __device__ __forceinline__ void tet_rows(S* dst, const S* src, const int* sk, in
     for (int i = threadIdx.x; i < ne * 4 * NP; i += L::NTH) {
       const int e = i / (4 * NP), r = i - e * 4 * NP;
       const int fld = r / NP, n = r - fld * NP;
-      cp_async(dst + e * L::EQ + fld * NPK + n, src + (size_t)sk[e] * 4 * NP + r);
+      cp_async(dst + e * L::EQ + fld * NP + n, src + (size_t)sk[e] * 4 * NP + r);
     }
   }
 }
@@ -178,12 +181,12 @@ __global__ void __launch_bounds__(TetMma<N, S>::NTH, TetMma<N, S>::MINB)
   for (int i = tid; i < NFP; i += NTH) sfn[i] = __ldg(TY.iop[0] + i);
   // K padding must be zero for the DMMA (rows are never written by copies)
   constexpr int PADN = (NPK > NP) ? NPK - NP : 1, PADF = (NFK > NFN) ? NFK - NFN : 1;
-  if (NPK > NP)
-    for (int i = tid; i < EB * 11 * PADN; i += NTH) {
-      const int e = i / (11 * PADN), r = i - e * 11 * PADN;
+  if (NPK > NP)   // v_c K padding, and the q-row tail the last field's padding reads
+    for (int i = tid; i < EB * 4 * PADN; i += NTH) {
+      const int e = i / (4 * PADN), r = i - e * 4 * PADN;
       const int fld = r / PADN, n = NP + r - fld * PADN;
-      if (fld < 4) sq[e * EQ + fld * NPK + n] = S(0);
-      else if (fld >= 8) sv[e * EV + (fld - 8) * NPK + n] = S(0);
+      if (fld == 0) sq[e * EQ + 3 * NP + n] = S(0);
+      else sv[e * EV + (fld - 1) * NPK + n] = S(0);
     }
   __syncthreads();
 
@@ -259,7 +262,7 @@ __global__ void __launch_bounds__(TetMma<N, S>::NTH, TetMma<N, S>::MINB)
     const int e = i / NP, n = i - e * NP;
     const S* G = sg + e * GEO_TET;
     const S* u = sq + e * EQ + n;
-    const R u0 = u[NPK], u1 = u[2 * NPK], u2 = u[3 * NPK];
+    const R u0 = u[NP], u1 = u[2 * NP], u2 = u[3 * NP];
 #pragma unroll
     for (int c = 0; c < 3; ++c)
       sv[e * EV + c * NPK + n] = S(R(G[c * 3]) * u0 + R(G[c * 3 + 1]) * u1 + R(G[c * 3 + 2]) * u2);
@@ -307,7 +310,7 @@ __global__ void __launch_bounds__(TetMma<N, S>::NTH, TetMma<N, S>::MINB)
     const int node = sfn[j];
     const S* qe = sq + e * EQ + node;
     const R pm = qe[0];
-    const R um[3] = {qe[NPK], qe[2 * NPK], qe[3 * NPK]};
+    const R um[3] = {qe[NP], qe[2 * NP], qe[3 * NP]};
     const S* g = sg + e * GEO_TET + 9 + FS * f;
     const R nrm[3] = {g[0], g[1], g[2]};
     R pp, up[3];
@@ -382,19 +385,19 @@ __global__ void __launch_bounds__(TetMma<N, S>::NTH, TetMma<N, S>::MINB)
         for (int x = 0; x < 4; ++x) {
           const S v = (x == 0 ? S(accp[i] * R(kap)) : S(accu[x - 1][i] * R(irho))) +
                       frc_at<S>(E, HW_TET, base + x * NP);
-          const S qv = qe[x * NPK];
+          const S qv = qe[x * NP];
           if (lsrk) {
-            const S r = S(E.a) * re[x * NPK] + S(E.dt) * v;
-            re[x * NPK] = r;
-            qe[x * NPK] = qv + S(E.b) * r;
+            const S r = S(E.a) * re[x * NP] + S(E.dt) * v;
+            re[x * NP] = r;
+            qe[x * NP] = qv + S(E.b) * r;
           } else if (E.mode == MODE_RHS) {
-            qe[x * NPK] = v;
+            qe[x * NP] = v;
           } else {
             S acc = S(E.c0) * v;
             if (E.nhist > 1) acc += S(E.c1) * ((const S*)E.h1[HW_TET])[base + x * NP];
             if (E.nhist > 2) acc += S(E.c2) * ((const S*)E.h2[HW_TET])[base + x * NP];
-            re[x * NPK] = v;
-            qe[x * NPK] = qv + S(E.dt) * acc;
+            re[x * NP] = v;
+            qe[x * NP] = qv + S(E.dt) * acc;
           }
         }
       }
@@ -432,8 +435,8 @@ __global__ void __launch_bounds__(TetMma<N, S>::NTH, TetMma<N, S>::MINB)
       for (int x = 0; x < 3; ++x)
         epilogue_s<S>(E, HW_TET, base + (1 + x) * NP,
                       S(accu[x][i] * irho) + frc_at<S>(E, HW_TET, base + (1 + x) * NP),
-                      qe[(1 + x) * NPK],
-                      re[(1 + x) * NPK]);
+                      qe[(1 + x) * NP],
+                      re[(1 + x) * NP]);
     }
   }
 }
