@@ -7,8 +7,10 @@ import os
 import subprocess
 import sys
 
-KINDS = [("hex_kernel", "hex"), ("dense_mma_kernel<3, 1", "wedge"),
-         ("dense_mma_kernel<3, 2", "pyramid"), ("tet_mma_kernel", "tet")]
+import re
+
+KINDS = [(r"hex_kernel<", "hex"), (r"dense_mma_kernel(_big)?<\d+, 1,", "wedge"),
+         (r"dense_mma_kernel(_big)?<\d+, 2,", "pyramid"), (r"tet_mma_kernel<", "tet")]
 
 
 def main(rep, note, prefix="hybrid:38/N3/GL/f64"):
@@ -22,7 +24,7 @@ def main(rep, note, prefix="hybrid:38/N3/GL/f64"):
     seen = set()
     for r in rows[2:]:
         name = r[hdr.index("Kernel Name")]
-        kind = next((k for s, k in KINDS if s in name), None)
+        kind = next((k for s, k in KINDS if re.search(s, name)), None)
         if kind is None or kind in seen:
             continue
         seen.add(kind)
