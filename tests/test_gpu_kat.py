@@ -252,3 +252,67 @@ def test_l2_error_on_device(native_lib):
                 d.l2_error(host, cavity_fields, 5e-3)):
         for k in ("p", "u", "total"):
             assert abs(got[k] - ref[k]) <= 1e-12 * ref[k], (k, got[k], ref[k])
+
+
+def _assemble_rhs_operator(d):
+    """L with rhs = L U, assembled column by column from the device RHS of
+    unit vectors (the matrix-free operator of SPEC.md:499-502), batched:
+    one compute_rhs per unit vector of the global DOF vector."""
+    n = d.n_dof
+    L = np.empty((n, n))
+    base = np.zeros(n)
+    for i in range(n):
+        base[i] = 1.0
+        r = d.compute_rhs(d.vector_to_state(base))
+        L[:, i] = d.state_to_vector(r)
+        base[i] = 0.0
+    return L
+
+
+def _energy_weights(d):
+    """W with U^T W U = discrete_energy(U) (hybridwave/dg.py:655-674)."""
+    blocks = []
+    for t in d.types:
+        dd = d.data[t]
+        mat = d.mesh.materials[t]
+        Np = d.ops[t].Np
+        for k in range(d.n_elems[t]):
+            if t == "hex":
+                Mk = np.diag(dd.w3 * dd.J[k])
+            elif t == "tet":
+                Mk = d.ops[t].M_ref * dd.J[k, 0]
+            elif t == "wedge":
+                Mk = np.eye(Np)
+            else:
+                Mk = np.diag(dd.J[k])
+            blocks += [Mk / mat[k, 1]] + [Mk * mat[k, 0]] * 3
+    from scipy.linalg import block_diag
+    return block_diag(*blocks)
+
+
+@pytest.mark.parametrize("spec,N,form", [("hybrid:2", 1, "GL"), ("hybrid:2", 1, "SEM"),
+                                          ("tet:1", 2, "GL"), ("pyramid:1", 2, "SEM")])
+def test_energy_stability_of_assembled_operator(spec, N, form, native_lib):
+    """SPEC.md:500-502, 516 on the device operator: with zero penalty the
+    RHS operator is skew in the energy inner product (W L + L^T W = 0,
+    1e-10); with the upwind penalty its symmetric part is negative
+    semidefinite (1e-10) and max Re eig(L) <= 1e-8 (energy stability)."""
+    from conftest import set_random_materials
+    m = build_mesh(spec)
+    set_random_materials(m, 13)
+    from paper_1507_02557_b200.dg import Discretization
+    for pen in (0.0, 1.0):
+        d = Discretization(m, N, form, penalty_scale=pen)
+        if d.n_dof > 2500:
+            pytest.skip("mesh too large for dense assembly")
+        L = _assemble_rhs_operator(d)
+        W = _energy_weights(d)
+        S = W @ L
+        sym = 0.5 * (S + S.T)
+        scale = np.abs(S).max()
+        if pen == 0.0:
+            assert np.abs(sym).max() <= 1e-10 * scale
+        else:
+            assert np.linalg.eigvalsh(sym).max() <= 1e-10 * scale
+            ev = np.linalg.eigvals(L)
+            assert ev.real.max() <= 1e-8 * np.abs(ev).max()

@@ -124,3 +124,19 @@ def test_run_config_validation():
     assert app_mesh("graded:4").n_elements > 0
     with pytest.raises(ValueError):
         app_mesh("torus:3")
+
+
+def test_energy_weight_matrix_matches_discrete_energy():
+    """The energy inner product the GPU stability test uses (tests/
+    test_gpu_kat.py::_energy_weights) is discrete_energy's."""
+    import sys
+    sys.path.insert(0, os.path.dirname(__file__))
+    from test_gpu_kat import _energy_weights
+    from paper_1507_02557_b200.dg import Discretization, discrete_energy
+    m = build_mesh("hybrid:2")
+    set_random_materials(m, 13)
+    d = Discretization(m, 1, "GL", device="cpu")
+    rng = np.random.default_rng(4)
+    u = rng.standard_normal(d.n_dof)
+    W = _energy_weights(d)
+    assert abs(u @ W @ u - discrete_energy(d.vector_to_state(u), d)) <= 1e-12 * abs(u @ W @ u)
