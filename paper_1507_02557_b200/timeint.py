@@ -282,13 +282,33 @@ class MRABDriver:
 
     def _macro(self, q, eff, ring, n_hist, steps, dt_min, st):
         """Launch one macro step (2^(L-1) ticks) on stream st; advances the
-        host-side counters n_hist / steps / rhs_evals."""
+        host-side counters n_hist / steps / rhs_evals.  Returns (q, eff):
+        tick 0 steps every level, so it reads q directly and writes the new
+        state into the other buffer (no effective-state copy of the whole
+        mesh); the two buffers swap roles once per macro step."""
         disc, L = self.disc, self.n_levels
         lib, dm = nat.lib(), disc.device_mesh
         F = lambda s: nat.fields(disc.slots(s))
         subs = self._sub_structs
         for tick in range(2 ** (L - 1)):
             stepping = [lev for lev in range(1, L + 1) if tick % (2 ** (L - lev)) == 0]
+            if tick == 0:   # every level steps: q is the effective state everywhere
+                dm.compute_traces(F(q), 0, st, subset=self._trace_subs[tick])
+                dm.set_traces(0, None)
+                if dm.corr:
+                    disc.apply_corrections()
+                for lev in stepping:
+                    n_hist[lev] = min(n_hist[lev] + 1, 3)
+                    steps[lev] += 1
+                    s0 = steps[lev] % 3
+                    h0, h1, h2 = ring[s0], ring[(s0 - 1) % 3], ring[(s0 - 2) % 3]
+                    nh = n_hist[lev]
+                    c = list(ab_coefficients(nh)) + [0.0] * (3 - nh)
+                    nat.check(lib.hw_ab_step(dm.struct, F(q), F(eff), F(h0), F(h1), F(h2), nh,
+                                             c[0], c[1], c[2], dt_min * 2 ** (L - lev),
+                                             subs[lev], st))
+                q, eff = eff, q
+                continue
             # effective state: q, plus the dense-output correction on
             # non-stepping levels (timeint.py:144-173)
             for lev in range(1, L + 1):
@@ -325,6 +345,7 @@ class MRABDriver:
                                          c[0], c[1], c[2], dt_min * 2 ** (L - lev),
                                          subs[lev], st))
         self._count(1)
+        return q, eff
 
     def _count(self, n_macro):
         L = self.n_levels
@@ -431,29 +452,34 @@ class MRABDriver:
         n_hist = np.zeros(L + 1, dtype=int)
         steps = np.zeros(L + 1, dtype=int)
         use_graph = graph and callback is None
-        gkey = dt_min
-        g = self._graphs.get(gkey) if use_graph else None
         m = 0
         while m < n_macro:
             t0 = m * dt_min * 2 ** (L - 1)
             if use_graph and n_macro - m >= 3 and (n_hist[1:] == 3).all():
+                # the period's graph depends on which buffer holds q (the
+                # buffers swap once per macro step, an odd number per period)
+                gkey = (dt_min, q[disc.types[0]].data_ptr())
+                g = self._graphs.get(gkey)
                 if g is None:
                     g = self._graphs[gkey] = torch.cuda.CUDAGraph()
                     saved = (n_hist.copy(), steps.copy(), {t: v.copy() for t, v in self.rhs_evals.items()})
+                    qq, ee = q, eff
                     with torch.cuda.graph(g):
                         for _ in range(3):
-                            self._macro(q, eff, ring, n_hist, steps, dt_min, disc.stream_ptr())
+                            qq, ee = self._macro(qq, ee, ring, n_hist, steps, dt_min,
+                                                 disc.stream_ptr())
                     # capture launches nothing: restore the counters, replay below
                     n_hist[:], steps[:] = saved[0], saved[1]
                     self.rhs_evals = saved[2]
                 g.replay()
+                q, eff = eff, q
                 for lev in range(1, L + 1):
                     steps[lev] += 3 * 2 ** (lev - 1)
                 self._count(3)
                 self.macro_steps += 3
                 m += 3
                 continue
-            self._macro(q, eff, ring, n_hist, steps, dt_min, disc.stream_ptr())
+            q, eff = self._macro(q, eff, ring, n_hist, steps, dt_min, disc.stream_ptr())
             self.macro_steps += 1
             m += 1
             if callback is not None:
