@@ -110,6 +110,17 @@ def test_hexdom120_rhs_sampled(native_lib):
     _check_sampled(d, q, out, seed=4)
 
 
+def test_hexdom120_fp32_sampled(native_lib):
+    """C4 with fp32 storage against the fp64 oracle on the sample (1e-4)."""
+    from paper_1507_02557_b200.app import build_mesh
+    from paper_1507_02557_b200.dg import Discretization
+    d = Discretization(build_mesh("hexdom:120"), 4, "GL", dtype=torch.float32)
+    q64 = _random_device_state(d, 45)
+    q64 = {t: v.float().double() for t, v in q64.items()}
+    out = d.rhs_device({t: v.float() for t, v in q64.items()})
+    _check_sampled(d, q64, out, seed=5, tol=1e-4)
+
+
 def test_hybrid38_linearity(hyb38, native_lib):
     """RHS(a x + b y) = a RHS(x) + b RHS(y) on every element of C3 (N=3 GL)."""
     from paper_1507_02557_b200.dg import Discretization
