@@ -468,8 +468,11 @@ __global__ void __launch_bounds__(NT) dense_kernel(hw_mesh_t M, hw_fields_t Q, E
   const bool naw = T == HW_WEDGE && TY.op[8] != nullptr;
   const R* wgeo = (const R*)TY.op[8];
   const R* wcst = (const R*)TY.op[9];
-  R* cs = reinterpret_cast<R*>(
-      (reinterpret_cast<uintptr_t>(sne + EPB * NF) + 15) & ~uintptr_t(15));
+  // (offset arithmetic on smem_raw itself keeps the pointer in the shared
+  // window: LDS / STS instead of generic loads and stores)
+  const unsigned cs_off = (unsigned)(((reinterpret_cast<const unsigned char*>(sne + EPB * NF) -
+                                       smem_raw) + 15) & ~15);
+  R* cs = reinterpret_cast<R*>(smem_raw + cs_off);
   if (T == HW_WEDGE && naw) {
     // trial pass at the volume cubature points: w grad p (incl. the
     // -p grad J / 2J term), w G u, w gJfac . u (hybridwave/dg.py:430-443)
