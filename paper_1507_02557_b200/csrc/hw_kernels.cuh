@@ -510,11 +510,18 @@ __global__ void __launch_bounds__(NT) dense_kernel(hw_mesh_t M, hw_fields_t Q, E
   // non-affine skew pyramid)
   for (int i = tid; i < ne * NP; i += NT) {
     const int e = i / NP, n = i - e * NP;
-    const R* G = sg + e * X::GEO;
+    // metric in registers (a pointer that may be shared or global would
+    // turn every access into a generic load)
+    R G[9];
     R sc = R(1);
     if (naff(e)) {
-      G = ngeo + ((size_t)sk[e] * NP + n) * 10;
-      if (vskew) sc = G[9];
+      const R* Gg = ngeo + ((size_t)sk[e] * NP + n) * 10;
+#pragma unroll
+      for (int a = 0; a < 9; ++a) G[a] = ldg(Gg + a);
+      if (vskew) sc = ldg(Gg + 9);
+    } else {
+#pragma unroll
+      for (int a = 0; a < 9; ++a) G[a] = sg[e * X::GEO + a];
     }
     const R* u = sq + e * 4 * NP + NP + n;
 #pragma unroll
@@ -599,11 +606,16 @@ __global__ void __launch_bounds__(NT) dense_kernel(hw_mesh_t M, hw_fields_t Q, E
           div += a0 * v[m] + a1 * v[NP + m] + a2 * v[2 * NP + m];
         }
       }
-      const R* G = sg + e * X::GEO;
+      R G[9];
       R iJ = R(1);
       if (naff(e)) {
-        G = ngeo + ((size_t)sk[e] * NP + n) * 10;
-        iJ = R(1) / G[9];
+        const R* Gg = ngeo + ((size_t)sk[e] * NP + n) * 10;
+#pragma unroll
+        for (int a = 0; a < 9; ++a) G[a] = ldg(Gg + a);
+        iJ = R(1) / ldg(Gg + 9);
+      } else {
+#pragma unroll
+        for (int a = 0; a < 9; ++a) G[a] = sg[e * X::GEO + a];
       }
       acc[s][0] = vskew ? div * iJ : -div;   // affine: J folded into the operators
 #pragma unroll
