@@ -64,7 +64,9 @@ struct TT<N, HW_WEDGE> {
 template <int N>
 struct Naw {
   using D = Dims<N>;
-  static constexpr int NP = D::NP_WEDGE, NQ = D::NQ_WEDGE, NQT = 6 * D::N1 * D::N1,
+  // NQT: the reference's triangle face rule without its duplicate points
+  // (6(N+1)^2 stored, each twice with equal weights: device.wedge_cubature_ops)
+  static constexpr int NP = D::NP_WEDGE, NQ = D::NQ_WEDGE, NQT = 3 * D::N1 * D::N1,
                        NFN = D::NFN, NFP = D::NFP_WEDGE;
   static constexpr int GF = NQ * 12, GT = GF + NFP * 5, GW = GT + 2 * NQT * 3;
   static constexpr int CVN = 4 * NP * NQ, CLQ = 8 * NP * NQ, CVF = CLQ + 2 * NQT * NFN;

@@ -70,8 +70,22 @@ def wedge_cubature_ops(disc, dops):
         quad[:, ds, :3] = d.normals[:, rs]
         quad[:, ds, 3] = d.wJs[:, rs] / ops.face_wts[f][None, :] * d.invsqrtJ_face[:, rs]
         quad[:, ds, 4] = d.invsqrtJ_face[:, rs]
+    # the symmetric triangle rule stores each point twice with equal
+    # weights: keep one of each pair with the summed
+    # weight (identical integrand at both: <= 1e-15 relative)
     nqt = int(roffs[1] - roffs[0])
-    tri = np.zeros((K, 2, nqt, 3))
+    uniq, pair = [], []
+    for f in range(2):
+        key = np.round(ops.face_pts2d[f], 11)
+        _, first, inv = np.unique(key, axis=0, return_index=True, return_inverse=True)
+        inv = inv.ravel()
+        partner = np.array([np.flatnonzero(inv == g) for g in range(len(first))])
+        if partner.shape[1:] != (2,):
+            raise ValueError("triangle face rule is not pairwise duplicated")
+        uniq.append(partner[:, 0])
+        pair.append(partner)
+    nqu = len(uniq[0])
+    tri = np.zeros((K, 2, nqu, 3))
     base = disc.trace_bases["wedge"]
     gidx = np.asarray(disc.gather_idx)
     bnd = np.asarray(disc.bnd_mask)
@@ -81,17 +95,20 @@ def wedge_cubature_ops(disc, dops):
         g = gidx[flat] - base
         ok = ~bnd[flat] & (g >= 0) & (g < K * tot)
         gc = np.where(ok, g, 0)
-        tri[:, f, :, 0] = d.invsqrtJ_face[:, rs]
+        u = uniq[f]
+        tri[:, f, :, 0] = d.invsqrtJ_face[:, rs][:, u]
         # the neighbour's 1/sqrt(J): a wedge's at the coincident point; a tet
         # or pyramid trace carries no sqrt(J) factor
         other = ~bnd[flat] & ~ok
-        tri[:, f, :, 1] = np.where(ok, d.invsqrtJ_face[gc // tot, gc % tot],
-                                   np.where(other, 1.0, 0.0))
-        tri[:, f, :, 2] = d.wJs[:, rs] * d.invsqrtJ_face[:, rs]
+        nb = np.where(ok, d.invsqrtJ_face[gc // tot, gc % tot], np.where(other, 1.0, 0.0))
+        tri[:, f, :, 1] = nb[:, u]
+        wsc = d.wJs[:, rs] * d.invsqrtJ_face[:, rs]
+        tri[:, f, :, 2] = wsc[:, pair[f][:, 0]] + wsc[:, pair[f][:, 1]]
     geo = np.concatenate([vol.reshape(K, -1), quad.reshape(K, -1), tri.reshape(K, -1)], axis=1)
     mats = [ops.V, ops.Dr3, ops.Ds3, ops.Dt3]
-    Lq = np.stack([_tri_lagrange(dops["tri2d"], ops.face_pts2d[f], disc.N) for f in range(2)])
-    Vf = np.stack([ops.Vf[roffs[f]:roffs[f + 1]] for f in range(2)])
+    Lq = np.stack([_tri_lagrange(dops["tri2d"], ops.face_pts2d[f][uniq[f]], disc.N)
+                   for f in range(2)])
+    Vf = np.stack([ops.Vf[roffs[f]:roffs[f + 1]][uniq[f]] for f in range(2)])
     const = np.concatenate([np.stack([m.T for m in mats]).ravel(), np.stack(mats).ravel(),
                             Lq.ravel(), Vf.ravel()])
     return {8: geo, 9: const}

@@ -238,7 +238,7 @@ def naw_rhs(pack, disc, state):
     K = P["K"]
     q = np.asarray(state["wedge"], dtype=float)
     Np = q.shape[2]
-    nq, nqt, nfn = (N + 1) ** 3, 6 * (N + 1) ** 2, d["NFN"]
+    nq, nqt, nfn = (N + 1) ** 3, 3 * (N + 1) ** 2, d["NFN"]   # deduplicated triangle rule
     lay = face_layout("wedge", N)
     nfp = lay[-1][1] + lay[-1][2]
     GF, GT = nq * 12, nq * 12 + nfp * 5
