@@ -108,7 +108,7 @@ static int launch_dense(const hw_mesh_t& M, const hw_fields_t& Q, const Epi& E,
   using L = Smem<N, T, R>;
   // non-affine wedges: cubature scratch (Naw) behind the layout
   constexpr size_t NAW_BYTES =
-      (T == HW_WEDGE) ? 16 + sizeof(R) * (size_t)L::EPB * (Naw<N>::CS + 4 * L::NP) : 0;
+      (T == HW_WEDGE) ? 16 + sizeof(R) * (size_t)L::EPB * Naw<N>::CS : 0;
   static_assert(L::BYTES + NAW_BYTES <= 227 * 1024, "dense_kernel shared memory");
   const size_t bytes = L::BYTES + (M.t[T].op[8] != nullptr ? NAW_BYTES : 0);
   int rc;

@@ -83,14 +83,6 @@ __host__ __device__ constexpr int n_dofs(int t) {
        : t == HW_WEDGE ? Dims<N>::NP_WEDGE : Dims<N>::NP_PYR;
 }
 
-// fp64 tensor-core MMA (SASS DMMA): C(8x8) += A(8x4) B(4x8); lane l holds
-// A[l/4][l%4], B[l%4][l/4] and C[l/4][2(l%4) + {0,1}]
-__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-               : "+d"(c0), "+d"(c1)
-               : "d"(a), "d"(b));
-}
-
 template <typename R>
 __device__ __forceinline__ R ldg(const R* p) { return __ldg(p); }
 __device__ __forceinline__ double2 ldg2(const double* p) {   // 16-byte aligned pair

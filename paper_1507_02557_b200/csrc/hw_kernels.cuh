@@ -475,98 +475,36 @@ __global__ void __launch_bounds__(NT) dense_kernel(hw_mesh_t M, hw_fields_t Q, E
   const unsigned cs_off = (unsigned)(((reinterpret_cast<const unsigned char*>(sne + EPB * NF) -
                                        smem_raw) + 15) & ~15);
   R* cs = reinterpret_cast<R*>(smem_raw + cs_off);
-  // Naw volume passes on DMMA (fp64 tensor cores, one warp per 8x8 tile;
-  // warps take the tiles round-robin).  The operators are read straight
-  // from global memory in their stored layouts (L1-resident); rows / k /
-  // columns outside the block's extents are zero.
-  R* rs = cs + EPB * W8::CS;   // test-pass results [e][field][NP]
   if (T == HW_WEDGE && naw) {
-    // trial pass: U_f = V q_f and dP_c = D3_c p at the volume cubature points
-    // (dense GEMMs, rows = cubature points, columns = (element, field)),
-    // into the scratch slots 0..3 (U) and 4..6 (dP)
-    constexpr int NQ = W8::NQ, RQ = (NQ + 7) / 8, KM = (NP + 3) / 4;
-    constexpr int CTU = (EPB * 4 + 7) / 8, CTD = (EPB + 7) / 8;
-    constexpr int NWK = NT / 32;
-    const int lane = tid & 31, warp = tid >> 5;
-    const int ar = lane >> 2, ak = lane & 3;
-    const int ntask = RQ * (CTU + 3 * CTD);
-    for (int task = warp; task < ntask; task += NWK) {
-      int rt, ct, op;              // op: 0 = V (columns (e, f)), 1..3 = D3_c (columns e)
-      if (task < RQ * CTU) { op = 0; rt = task / CTU; ct = task - rt * CTU; }
-      else { const int t2 = task - RQ * CTU; op = 1 + t2 / (RQ * CTD);
-             const int r2 = t2 - (op - 1) * RQ * CTD; rt = r2 / CTD; ct = r2 - rt * CTD; }
-      const R* A = wcst + (size_t)op * NP * NQ;        // [m][qp]
-      const int qa = rt * 8 + ar;                      // A row of this lane
-      const int bcol = ct * 8 + ar;                    // B column of this lane
-      const int be = op == 0 ? bcol >> 2 : bcol, bf = op == 0 ? (bcol & 3) : 0;
-      double c0 = 0.0, c1 = 0.0;
+    // trial pass at the volume cubature points: w grad p (incl. the
+    // -p grad J / 2J term), w G u, w gJfac . u (hybridwave/dg.py:430-443)
+    for (int i = tid; i < ne * W8::NQ; i += NT) {
+      const int e = i / W8::NQ, qp = i - e * W8::NQ;
+      const R* qe = sq + e * 4 * NP;
+      R U[4] = {R(0), R(0), R(0), R(0)}, dc[3] = {R(0), R(0), R(0)};
 #pragma unroll 2
-      for (int ks = 0; ks < KM; ++ks) {
-        const int m = ks * 4 + ak;
-        const double a = (qa < NQ && m < NP) ? double(ldg(A + (size_t)m * NQ + qa)) : 0.0;
-        const double b = (be < ne && m < NP) ? double(sq[be * 4 * NP + bf * NP + m]) : 0.0;
-        dmma884(c0, c1, a, b);
+      for (int m = 0; m < NP; ++m) {
+        const R v = ldg(wcst + m * W8::NQ + qp), pm = qe[m];
+        U[0] += v * pm;
+        U[1] += v * qe[NP + m];
+        U[2] += v * qe[2 * NP + m];
+        U[3] += v * qe[3 * NP + m];
+        dc[0] += ldg(wcst + (NP + m) * W8::NQ + qp) * pm;
+        dc[1] += ldg(wcst + (2 * NP + m) * W8::NQ + qp) * pm;
+        dc[2] += ldg(wcst + (3 * NP + m) * W8::NQ + qp) * pm;
       }
-      const int qp = rt * 8 + ar;
-#pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const int col = ct * 8 + ak * 2 + i;
-        const int e = op == 0 ? col >> 2 : col, slot = op == 0 ? (col & 3) : 3 + op;
-        if (qp < NQ && e < ne) cs[e * W8::CS + slot * NQ + qp] = R(i ? c1 : c0);
-      }
-    }
-    __syncthreads();
-    // w grad p (incl. the -p grad J / 2J term), w G u, w gJfac . u at each
-    // point (hybridwave/dg.py:430-443), in place over the trial values
-    for (int i = tid; i < ne * NQ; i += NT) {
-      const int e = i / NQ, qp = i - e * NQ;
-      R* c = cs + e * W8::CS + qp;
-      const R U[4] = {c[0], c[NQ], c[2 * NQ], c[3 * NQ]};
-      const R dc[3] = {c[4 * NQ], c[5 * NQ], c[6 * NQ]};
       const R* gq = wgeo + (size_t)sk[e] * W8::GW + qp * 12;
       R gl[12];
 #pragma unroll
       for (int r = 0; r < 12; ++r) gl[r] = ldg(gq + r);
+      R* c = cs + e * W8::CS + qp;
 #pragma unroll
       for (int x = 0; x < 3; ++x)
-        c[x * NQ] = gl[x] * dc[0] + gl[3 + x] * dc[1] + gl[6 + x] * dc[2] + gl[9 + x] * U[0];
+        c[x * W8::NQ] = gl[x] * dc[0] + gl[3 + x] * dc[1] + gl[6 + x] * dc[2] + gl[9 + x] * U[0];
 #pragma unroll
       for (int cc = 0; cc < 3; ++cc)
-        c[(3 + cc) * NQ] = gl[3 * cc] * U[1] + gl[3 * cc + 1] * U[2] + gl[3 * cc + 2] * U[3];
-      c[6 * NQ] = gl[9] * U[1] + gl[10] * U[2] + gl[11] * U[3];
-    }
-    __syncthreads();
-    // test pass: R_u = -V^T (w grad p), R_p = sum_c D3_c^T (w G u)_c +
-    // V^T (w gJ . u): rows = nodes, k = cubature points, columns = elements
-    {
-      constexpr int RN = (NP + 7) / 8, KQ = (NQ + 3) / 4;
-      const R* vn = wcst + W8::CVN;                    // [op][qp][m]
-      const int nt2 = RN * CTD * 4;
-      for (int task = warp; task < nt2; task += NWK) {
-        const int fo = task % 4, r2 = task / 4, rt = r2 / CTD, ct = r2 - rt * CTD;
-        const int na = rt * 8 + ar, be = ct * 8 + ar;
-        double c0 = 0.0, c1 = 0.0;
-        // field u_x: one GEMM (V^T, slot x); field p: D3_c^T slots 3..5, V^T slot 6
-        const int ng = fo == 0 ? 4 : 1;
-        for (int g = 0; g < ng; ++g) {
-          const int opi = fo == 0 ? (g < 3 ? 1 + g : 0) : 0;
-          const int slot = fo == 0 ? 3 + g : fo - 1;
-          const R* A = vn + (size_t)opi * NQ * NP;
-#pragma unroll 2
-          for (int ks = 0; ks < KQ; ++ks) {
-            const int qp = ks * 4 + ak;
-            const double a = (na < NP && qp < NQ) ? double(ldg(A + (size_t)qp * NP + na)) : 0.0;
-            const double b = (be < ne && qp < NQ) ? double(cs[be * W8::CS + slot * NQ + qp]) : 0.0;
-            dmma884(c0, c1, a, b);
-          }
-        }
-        const double sgn = fo == 0 ? 1.0 : -1.0;
-#pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          const int e = ct * 8 + ak * 2 + i;
-          if (na < NP && e < ne) rs[(e * 4 + fo) * NP + na] = R(sgn * (i ? c1 : c0));
-        }
-      }
+        c[(3 + cc) * W8::NQ] = gl[3 * cc] * U[1] + gl[3 * cc + 1] * U[2] + gl[3 * cc + 2] * U[3];
+      c[6 * W8::NQ] = gl[9] * U[1] + gl[10] * U[2] + gl[11] * U[3];
     }
   }
 
@@ -605,8 +543,21 @@ __global__ void __launch_bounds__(NT) dense_kernel(hw_mesh_t M, hw_fields_t Q, E
 #pragma unroll
     for (int c = 0; c < 4; ++c) acc[s][c] = R(0);
     if (T == HW_WEDGE && naw && e < ne) {
-#pragma unroll
-      for (int c = 0; c < 4; ++c) acc[s][c] = rs[(e * 4 + c) * NP + n];   // DMMA test pass
+      // test pass: R_u = -V^T (w grad p), R_p = sum_c D3_c^T (w G u)_c + V^T (w gJ . u)
+      const R* vn = wcst + W8::CVN;
+      const R* c = cs + e * W8::CS;
+      R a0 = R(0), a1 = R(0), a2 = R(0), a3 = R(0);
+#pragma unroll 2
+      for (int qp = 0; qp < W8::NQ; ++qp) {
+        const R v = ldg(vn + qp * NP + n), dr = ldg(vn + (W8::NQ + qp) * NP + n),
+                ds = ldg(vn + (2 * W8::NQ + qp) * NP + n), dt = ldg(vn + (3 * W8::NQ + qp) * NP + n);
+        a1 -= v * c[qp];
+        a2 -= v * c[W8::NQ + qp];
+        a3 -= v * c[2 * W8::NQ + qp];
+        a0 += dr * c[3 * W8::NQ + qp] + ds * c[4 * W8::NQ + qp] + dt * c[5 * W8::NQ + qp] +
+              v * c[6 * W8::NQ + qp];
+      }
+      acc[s][0] = a0; acc[s][1] = a1; acc[s][2] = a2; acc[s][3] = a3;
     } else if (e < ne) {
       R div = R(0), dp0 = R(0), dp1 = R(0), dp2 = R(0);
       const R* p = sq + e * 4 * NP;

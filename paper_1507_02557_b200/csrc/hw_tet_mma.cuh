@@ -24,6 +24,11 @@
 
 namespace hw {
 
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
 
 __host__ __device__ constexpr int stride4mod16(int n) {   // smallest s >= n, s = 4 (mod 16)
   return n + ((4 - n % 16) + 16) % 16;
