@@ -641,8 +641,10 @@ static int launch_energy(const hw_mesh_t& M, const hw_fields_t& Q, double* out,
   for (int t = 0; t < HW_NTYPES; ++t) {
     const int64_t K = M.t[t].K;
     if (K <= 0) continue;
-    const int64_t items = K * np_of(t, N);
-    const unsigned g = grid_for(items);
+    // one warp per element, 8 per block
+    int64_t gb = (K + 7) / 8;
+    if (gb > 148 * 16) gb = 148 * 16;
+    const unsigned g = (unsigned)(gb > 0 ? gb : 1);
     switch (t) {
       case HW_HEX: energy_kernel<N, HW_HEX, R><<<g, 256, 0, st>>>(M, Q, out, K); break;
       case HW_WEDGE: energy_kernel<N, HW_WEDGE, R><<<g, 256, 0, st>>>(M, Q, out, K); break;

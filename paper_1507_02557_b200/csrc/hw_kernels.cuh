@@ -1239,59 +1239,89 @@ __global__ void HW_HEX_BOUNDS hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi E,
 template <int N, int T, typename R>
 __global__ void __launch_bounds__(256) energy_kernel(hw_mesh_t M, hw_fields_t Q, double* out,
                                                      int64_t K) {
+  // one warp per element (lanes over the nodes: coalesced state reads, the
+  // element's record and material read once); tets stage the element rows
+  // in shared memory for (M_ref u)_n with M_ref resident per block
   using X = TT<N, T>;
   using D = Dims<N>;
-  constexpr int NP = X::NP;
+  constexpr int NP = X::NP, NW = 8;
   const hw_type_t& TY = M.t[T];
   const R* q = (const R*)Q.p[T];
   const R* geo = (const R*)TY.geo;
   const R* mat = (const R*)TY.mat;
+  constexpr bool SMEM_M = T == HW_TET && NP * NP <= 4096;   // N <= 5: M_ref in smem
+  __shared__ double sM[SMEM_M ? NP * NP : 1];
+  __shared__ double sqe[(T == HW_TET) ? NW * 4 * NP : 1];
+  __shared__ double sw1[D::N1];
+  if (SMEM_M)
+    for (int i = threadIdx.x; i < NP * NP; i += blockDim.x) sM[i] = (double)ldg((const R*)TY.op[4] + i);
+  if (T == HW_HEX && threadIdx.x < D::N1) sw1[threadIdx.x] = (double)ldg((const R*)TY.op[2] + threadIdx.x);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double acc = 0.0;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < K * NP;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t e = i / NP;
-    const int n = (int)(i - e * NP);
+  for (int64_t e = (int64_t)blockIdx.x * NW + warp; e < K; e += (int64_t)gridDim.x * NW) {
     const R* qe = q + e * 4 * NP;
     const double wp = 1.0 / (double)mat[e * 4 + 0], wu = 1.0 / (double)mat[e * 4 + 1];
-    double w = 1.0;
+    const R* g = geo + e * X::GEO;
+    bool aff = true;
+    double we = 1.0;   // element-constant mass weight (J; wedge 1)
     if (T == HW_HEX) {
-      const R* g = geo + e * GEO_HEX;
-      const R* w1 = (const R*)TY.op[2];
-      const int a = n / (D::N1 * D::N1), b = (n / D::N1) % D::N1, c = n % D::N1;
-      double J;
-      if (g[HX_AFF] != R(0)) {
-        J = (double)g[HX_J];
-      } else {
-        const R* x1 = (const R*)TY.op[4];
-        R G[9];
-        J = (double)hex_metric<R>(g, x1[a], x1[b], x1[c], G);
-      }
-      w = (double)w1[a] * (double)w1[b] * (double)w1[c] * J;
+      aff = g[HX_AFF] != R(0);
+      if (aff) we = (double)g[HX_J];
+    } else if (T == HW_PYRAMID && g[PY_NAFF] != R(0)) {
+      aff = false;
     } else if (T != HW_WEDGE) {
-      const R* G = geo + e * X::GEO;
-      const double det = (double)G[0] * ((double)G[4] * G[8] - (double)G[5] * G[7]) -
-                         (double)G[1] * ((double)G[3] * G[8] - (double)G[5] * G[6]) +
-                         (double)G[2] * ((double)G[3] * G[7] - (double)G[4] * G[6]);
-      w = 1.0 / det;   // G = dr/dx: det G = 1/J
+      const double det = (double)g[0] * ((double)g[4] * g[8] - (double)g[5] * g[7]) -
+                         (double)g[1] * ((double)g[3] * g[8] - (double)g[5] * g[6]) +
+                         (double)g[2] * ((double)g[3] * g[7] - (double)g[4] * g[6]);
+      we = 1.0 / det;   // G = dr/dx: det G = 1/J
     }
-    double s = 0.0;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const double v = (double)qe[c * NP + n];
-      double mv = v;
-      if (T == HW_TET) {   // (M_ref u)_n
-        const R* Mr = (const R*)TY.op[4] + n * NP;
-        mv = 0.0;
-        for (int j = 0; j < NP; ++j) mv += (double)Mr[j] * (double)qe[c * NP + j];
+    double* sq = sqe + warp * 4 * NP;
+    if (T == HW_TET) {
+      for (int i = lane; i < 4 * NP; i += 32) sq[i] = (double)qe[i];
+      __syncwarp();
+    }
+    for (int n = lane; n < NP; n += 32) {
+      double w = we;
+      if (T == HW_HEX) {
+        const int a = n / (D::N1 * D::N1), b = (n / D::N1) % D::N1, c = n % D::N1;
+        double J = we;
+        if (!aff) {
+          const R* x1 = (const R*)TY.op[4];
+          R G[9];
+          J = (double)hex_metric<R>(g, x1[a], x1[b], x1[c], G);
+        }
+        w = sw1[a] * sw1[b] * sw1[c] * J;
+      } else if (T == HW_PYRAMID && !aff) {
+        w = (double)ldg((const R*)TY.op[8] + ((size_t)e * NP + n) * 10 + 9);   // J at the node
       }
-      s += (c == 0 ? wp : wu) * v * mv;
+      double s = 0.0;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        double v, mv;
+        if (T == HW_TET) {   // (M_ref u)_n
+          v = sq[c * NP + n];
+          mv = 0.0;
+          if constexpr (SMEM_M) {
+            for (int j = 0; j < NP; ++j) mv += sM[n * NP + j] * sq[c * NP + j];
+          } else {
+            const R* Mr = (const R*)TY.op[4] + n * NP;
+            for (int j = 0; j < NP; ++j) mv += (double)ldg(Mr + j) * sq[c * NP + j];
+          }
+        } else {
+          v = (double)qe[c * NP + n];
+          mv = v;
+        }
+        s += (c == 0 ? wp : wu) * v * mv;
+      }
+      acc += w * s;
     }
-    acc += w * s;
+    if (T == HW_TET) __syncwarp();
   }
   // block reduction
   __shared__ double red[32];
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  if (lane == 0) red[warp] = acc;
   __syncthreads();
   if (threadIdx.x < 32) {
     acc = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
