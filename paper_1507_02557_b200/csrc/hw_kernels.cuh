@@ -1277,11 +1277,28 @@ __global__ void __launch_bounds__(256) energy_kernel(hw_mesh_t M, hw_fields_t Q,
       we = 1.0 / det;   // G = dr/dx: det G = 1/J
     }
     double* sq = sqe + warp * 4 * NP;
+    constexpr int IT = (NP + 31) / 32;
+    double qv[IT][4];          // this lane's node values, all loads in flight at once
+#pragma unroll
+    for (int u = 0; u < IT; ++u) {
+      const int n = lane + 32 * u;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) qv[u][c] = n < NP ? (double)qe[c * NP + n] : 0.0;
+    }
     if (T == HW_TET) {
-      for (int i = lane; i < 4 * NP; i += 32) sq[i] = (double)qe[i];
+#pragma unroll
+      for (int u = 0; u < IT; ++u) {
+        const int n = lane + 32 * u;
+        if (n < NP)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) sq[c * NP + n] = qv[u][c];
+      }
       __syncwarp();
     }
-    for (int n = lane; n < NP; n += 32) {
+#pragma unroll
+    for (int u = 0; u < IT; ++u) {
+      const int n = lane + 32 * u;
+      if (n >= NP) break;
       double w = we;
       if (T == HW_HEX) {
         const int a = n / (D::N1 * D::N1), b = (n / D::N1) % D::N1, c = n % D::N1;
@@ -1299,8 +1316,8 @@ __global__ void __launch_bounds__(256) energy_kernel(hw_mesh_t M, hw_fields_t Q,
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         double v, mv;
+        v = qv[u][c];
         if (T == HW_TET) {   // (M_ref u)_n
-          v = sq[c * NP + n];
           mv = 0.0;
           if constexpr (SMEM_M) {
             for (int j = 0; j < NP; ++j) mv += sM[n * NP + j] * sq[c * NP + j];
@@ -1309,7 +1326,6 @@ __global__ void __launch_bounds__(256) energy_kernel(hw_mesh_t M, hw_fields_t Q,
             for (int j = 0; j < NP; ++j) mv += (double)ldg(Mr + j) * sq[c * NP + j];
           }
         } else {
-          v = (double)qe[c * NP + n];
           mv = v;
         }
         s += (c == 0 ? wp : wu) * v * mv;
