@@ -1320,9 +1320,11 @@ __global__ void __launch_bounds__(256) energy_kernel(hw_mesh_t M, hw_fields_t Q,
         if (T == HW_TET) {   // (M_ref u)_n
           mv = 0.0;
           if constexpr (SMEM_M) {
+#pragma unroll 5
             for (int j = 0; j < NP; ++j) mv += sM[n * NP + j] * sq[c * NP + j];
           } else {
             const R* Mr = (const R*)TY.op[4] + n * NP;
+#pragma unroll 5
             for (int j = 0; j < NP; ++j) mv += (double)ldg(Mr + j) * sq[c * NP + j];
           }
         } else {
