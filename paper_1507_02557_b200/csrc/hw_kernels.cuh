@@ -1236,6 +1236,14 @@ __global__ void HW_HEX_BOUNDS hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi E,
 // p / kappa + rho |u|^2, mass: hex w3 J (per node), tet J M_ref, pyramid J,
 // wedge identity (LSC basis).  One thread per (element, node); block sums
 // accumulate into out[T] with a double atomicAdd.
+// J of a trilinear hex at node (a, b, c) (out of line: the energy kernel's
+// unrolled node loop would otherwise inline one metric per node it holds)
+template <typename R>
+__device__ __noinline__ double hex_J_at(const R* g, const R* x1, int a, int b, int c) {
+  R G[9];
+  return (double)hex_metric<R>(g, x1[a], x1[b], x1[c], G);
+}
+
 template <int N, int T, typename R>
 __global__ void __launch_bounds__(256) energy_kernel(hw_mesh_t M, hw_fields_t Q, double* out,
                                                      int64_t K) {
@@ -1302,35 +1310,26 @@ __global__ void __launch_bounds__(256) energy_kernel(hw_mesh_t M, hw_fields_t Q,
       double w = we;
       if (T == HW_HEX) {
         const int a = n / (D::N1 * D::N1), b = (n / D::N1) % D::N1, c = n % D::N1;
-        double J = we;
-        if (!aff) {
-          const R* x1 = (const R*)TY.op[4];
-          R G[9];
-          J = (double)hex_metric<R>(g, x1[a], x1[b], x1[c], G);
-        }
+        const double J = aff ? we : hex_J_at<R>(g, (const R*)TY.op[4], a, b, c);
         w = sw1[a] * sw1[b] * sw1[c] * J;
       } else if (T == HW_PYRAMID && !aff) {
         w = (double)ldg((const R*)TY.op[8] + ((size_t)e * NP + n) * 10 + 9);   // J at the node
       }
       double s = 0.0;
+      if constexpr (T == HW_TET) {   // (M_ref u)_n for the four fields at once
+        double mv[4] = {0.0, 0.0, 0.0, 0.0};
+        const R* Mr = (const R*)TY.op[4] + n * NP;
+#pragma unroll 5
+        for (int j = 0; j < NP; ++j) {
+          const double m = SMEM_M ? sM[n * NP + j] : (double)ldg(Mr + j);
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        double v, mv;
-        v = qv[u][c];
-        if (T == HW_TET) {   // (M_ref u)_n
-          mv = 0.0;
-          if constexpr (SMEM_M) {
-#pragma unroll 5
-            for (int j = 0; j < NP; ++j) mv += sM[n * NP + j] * sq[c * NP + j];
-          } else {
-            const R* Mr = (const R*)TY.op[4] + n * NP;
-#pragma unroll 5
-            for (int j = 0; j < NP; ++j) mv += (double)ldg(Mr + j) * sq[c * NP + j];
-          }
-        } else {
-          mv = v;
+          for (int c = 0; c < 4; ++c) mv[c] += m * sq[c * NP + j];
         }
-        s += (c == 0 ? wp : wu) * v * mv;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) s += (c == 0 ? wp : wu) * qv[u][c] * mv[c];
+      } else {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) s += (c == 0 ? wp : wu) * qv[u][c] * qv[u][c];
       }
       acc += w * s;
     }
