@@ -850,14 +850,17 @@ __constant__ int c_hex_spc[2][8][6][4];
 #ifndef HW_HEX_NT
 #define HW_HEX_NT 128
 #endif
+// blocks per SM the register allocation must allow: fp64 N <= 4 is one
+// element per block, so 7 resident blocks (72 registers) keep 28 warps
+// in flight; the compiler's own choice for N = 4 is 76 (6 blocks)
 #ifndef HW_HEX_MINB
 #define HW_HEX_MINB 0
 #endif
-#if HW_HEX_MINB > 0
-#define HW_HEX_BOUNDS __launch_bounds__(HW_HEX_NT, HW_HEX_MINB)
-#else
-#define HW_HEX_BOUNDS __launch_bounds__(HW_HEX_NT)
-#endif
+template <int N, typename R>
+constexpr int hex_minb() {
+  return HW_HEX_MINB > 0 ? HW_HEX_MINB : ((sizeof(R) == 8 && N <= 4) ? 7 : 0);
+}
+#define HW_HEX_BOUNDS __launch_bounds__(HW_HEX_NT, (hex_minb<N, R>()))
 template <int N, typename R, bool SK = false>   // SK: skew form (testing hook)
 __global__ void HW_HEX_BOUNDS hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi E,
                                                  const int32_t* __restrict__ list,
@@ -974,7 +977,24 @@ __global__ void HW_HEX_BOUNDS hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi E,
   // here in the flux storage (written only after the volume pass)
   constexpr bool skew = SK;
   R* spre = sf;   // [e][c][node]
-  if (skew) {
+  static_assert(3 * NP <= 4 * NFP, "the volume scratch lives in the flux storage");
+  if (!skew) {
+    // affine elements: div u = sum_c d_c V_c with the contravariant velocity
+    // V_c = sum_x G[c][x] u_x (G constant), so the volume pass differentiates
+    // two quantities per direction (p, V_c) instead of four
+    for (int i = tid; i < ne * NP; i += NT) {
+      const int e = i / NP, n = i - e * NP;
+      const R* Xe = sg + e * GEO_HEX;
+      if (Xe[HX_AFF] == R(0)) continue;
+      const R* u = sq + e * 4 * NP + n;
+      const R u0 = u[NP], u1 = u[2 * NP], u2 = u[3 * NP];
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+        spre[(e * 3 + c) * NP + n] =
+            Xe[HX_G + 3 * c] * u0 + Xe[HX_G + 3 * c + 1] * u1 + Xe[HX_G + 3 * c + 2] * u2;
+    }
+    __syncthreads();
+  } else {
     for (int i = tid; i < ne * NP; i += NT) {
       const int e = i / NP, n = i - e * NP;
       const int ii = n / (N1 * N1), jj = (n / N1) % N1, kk = n % N1;
@@ -1007,6 +1027,28 @@ __global__ void HW_HEX_BOUNDS hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi E,
     minv[s] = R(0);
     if (e < ne) {
       const int ii = n / (N1 * N1), jj = (n / N1) % N1, kk = n % N1;
+      const R* Xe = sg + e * GEO_HEX;
+      if (!skew && Xe[HX_AFF] != R(0)) {
+        const R* u = sq + e * 4 * NP;
+        const R* V = spre + e * 3 * NP;
+        R a0 = R(0), a1 = R(0), a2 = R(0), div = R(0);
+#pragma unroll
+        for (int l = 0; l < N1; ++l) {
+          const R dr = sD[ii * N1 + l], ds = sD[jj * N1 + l], dt = sD[kk * N1 + l];
+          const int nr = (l * N1 + jj) * N1 + kk, ns = (ii * N1 + l) * N1 + kk,
+                    nt = (ii * N1 + jj) * N1 + l;
+          a0 += dr * u[nr];
+          a1 += ds * u[ns];
+          a2 += dt * u[nt];
+          div += dr * V[nr] + ds * V[NP + ns] + dt * V[2 * NP + nt];
+        }
+#pragma unroll
+        for (int x = 0; x < 3; ++x)
+          acc[s][1 + x] = -(Xe[HX_G + x] * a0 + Xe[HX_G + 3 + x] * a1 + Xe[HX_G + 6 + x] * a2);
+        acc[s][0] = -div;
+        minv[s] = siw1[ii] * siw1[jj] * siw1[kk] * Xe[HX_IJ];
+        continue;
+      }
       R d[4][3];
 #pragma unroll
       for (int f = 0; f < 4; ++f) {
@@ -1022,7 +1064,6 @@ __global__ void HW_HEX_BOUNDS hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi E,
       }
       R G[9];
       R iJ;
-      const R* Xe = sg + e * GEO_HEX;
       if (Xe[HX_AFF] != R(0)) {       // affine: constant metric from the record
 #pragma unroll
         for (int a = 0; a < 9; ++a) G[a] = Xe[HX_G + a];
