@@ -1227,9 +1227,15 @@ __global__ void HW_HEX_BOUNDS hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi E,
     // GL hex traces of the new state: one thread per (element, axis, line)
     // reads the line once and interpolates to both end faces of the axis;
     // into the (dead) own-trace rows, bulk-stored with the state rows
-    for (int it = tid; it < ne * 3 * NFQ; it += NT) {
-      const int e = it / (3 * NFQ), r = it - e * 3 * NFQ;
-      const int a = r / NFQ, uv = r - a * NFQ, u = uv / N1, v = uv - u * N1;
+    // (when the (element, axis) pairs fit one warp each, every warp takes
+    // one axis: its loads and its face-row stores then stay within one
+    // contiguous block of words, without the bank conflicts of a warp
+    // straddling two axes)
+    constexpr int LW = (NFQ > 16 && NFQ <= 32 && EPB * 3 * 32 <= NT) ? 32 : NFQ;
+    for (int it = tid; it < ne * 3 * LW; it += NT) {
+      const int e = it / (3 * LW), r = it - e * 3 * LW;
+      const int a = r / LW, uv = r - a * LW, u = uv / N1, v = uv - u * N1;
+      if (uv >= NFQ) continue;
       // base node (axis index 0) and stride along the axis
       const int ii = a == 0 ? 0 : u, jj = a == 0 ? u : (a == 1 ? 0 : v), kk = a == 2 ? 0 : v;
       const int base = (ii * N1 + jj) * N1 + kk;
