@@ -850,15 +850,16 @@ __constant__ int c_hex_spc[2][8][6][4];
 #ifndef HW_HEX_NT
 #define HW_HEX_NT 128
 #endif
-// blocks per SM the register allocation must allow: fp64 N <= 4 is one
-// element per block, so 7 resident blocks (72 registers) keep 28 warps
-// in flight; the compiler's own choice for N = 4 is 76 (6 blocks)
+// blocks per SM the register allocation must allow (fp64): 7 resident
+// blocks (72 registers) for N <= 3; N = 4 (one element per block) runs
+// best at 8 (64 registers, 60 B of spills: C4 hex 11.3 -> 11.0 ms; the
+// compiler's own choice is 76 registers, 6 blocks, 11.9 ms)
 #ifndef HW_HEX_MINB
 #define HW_HEX_MINB 0
 #endif
 template <int N, typename R>
 constexpr int hex_minb() {
-  return HW_HEX_MINB > 0 ? HW_HEX_MINB : ((sizeof(R) == 8 && N <= 4) ? 7 : 0);
+  return HW_HEX_MINB > 0 ? HW_HEX_MINB : ((sizeof(R) == 8 && N <= 4) ? (N == 4 ? 8 : 7) : 0);
 }
 #define HW_HEX_BOUNDS __launch_bounds__(HW_HEX_NT, (hex_minb<N, R>()))
 template <int N, typename R, bool SK = false>   // SK: skew form (testing hook)
