@@ -1,3 +1,4 @@
+# Default bench with its wall time, then the ncu launch list and one --set full C4 stage capture
 set -x
 mkdir -p gpurun_out/final
 t0=$(date +%s); python bench.py > gpurun_out/final/bench.json 2> gpurun_out/final/bench.err; t1=$(date +%s); echo "bench wall s: $((t1 - t0))" | tee gpurun_out/final/bench_wall.txt
