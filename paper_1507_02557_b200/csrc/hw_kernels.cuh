@@ -333,9 +333,8 @@ struct Smem {
   static constexpr int SMAT = SG + EPB * X::GEO;
   static constexpr int SOPS = SMAT + EPB * 4;   // hex: D1, x, w, Vend, 1/w
   static constexpr int TOTAL = SOPS + ((T == HW_HEX) ? (N + 1) * (N + 1) + 5 * (N + 1) : 0);
-  // ints: element ids, links (x2); hex: node -> face point table (6 x NP)
-  static constexpr size_t BYTES =
-      sizeof(R) * TOTAL + sizeof(int) * (2 * EPB * NF + EPB + ((T == HW_HEX) ? 24 : 0));
+  // ints: element ids, links (x2)
+  static constexpr size_t BYTES = sizeof(R) * TOTAL + sizeof(int) * (2 * EPB * NF + EPB);
 };
 
 template <int N, int T, typename R>
@@ -874,7 +873,6 @@ __global__ void HW_HEX_BOUNDS hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi E,
   R* sm = reinterpret_cast<R*>(smem_raw);
   int* sk = reinterpret_cast<int*>(sm + L::TOTAL);
   int* snc = sk + EPB;
-  int* spc = snc + 2 * EPB * 6;  // node -> face point: per face pt = c . (i, j, k, 1)
   R* sq = sm + L::SQ;
   R* sf = sm + L::SF;
   R* sg = sm + L::SG;
@@ -897,7 +895,6 @@ __global__ void HW_HEX_BOUNDS hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi E,
     siw1[tid] = R(1) / sw1[tid];
     sx[tid] = ldg((const R*)TY.op[4] + tid);
   }
-  (void)spc;
   if (tid < ne) sk[tid] = list ? list[w0 + tid] : (int)(w0 + tid);
   // TMA bulk copies of the element rows: every hex row (state, residual,
   // traces, record, material) is a multiple of 16 bytes, so each element
