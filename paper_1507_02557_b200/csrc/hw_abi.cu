@@ -897,7 +897,8 @@ int hw_wedge_face_correction(const hw_mesh_t* mesh, int elem_type, int n_pairs,
                              const double* P, int nq, int nfn, void* out, void* stream) {
   HW_DEVICE_GUARD(mesh);
   if (n_pairs <= 0) return 0;
-  if (elem_type != HW_TET) return fail("hw_wedge_face_correction: tets only");
+  if (elem_type != HW_TET && elem_type != HW_PYRAMID)
+    return fail("hw_wedge_face_correction: tets and pyramids only");
   if (!mesh->tr_in[HW_WEDGE]) return fail("hw_wedge_face_correction: no wedge traces");
   const int np = np_of(elem_type, mesh->N), nfp_w = [&] {
     const int N = mesh->N, nfn_ = (N + 1) * (N + 2) / 2, nfq = (N + 1) * (N + 1);

@@ -38,11 +38,6 @@ def _affine_check(disc, t, verts):
     from .refelem import affine_mask
     if t != "wedge" or len(verts) == 0 or affine_mask(t, verts, tol=1e-10).all():
         return False
-    nb = disc.mesh.nbr["wedge"][:, :2, 0]
-    if np.any(nb == 2):
-        raise NotImplementedError(
-            f"non-affine wedges with {int(np.sum(nb == 2))} triangle faces shared with "
-            "pyramids (no generator or test mesh has them; tets are supported, DESIGN.md)")
     return True
 
 
@@ -139,7 +134,7 @@ def wedge_face_corrections(disc, pack):
     wbase = disc.trace_bases["wedge"]
     gidx = np.asarray(disc.gather_idx)
     nfp_w = pack["types"]["wedge"]["nfp"]
-    for t, tid_faces in (("tet", range(4)),):
+    for t, tid_faces in (("tet", range(4)), ("pyramid", range(1, 5))):
         if t not in disc.types:
             continue
         nbr = disc.mesh.nbr[t]
@@ -606,7 +601,7 @@ class DeviceMesh:
                                                              dtype=dtype, device=self.device)
         self.struct = S
         self.set_traces(0, None)
-        # tet faces across non-affine wedge triangles (face-cubature correction)
+        # tet / pyramid faces across non-affine wedge triangles (face-cubature correction)
         self.corr = {}
         for t, c in wedge_face_corrections(disc, pack).items():
             self.corr[t] = {"n": int(len(c["idata"])), "nq": c["nq"], "nfn": c["nfn"],

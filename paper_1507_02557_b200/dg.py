@@ -385,7 +385,7 @@ class Discretization:
         return bool(self.device_mesh.corr)
 
     def apply_corrections(self, after_forcing=False):
-        """Extra-RHS rows of the tets across non-affine wedge triangles: the
+        """Extra-RHS rows of the tets / pyramids across non-affine wedge triangles: the
         reference's face-cubature integral minus the kernels' nodal lift
         (hw_wedge_face_correction) from the current input traces
         (mesh->tr_in), installed in the mesh's frc slots (accumulates onto a

@@ -494,3 +494,65 @@ def wedge_tet_columns_mesh(nx=4, ny=2, nz=2):
                 else:
                     tet.append(_orient_tets(c[kuhn].reshape(-1, 4), X))
     return HybridMesh(X, {"wedge": np.vstack(wed), "tet": np.vstack(tet)})
+
+
+def _orient_wedges(conn, X):
+    """Wedges (two triangles, corresponding corners) in the orientation of
+    _WEDGE_LOCAL's: flip both triangles where the sign differs."""
+    def sign(c):
+        v = X[c]
+        return np.sign(np.einsum("ij,ij->i", np.cross(v[:, 1] - v[:, 0], v[:, 2] - v[:, 0]),
+                                 v[:, 3] - v[:, 0]))
+    ref = REF_VERTS["hex"][_WEDGE_LOCAL[0]]
+    want = np.sign(np.dot(np.cross(ref[1] - ref[0], ref[2] - ref[0]), ref[3] - ref[0]))
+    conn = conn.copy()
+    bad = sign(conn) != want
+    conn[bad] = conn[bad][:, [0, 2, 1, 3, 5, 4]]
+    return conn
+
+
+def wedge_pyramid_columns_mesh(ny=2, jitter=0.0, seed=0):
+    """Test mesh (not in the reference): ny rows of four cells along x,
+    [pyramids | wedges | wedges | pyramids], one cell thick in z.  A
+    pyramid cell is the cube split into 3 pyramids with a common apex at a
+    corner on its wedge-side x-face, whose two triangles then meet the
+    wedge pair's triangles (the wedge diagonal goes through the apex corner;
+    rows alternate the apex's y side so the pyramid cells stay conforming).
+    jitter > 0 moves the vertices of the middle x-plane (shared by wedges
+    only): the wedges become non-affine, the pyramids stay affine."""
+    nx, nz = 4, 1
+    xs, ys, zs = np.linspace(0.0, 1.0, nx + 1), np.linspace(0.0, 1.0, ny + 1), np.array([0.0, 1.0 / ny])
+    gx, gy, gz = np.meshgrid(xs, ys, zs, indexing="ij")
+    X = np.column_stack([gx.transpose(2, 1, 0).ravel(), gy.transpose(2, 1, 0).ravel(),
+                         gz.transpose(2, 1, 0).ravel()])
+
+    def vid(i, j, k):
+        return (k * (ny + 1) + j) * (nx + 1) + i
+
+    hexf = FACES["hex"]
+    wed, pyr = [], []
+    for j in range(ny):
+        low = j % 2 == 0                 # apex (and wedge diagonal) on the row's low-y side
+        for i in range(nx):
+            c = np.array([vid(i, j, 0), vid(i + 1, j, 0), vid(i + 1, j + 1, 0),
+                          vid(i, j + 1, 0), vid(i, j, 1), vid(i + 1, j, 1),
+                          vid(i + 1, j + 1, 1), vid(i, j + 1, 1)])
+            if i in (1, 2):
+                # x-face diagonal (y_a, z0)-(y_b, z1): through local 0-7 (low) or 3-4
+                loc = _WEDGE_LOCAL if low else np.array([[3, 4, 0, 2, 5, 1], [3, 7, 4, 2, 6, 5]])
+                wed.append(c[loc])
+            else:
+                # apex corner: on the x-face towards the wedges, at z0 and the row's y side
+                xi = 1 if i == 0 else 0
+                apex_local = {(0, True): 0, (1, True): 1, (0, False): 3, (1, False): 2}[(xi, low)]
+                for f, (_, ix) in enumerate(hexf):
+                    if apex_local in ix:
+                        continue
+                    pyr.append(np.concatenate([c[list(ix)][::-1], [c[apex_local]]]))
+    wed = _orient_wedges(np.vstack(wed), X)
+    if jitter > 0:
+        rng = np.random.default_rng(seed)
+        mid = np.abs(X[:, 0] - xs[2]) < 1e-12
+        X = X.copy()
+        X[mid] += jitter / nx * rng.uniform(-1, 1, (int(mid.sum()), 3)) * np.array([1.0, 0.0, 0.0])
+    return HybridMesh(X, {"wedge": wed, "pyramid": np.array(pyr)})

@@ -114,8 +114,8 @@ class PartStepper:
         d = self.disc
         dev = d.device
         if d.device_mesh.corr:
-            raise NotImplementedError("partitioned runs of meshes with tets across non-affine "
-                                      "wedge triangles (single-GPU only)")
+            raise NotImplementedError("partitioned runs of meshes with tets / pyramids across "
+                                      "non-affine wedge triangles (single-GPU only)")
         self.S = Stepper(d, state_local, "lsrk")
         empty = torch.zeros(0, dtype=torch.int32, device=dev)
 
@@ -281,8 +281,8 @@ class PartMRAB:
         self.disc = d = Discretization(part.mesh, N, formulation, dtype=dtype, device=device)
         dev = d.device
         if d.device_mesh.corr:
-            raise NotImplementedError("partitioned runs of meshes with tets across non-affine "
-                                      "wedge triangles (single-GPU only)")
+            raise NotImplementedError("partitioned runs of meshes with tets / pyramids across "
+                                      "non-affine wedge triangles (single-GPU only)")
         self.L = L = int(n_levels)
         self.levels = {t: np.asarray(levels_local[t]) for t in d.types}
         self.q = d.to_device(state_local)

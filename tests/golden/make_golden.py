@@ -369,7 +369,39 @@ def wedge_tet_fixtures():
     print("wedge/tet fixtures written")
 
 
+def wedge_pyramid_fixtures():
+    """Non-affine (jittered) wedges whose triangle faces meet affine
+    pyramids: the reference's RHS and 10 LSRK-45 steps on the repo's
+    wedge_pyramid_columns_mesh (every number from the reference)."""
+    sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+    from paper_1507_02557_b200.mesh import wedge_pyramid_columns_mesh
+    from hybridwave.mesh import HybridMesh
+    fd = {}
+    g = wedge_pyramid_columns_mesh(2, 0.3, 1)
+    fd["X"] = g.vertices.copy()
+    for tag, N, form in [("n1_gl", 1, "GL"), ("n2_gl", 2, "GL"), ("n3_sem", 3, "SEM"),
+                         ("n3_gl", 3, "GL")]:
+        m = HybridMesh(g.vertices.copy(), {t: g.blocks[t].copy() for t in g.elem_types})
+        set_random_materials(m, 5)
+        d = Discretization(m, N, form)
+        rng = np.random.default_rng(N + 40)
+        st = {t: rng.standard_normal((d.n_elems[t], 4, d.ops[t].Np)) for t in d.types}
+        rhs = d.compute_rhs(st, 0.0)
+        for t in d.types:
+            fd[f"{tag}/rhs/{t}"] = rhs[t]
+        st0 = d.project(cavity_fields, 0.0)
+        dt = 0.5 * min(float(v.min()) for v in local_timesteps(d, 0.5).values())
+        lk = lsrk_run_ref(d, st0, dt, 10 * dt)
+        for t in d.types:
+            fd[f"{tag}/lsrk/{t}"] = lk[t]
+        fd[f"{tag}/dt"] = np.array(dt)
+    np.savez_compressed(os.path.join(HERE, "wedge_pyramid.npz"), **fd)
+    print("wedge/pyramid fixtures written")
+
+
 if __name__ == "__main__":
+    if sys.argv[1:] == ["wedge_pyramid"]:
+        sys.exit(wedge_pyramid_fixtures())
     if sys.argv[1:] == ["wedge_tet"]:
         sys.exit(wedge_tet_fixtures())
     if sys.argv[1:] == ["mrab_levels"]:

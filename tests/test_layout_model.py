@@ -133,3 +133,42 @@ def test_oracle_on_wedge_tet_mesh_matches_reference():
         rng = np.random.default_rng(N + 30)
         st = {t: rng.standard_normal((d.n_elems[t], 4, d.ops[t].Np)) for t in d.types}
         assert rel_err(oracle.compute_rhs(d, st), {t: Gw[f"{tag}/rhs/{t}"] for t in d.types}) < 1e-12
+
+
+def test_wedge_pyramid_mesh_corrections_cover_every_shared_triangle():
+    """Jittered wedges next to affine pyramids (wedge_pyramid_columns_mesh):
+    every pyramid triangle shared with a wedge gets a correction row; the
+    pyramids stay affine (DMMA kernel), the wedges take the cubature path."""
+    from paper_1507_02557_b200.device import wedge_face_corrections
+    from paper_1507_02557_b200.dg import Discretization
+    from paper_1507_02557_b200.mesh import HybridMesh, mesh_volume, wedge_pyramid_columns_mesh
+    from paper_1507_02557_b200.refelem import affine_mask
+    g = wedge_pyramid_columns_mesh(2, 0.3, 1)
+    X = load_golden("wedge_pyramid")["X"]
+    np.testing.assert_array_equal(g.vertices, X)
+    m = HybridMesh(X, g.blocks)
+    assert abs(mesh_volume(m) - 0.5) < 1e-12
+    assert not affine_mask("wedge", X[m.blocks["wedge"]], tol=1e-10).any()
+    assert affine_mask("pyramid", X[m.blocks["pyramid"]], tol=1e-10).all()
+    d = Discretization(m, 2, "GL")
+    pack = pack_mesh(d)
+    assert 8 in pack["types"]["wedge"]["op"] and 8 not in pack["types"]["pyramid"]["op"]
+    c = wedge_face_corrections(d, pack)
+    shared = int(np.sum(d.mesh.nbr["pyramid"][:, :, 0] == 1))
+    assert set(c) == {"pyramid"} and c["pyramid"]["idata"].shape[0] == shared == 8
+    assert set(c["pyramid"]["idata"][:, 1]) <= {1, 2, 3, 4}          # triangle faces only
+
+
+def test_oracle_on_wedge_pyramid_mesh_matches_reference():
+    from conftest import set_random_materials
+    from paper_1507_02557_b200.dg import Discretization
+    from paper_1507_02557_b200.mesh import HybridMesh, wedge_pyramid_columns_mesh
+    Gw = load_golden("wedge_pyramid")
+    g = wedge_pyramid_columns_mesh(2, 0.3, 1)
+    for tag, N, form in [("n1_gl", 1, "GL"), ("n3_sem", 3, "SEM")]:
+        m = HybridMesh(Gw["X"], g.blocks)
+        set_random_materials(m, 5)
+        d = Discretization(m, N, form, device="cpu")
+        rng = np.random.default_rng(N + 40)
+        st = {t: rng.standard_normal((d.n_elems[t], 4, d.ops[t].Np)) for t in d.types}
+        assert rel_err(oracle.compute_rhs(d, st), {t: Gw[f"{tag}/rhs/{t}"] for t in d.types}) < 1e-12
