@@ -384,23 +384,27 @@ class Discretization:
     def has_corrections(self):
         return bool(self.device_mesh.corr)
 
-    def apply_corrections(self, after_forcing=False):
+    def apply_corrections(self, after_forcing=False, rows=None, zero=True):
         """Extra-RHS rows of the tets / pyramids across non-affine wedge triangles: the
         reference's face-cubature integral minus the kernels' nodal lift
         (hw_wedge_face_correction) from the current input traces
         (mesh->tr_in), installed in the mesh's frc slots (accumulates onto a
-        forcing term set just before)."""
+        forcing term set just before).  rows: a subset of the correction
+        rows (partitioned runs apply the rows of ghost wedges after the halo
+        exchange); zero=False adds onto the rows already accumulated."""
         dm, L, st = self.device_mesh, nat.lib(), self.stream_ptr()
         if not dm.corr:
             return
         buf = self.forcing_buffer()
-        for t, c in dm.corr.items():
-            if not after_forcing:        # rows hold the last stage's values
+        if zero and not after_forcing:       # rows hold the last stage's values
+            for t, c in dm.corr.items():
                 buf[t].index_fill_(0, c["elems"], 0.0)
+        for t, c in (dm.corr if rows is None else rows).items():
             nat.check(L.hw_wedge_face_correction(dm.struct, TYPE_ID[t], c["n"],
                                                  c["idata"].data_ptr(), c["fdata"].data_ptr(),
                                                  c["L"].data_ptr(), c["P"].data_ptr(), c["nq"],
                                                  c["nfn"], buf[t].data_ptr(), st))
+        for t in dm.corr:
             dm.struct.frc[TYPE_ID[t]] = buf[t].data_ptr()
 
     def prepare_stage(self, time):

@@ -103,6 +103,23 @@ def flat_face_offsets(pairs, local, row):
     return np.concatenate([int(k) * row + local[int(f)] for k, f in pairs])
 
 
+def _split_corrections(dm, part):
+    """The face-correction rows (device.wedge_face_corrections) of a rank's
+    local mesh split by the wedge they read: (owned wedge, ghost wedge).  A
+    row of an interior element always reads an owned wedge."""
+    nfp_w = dm.pack["types"]["wedge"]["nfp"]
+    n_own = part.n_owned["wedge"]
+    own_rows, ghost_rows = {}, {}
+    for t, c in dm.corr.items():
+        wk = c["idata"][:, 2].long() // (4 * nfp_w)       # wedge of the row's first face node
+        for dst, m in ((own_rows, wk < n_own), (ghost_rows, wk >= n_own)):
+            n = int(m.sum())
+            if n:
+                dst[t] = {**c, "n": n, "idata": c["idata"][m].contiguous(),
+                          "fdata": c["fdata"][m].contiguous()}
+    return own_rows, ghost_rows
+
+
 class PartStepper:
     """LSRK-45 on one rank's local part (owned + ghost elements)."""
 
@@ -113,9 +130,10 @@ class PartStepper:
         self.disc = Discretization(part.mesh, N, formulation, dtype=dtype, device=device)
         d = self.disc
         dev = d.device
-        if d.device_mesh.corr:
-            raise NotImplementedError("partitioned runs of meshes with tets / pyramids across "
-                                      "non-affine wedge triangles (single-GPU only)")
+        # tets / pyramids across non-affine wedge triangles: correction rows
+        # of owned wedges before the interior launch, of ghost wedges after
+        # the halo (their traces) has arrived
+        self.corr_rows = _split_corrections(d.device_mesh, part) if d.device_mesh.corr else None
         self.S = Stepper(d, state_local, "lsrk")
         empty = torch.zeros(0, dtype=torch.int32, device=dev)
 
@@ -219,6 +237,8 @@ class PartStepper:
         handle, self._handle = self._handle, None
         tin = S.tr                      # input trace set of this stage
         S._stage_traces()
+        if self.corr_rows is not None:
+            d.apply_corrections(rows=self.corr_rows[0])
         nat.check(L.hw_lsrk_stage(dm.struct, F(S.q), F(S.q2), F(S.res), a, b, h,
                                   self.sub_interior, st))
         self.transport.wait(handle)
@@ -228,6 +248,8 @@ class PartStepper:
                 nat.check(L.hw_halo_scatter(dm.struct, self.recvbuf[peer][t].data_ptr(),
                                             self.fstride[t], off.data_ptr(), off.numel(),
                                             dst.data_ptr(), st))
+        if self.corr_rows is not None and self.corr_rows[1]:
+            d.apply_corrections(rows=self.corr_rows[1], zero=False)
         nat.check(L.hw_lsrk_stage(dm.struct, F(S.q), F(S.q2), F(S.res), a, b, h,
                                   self.sub_boundary, st))
 
@@ -281,8 +303,9 @@ class PartMRAB:
         self.disc = d = Discretization(part.mesh, N, formulation, dtype=dtype, device=device)
         dev = d.device
         if d.device_mesh.corr:
-            raise NotImplementedError("partitioned runs of meshes with tets / pyramids across "
-                                      "non-affine wedge triangles (single-GPU only)")
+            raise NotImplementedError("partitioned multi-rate runs of meshes with tets / "
+                                      "pyramids across non-affine wedge triangles (use "
+                                      "PartStepper or the single-GPU MRABDriver)")
         self.L = L = int(n_levels)
         self.levels = {t: np.asarray(levels_local[t]) for t in d.types}
         self.q = d.to_device(state_local)

@@ -461,3 +461,51 @@ def test_nonaffine_wedge_lsrk(spec, N, form, steps, native_lib):
     s = lsrk_run(d, st, dt, steps * dt)
     ref = oracle.lsrk_run(lambda q, tau: oracle.compute_rhs(d, q), st, dt, steps * dt)
     assert _l2rel(s, ref) < 1e-10
+
+
+@pytest.mark.parametrize("mesh_name,nparts,method", [("wedge_tet", 2, "xslab"),
+                                                     ("wedge_tet", 3, "rcb"),
+                                                     ("wedge_pyramid", 2, "rcb")])
+def test_partitioned_lsrk_loopback_face_corrections(mesh_name, nparts, method, native_lib):
+    """Partitioned LSRK on meshes whose tets / pyramids meet non-affine wedge
+    triangles: the correction rows of ghost wedges run after the halo
+    exchange; equal to the single-GPU run to rounding."""
+    from paper_1507_02557_b200 import mesh as M
+    from paper_1507_02557_b200.dg import Discretization
+    from paper_1507_02557_b200.parallel import LoopbackTransport, PartStepper, make_parts
+    from paper_1507_02557_b200.timeint import LSRK_A, LSRK_B, Stepper
+    from conftest import load_golden, set_random_materials
+    g = (M.wedge_tet_columns_mesh(4, 2, 2) if mesh_name == "wedge_tet"
+         else M.wedge_pyramid_columns_mesh(2, 0.3, 1))
+    m = M.HybridMesh(load_golden(mesh_name)["X"], g.blocks)
+    set_random_materials(m, 4)
+    N, h = 2, 1e-3
+    d = Discretization(m, N, "GL")
+    assert d.has_corrections
+    rng = np.random.default_rng(3)
+    st = {t: rng.standard_normal((d.n_elems[t], 4, d.ops[t].Np)) for t in d.types}
+    S = Stepper(d, st, "lsrk")
+    for _ in range(3):
+        S.lsrk_step(h)
+    ref = {t: S.q[t].cpu().numpy() for t in d.types}
+    parts = make_parts(m, nparts, method, N=N)
+    T = LoopbackTransport()
+    ps = [PartStepper(p, N, "GL", {t: st[t][p.global_ids[t]] for t in p.types}, T)
+          for p in parts]
+    n_ghost_rows = sum(c["n"] for p in ps if p.corr_rows for c in p.corr_rows[1].values())
+    if mesh_name == "wedge_tet" and method == "xslab":
+        assert n_ghost_rows > 0            # the cut runs between a tet and a wedge column
+    for _ in range(3):
+        for a, b in zip(LSRK_A, LSRK_B):
+            for p in ps:
+                p.begin()
+            for p in ps:
+                p.finish(a, b, h)
+            for p in ps:
+                p.swap()
+    for p in ps:
+        own = p.owned_state()
+        for t in p.disc.types:
+            g_ = p.part.global_ids[t][:p.part.n_owned[t]]
+            r_ = ref[t][g_]
+            assert np.abs(own[t].cpu().numpy() - r_).max() <= 1e-12 * np.abs(r_).max()
