@@ -302,10 +302,6 @@ class PartMRAB:
         self.transport = transport
         self.disc = d = Discretization(part.mesh, N, formulation, dtype=dtype, device=device)
         dev = d.device
-        if d.device_mesh.corr:
-            raise NotImplementedError("partitioned multi-rate runs of meshes with tets / "
-                                      "pyramids across non-affine wedge triangles (use "
-                                      "PartStepper or the single-GPU MRABDriver)")
         self.L = L = int(n_levels)
         self.levels = {t: np.asarray(levels_local[t]) for t in d.types}
         self.q = d.to_device(state_local)
@@ -460,6 +456,8 @@ class PartMRAB:
         self.transport.wait(handle)
         dm.compute_traces(F(self.eff), 0, st, subset=self.trace_sub[tick])
         dm.set_traces(0, None)
+        if dm.corr:   # wedge face corrections from the effective state's traces (whole halo here)
+            d.apply_corrections()
         for lev in [lev for lev in range(1, L + 1) if tick % (2 ** (L - lev)) == 0]:
             self.n_hist[lev] = min(self.n_hist[lev] + 1, 3)
             self.steps[lev] += 1
