@@ -249,6 +249,16 @@ static int launch_traces_all(const hw_mesh_t& M, const hw_fields_t& Q, const hw_
   return 0;
 }
 
+template <int N, typename R, bool SK, bool SEM>
+static int launch_hex(const hw_mesh_t& M, const hw_fields_t& Q, const Epi& E,
+                      const int32_t* list, int64_t n, unsigned grid, cudaStream_t st) {
+  using L = Smem<N, HW_HEX, R, HW_HEX_NT>;
+  int rc;
+  if ((rc = set_smem(hex_kernel<N, R, SK, SEM>, L::BYTES))) return rc;
+  hex_kernel<N, R, SK, SEM><<<grid, HW_HEX_NT, L::BYTES, st>>>(M, Q, E, list, n);
+  return 0;
+}
+
 template <int N, typename R>
 static int launch_rhs_all(const hw_mesh_t& M, const hw_fields_t& Q, const Epi& E,
                           const hw_subset_t* sub, cudaStream_t st0) {
@@ -313,13 +323,12 @@ static int launch_rhs_all(const hw_mesh_t& M, const hw_fields_t& Q, const Epi& E
       case HW_HEX: {
         using L = Smem<N, HW_HEX, R, HW_HEX_NT>;
         const unsigned grid = (unsigned)((n + L::EPB - 1) / L::EPB);
-        if (M.t[HW_HEX].form == HW_FORM_SKEW) {
-          if ((rc = set_smem(hex_kernel<N, R, true>, L::BYTES))) return rc;
-          hex_kernel<N, R, true><<<grid, HW_HEX_NT, L::BYTES, st>>>(M, Q, E, list, n);
-        } else {
-          if ((rc = set_smem(hex_kernel<N, R, false>, L::BYTES))) return rc;
-          hex_kernel<N, R, false><<<grid, HW_HEX_NT, L::BYTES, st>>>(M, Q, E, list, n);
-        }
+        const bool skew = M.t[HW_HEX].form == HW_FORM_SKEW, sem = M.formulation == HW_SEM;
+        if (skew && sem) rc = launch_hex<N, R, true, true>(M, Q, E, list, n, grid, st);
+        else if (skew) rc = launch_hex<N, R, true, false>(M, Q, E, list, n, grid, st);
+        else if (sem) rc = launch_hex<N, R, false, true>(M, Q, E, list, n, grid, st);
+        else rc = launch_hex<N, R, false, false>(M, Q, E, list, n, grid, st);
+        if (rc) return rc;
         rc = check_launch("hex_kernel");
         break;
       }

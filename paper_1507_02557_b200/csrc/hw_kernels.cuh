@@ -861,7 +861,10 @@ constexpr int hex_minb() {
   return HW_HEX_MINB > 0 ? HW_HEX_MINB : ((sizeof(R) == 8 && N <= 4) ? (N == 4 ? 8 : 7) : 0);
 }
 #define HW_HEX_BOUNDS __launch_bounds__(HW_HEX_NT, (hex_minb<N, R>()))
-template <int N, typename R, bool SK = false>   // SK: skew form (testing hook)
+// SK: skew form (testing hook); SEM: GLL (spectral-element) nodes, a
+// template parameter so the face-point map is compile-time constant-bank
+// operands and the formulation branches fold away
+template <int N, typename R, bool SK = false, bool SEM = false>
 __global__ void HW_HEX_BOUNDS hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi E,
                                                  const int32_t* __restrict__ list,
                                                  int64_t nwork) {
@@ -884,7 +887,7 @@ __global__ void HW_HEX_BOUNDS hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi E,
   R* siw1 = sve + 2 * N1;        // 1 / w (1-D)
 
   const hw_type_t& TY = M.t[HW_HEX];
-  const bool sem = M.formulation == HW_SEM;
+  constexpr bool sem = SEM;
   const int tid = threadIdx.x;
   const int64_t w0 = (int64_t)blockIdx.x * EPB;
   const int ne = (int)((nwork - w0) < EPB ? (nwork - w0) : EPB);
@@ -1184,7 +1187,7 @@ __global__ void HW_HEX_BOUNDS hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi E,
       } else {
         w = sve[end * N1 + l];
       }
-      const int* cf = c_hex_spc[M.formulation][N][f];
+      const int* cf = c_hex_spc[SEM ? 1 : 0][N][f];
       const int pt = cf[0] * idx[0] + cf[1] * idx[1] + cf[2] * idx[2] + cf[3];
       const R* o = fl + f * NFQ + pt;
 #pragma unroll
@@ -1254,7 +1257,7 @@ __global__ void HW_HEX_BOUNDS hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi E,
 #pragma unroll
       for (int end = 0; end < 2; ++end) {
         const int f = 2 * a + end;
-        const int* cf = c_hex_spc[M.formulation][N][f];
+        const int* cf = c_hex_spc[SEM ? 1 : 0][N][f];
         const int pt = cf[0] * ii + cf[1] * jj + cf[2] * kk + cf[3];
 #pragma unroll
         for (int c = 0; c < 4; ++c) o[c * NFP + f * NFQ + pt] = end ? t1[c] : t0[c];
