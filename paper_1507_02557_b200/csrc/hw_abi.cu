@@ -254,8 +254,13 @@ static int launch_hex(const hw_mesh_t& M, const hw_fields_t& Q, const Epi& E,
                       const int32_t* list, int64_t n, unsigned grid, cudaStream_t st) {
   using L = Smem<N, HW_HEX, R, HW_HEX_NT>;
   int rc;
-  if ((rc = set_smem(hex_kernel<N, R, SK, SEM>, L::BYTES))) return rc;
-  hex_kernel<N, R, SK, SEM><<<grid, HW_HEX_NT, L::BYTES, st>>>(M, Q, E, list, n);
+  if (E.mode == MODE_LSRK) {
+    if ((rc = set_smem(hex_kernel<N, R, SK, SEM, true>, L::BYTES))) return rc;
+    hex_kernel<N, R, SK, SEM, true><<<grid, HW_HEX_NT, L::BYTES, st>>>(M, Q, E, list, n);
+  } else {
+    if ((rc = set_smem(hex_kernel<N, R, SK, SEM, false>, L::BYTES))) return rc;
+    hex_kernel<N, R, SK, SEM, false><<<grid, HW_HEX_NT, L::BYTES, st>>>(M, Q, E, list, n);
+  }
   return 0;
 }
 

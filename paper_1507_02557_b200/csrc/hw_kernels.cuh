@@ -864,7 +864,8 @@ constexpr int hex_minb() {
 // SK: skew form (testing hook); SEM: GLL (spectral-element) nodes, a
 // template parameter so the face-point map is compile-time constant-bank
 // operands and the formulation branches fold away
-template <int N, typename R, bool SK = false, bool SEM = false>
+// LS: the LSRK stage epilogue (E.mode == MODE_LSRK) compiled in alone
+template <int N, typename R, bool SK = false, bool SEM = false, bool LS = false>
 __global__ void HW_HEX_BOUNDS hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi E,
                                                  const int32_t* __restrict__ list,
                                                  int64_t nwork) {
@@ -904,7 +905,7 @@ __global__ void HW_HEX_BOUNDS hex_kernel(hw_mesh_t M, hw_fields_t Q, Epi E,
   // (of a subset list too) is one copy per array.  Group 0: volume inputs;
   // group 1: own traces (GL) and the LSRK residual, waited for by the flux.
   __shared__ __align__(8) uint64_t tbar[2];
-  const bool lsrk = E.mode == MODE_LSRK;
+  constexpr bool lsrk = LS;
   if (tid == 0) {
     mbar_init(&tbar[0], 1);
     mbar_init(&tbar[1], 1);
